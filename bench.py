@@ -1,0 +1,353 @@
+"""Benchmark: Arnoldi iterations/s of one-sync MGS-CWY GMRES(50) on the 3D
+7-point Laplacian (BASELINE.json config 2: 256^3, n = 16.7M) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+A step is one GMRES(50) restart cycle = 50 Arnoldi iterations (SpMV + K1
+one-pass [Q^T u, Q^T w] + K5 small state + K2 lagged update, then the
+cycle's least squares, x update and restart residual), all resident in HBM.
+`value` = whole-job iterations/s, device-timed with CUDA events; `e2e` = the
+same metric through the public drop-in call `solve(A, b_host, ...)` with the
+host->device copy of b and the device->host copy of x inside each step.
+
+--gpus N > 1 (torchrun) runs the row-partitioned (z-slab) solve with one
+NCCL all-gather per iteration plus the halo exchange; per-GPU slab fixed at
+256^3 (weak scaling; N=8 is the 512^3 cube of config 4).
+
+--impl reference times the reference algorithm on the host cores: the
+numpy oracle port (oracle/lowsync_oracle.py, same numpy/OpenBLAS calls as
+lowsync), a bounded sample of the same workload per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Arnoldi iters/sec (n=16.7M, m=50); ortho HBM GB/s vs peak; 1/2/4/8 B200"
+UNIT = "Arnoldi iterations/s"
+N_SLAB = 256
+M = 50
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _dims(n_gpus):
+    """Global grid for N GPUs: 256^3 per GPU, doubling x, y, z in turn
+    (N=8 -> 512^3 = config 4); slabs along z."""
+    nx = ny = nz = N_SLAB
+    k = 0
+    g = n_gpus
+    while g > 1:
+        if k % 3 == 0:
+            nx *= 2
+        elif k % 3 == 1:
+            ny *= 2
+        else:
+            nz *= 2
+        g //= 2
+        k += 1
+    return nx, ny, nz
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU side
+def cpu_sample(iters, threads=None):
+    """The reference algorithm (numpy oracle port) on the host cores: the
+    first `iters` Arnoldi iterations of the same C2 solve; solve time only."""
+    threads = threads or os.cpu_count()
+    os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
+    from oracle import lowsync_oracle as orc
+    A = orc.laplace3d(N_SLAB)
+    b = orc.rhs_random(A.n_rows, 42)
+    t0 = time.perf_counter()
+    run = orc.gmres(A, b, "one_sync_mgs", M, 1, 1e-14, max_iters=iters)
+    dt = time.perf_counter() - t0
+    assert len(run.curve) == iters
+    return iters / dt, dt, threads
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    per_step = 2
+    # warm-up steps are real work too (bounded); then time `steps`
+    from oracle import lowsync_oracle as orc
+    threads = os.cpu_count()
+    os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
+    A = orc.laplace3d(N_SLAB)
+    b = orc.rhs_random(A.n_rows, 42)
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        run = orc.gmres(A, b, "one_sync_mgs", M, 1, 1e-14, max_iters=per_step)
+        dt = time.perf_counter() - t0
+        assert len(run.curve) == per_step
+        if s >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = per_step * len(times) / tot
+    sample = (f"each step: prologue + first {per_step} Arnoldi iterations of one-sync GMRES(50) "
+              f"on 256^3 7-point (numpy oracle port, same numpy/OpenBLAS calls as lowsync); "
+              f"early iterations have small p, so this overstates the full-cycle rate")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "3D 7-point Laplacian 256^3 (n=16,777,216), one-sync MGS-CWY "
+                               "GMRES(50), seed-42 unit Gaussian b, x0=0", "n": A.n_rows, "m": M},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------- GPU side
+def _ortho_bytes(n, p, kind):
+    """Algorithmic HBM bytes per launch."""
+    if kind == "lagged_reduce":      # K1: reads Q (p cols, u = col p-1) and w
+        return 8 * n * (p + 1)
+    if kind == "lagged_update":      # K2: reads Q[:p-1], u, w; writes u, w
+        return 8 * n * (p + 3)
+    if kind == "spmv":               # K6 stencil: read x, write y
+        return 16 * n
+    return 0
+
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    import paper_1809_05805_b200 as P
+    from paper_1809_05805_b200 import _abi
+    from paper_1809_05805_b200.engine import Engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    comm = None
+    nx, ny, nz = _dims(world)
+    if world > 1:
+        from paper_1809_05805_b200.parallel import Comm, slab_problem
+        comm = Comm.init()
+        A_local, n_global = slab_problem((nx, ny, nz), comm)
+    else:
+        A_local = P.gen_laplace3d(N_SLAB)
+        n_global = A_local.n_rows
+    n = A_local.n_rows
+    rng = np.random.default_rng(42)
+    b_full = None
+    if world == 1:
+        b_full = rng.standard_normal(n)
+        b_full /= np.linalg.norm(b_full)
+        b_local = b_full
+    else:
+        from paper_1809_05805_b200.parallel import local_rhs
+        b_local = local_rhs((nx, ny, nz), comm, 42)
+
+    eng = Engine(A_local, M, "one_sync_mgs", 1e-14, comm=comm, use_graph=False,
+                 n_global=n_global)
+    eng.load(torch.as_tensor(b_local).cuda())
+    rep = eng.prologue()
+
+    timers = []
+    eng.timer = timers
+
+    def step():
+        r = eng.cycle()
+        assert r.stop_iter == _abi.NO_STOP, "bench cycles must run all m iterations"
+        return r
+
+    for _ in range(args.warmup):
+        step()
+    timers.clear()
+    torch.cuda.synchronize()
+    if comm is not None:
+        comm.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+    if comm is not None:
+        comm.barrier()
+    ms = ev0.elapsed_time(ev1)
+    if comm is not None:
+        ms = comm.max_scalar(ms)
+    iters = M * args.steps
+    value = iters / (ms / 1e3) * world     # weak scaling: N slabs per global iteration
+    # per-kernel device times (events around each launch in the timed region)
+    agg = {}
+    for name, p, e0, e1 in timers:
+        t = e0.elapsed_time(e1)
+        a = agg.setdefault(name, [0.0, 0, 0])
+        a[0] += t
+        a[1] += 1
+        a[2] += _ortho_bytes(n, p, name)
+    peak, peak_kind = _peaks()
+    kern = {}
+    for name, (t, cnt, byt) in agg.items():
+        kern[name] = {"ms_total": t, "launches": cnt, "ms_avg": t / cnt,
+                      "GBps": (byt / (t / 1e3) / 1e9) if byt and t > 0 else None}
+    dom = max(("lagged_reduce", "lagged_update"), key=lambda k: agg.get(k, [0])[0])
+    t_dom, c_dom, b_dom = agg[dom]
+    achieved = b_dom / (t_dom / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh)
+        traffic = tr.get(dom)
+    except Exception:
+        pass
+    ortho_t = agg["lagged_reduce"][0] + agg["lagged_update"][0]
+    ortho_b = agg["lagged_reduce"][2] + agg["lagged_update"][2]
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"3D 7-point Laplacian {nx}x{ny}x{nz} (n={n_global:,}), "
+                               "one-sync MGS-CWY GMRES(50), seed-42 unit Gaussian b, x0=0",
+                   "n_per_gpu": n, "m": M, "method": "one_sync_mgs",
+                   "step": "one GMRES(50) restart cycle = 50 Arnoldi iterations",
+                   "rel_tol": 1e-14, "l2": "inputs larger than L2 (basis 7.0 GB per GPU)",
+                   "partition": "z-slabs" if world > 1 else "none",
+                   "value_units": "global Arnoldi iterations/s x N (per-GPU slab 256^3)"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic,
+                     "bytes_per_launch_avg": b_dom / c_dom,
+                     "ortho_GBps": ortho_b / (ortho_t / 1e3) / 1e9,
+                     "ortho_frac": ortho_b / (ortho_t / 1e3) / 1e9 / peak},
+        "kernels": kern,
+        "gpu_launches": sum(v[1] for v in agg.values()),
+        "clocks": clk.summary(),
+    }
+    del eng
+    torch.cuda.empty_cache()
+    # e2e through the public API with host buffers (N=1)
+    if world == 1:
+        A = P.gen_laplace3d(N_SLAB)
+        cfg = P.GmresConfig(restart_m=M, max_restarts=1, rel_tol=1e-14, method="one_sync_mgs")
+        for _ in range(1):
+            x, h = P.solve(A, b_full, config=cfg, diagnostics_every=0)
+            h.release()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_steps = max(2, min(args.steps, 5))
+        for _ in range(e2e_steps):
+            x, h = P.solve(A, b_full, config=cfg, diagnostics_every=0)
+            assert h.iterations == M
+            h.release()
+        dt = time.perf_counter() - t0
+        result["e2e"] = {"value": M * e2e_steps / dt, "unit": UNIT,
+                         "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                         "steps": e2e_steps,
+                         "what": "solve(A, b_host) -> x_host, GmresConfig(50, 1 cycle)"}
+        if not args.no_cpu:
+            v, dt_cpu, thr = cpu_sample(args.cpu_iters)
+            result["cpu_baseline"] = {
+                "value": v, "unit": UNIT, "cores": thr, "kind": "port",
+                "sample": f"first {args.cpu_iters} Arnoldi iterations of the same 256^3 one-sync "
+                          f"GMRES(50) solve, numpy oracle port ({dt_cpu:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if comm is not None:
+        comm.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=8)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,261 @@
+/* liblsb200 -- B200 (sm_100a) kernels for the Arnoldi orthogonalization hot
+ * path of low-synchronization GMRES(m) (arXiv 1809.05805).
+ *
+ * C ABI only: plain pointers (device memory unless stated), 64-bit sizes,
+ * an opaque CUDA stream, an int status.  No torch or C++ types cross this
+ * boundary; the Python host layer (paper_1809_05805_b200/_abi.py) binds it
+ * with ctypes.  The reference package `lowsync` is pure numpy and has no
+ * FFI of its own; each entry point names the reference function (file:line
+ * under /root/reference/pkg/src/lowsync) whose arithmetic it replaces.
+ *
+ * Storage conventions
+ *   Krylov basis V : column j at V + j*ld (each column contiguous, like the
+ *                    reference's Fortran-order KrylovBasis, kernels.py:219);
+ *                    V and ld must be 16-byte aligned / even.
+ *   small matrices : R, T, L are cap x cap row-major; tri is (m+1) x m
+ *                    row-major; rot holds (c, s) pairs.
+ *   reductions     : deterministic -- per-CTA partials, then a fixed-order
+ *                    sum by the last CTA; bitwise reproducible run to run.
+ *   gating         : every cycle kernel takes (flags, it); once the solver
+ *                    has stopped at iteration d (flags->stop_iter == d), a
+ *                    kernel of iteration it > d returns immediately, so a
+ *                    whole restart cycle runs as one CUDA graph without host
+ *                    syncs.  Pass flags == NULL for ungated calls.
+ *
+ * All functions return 0 on success, LSB_E* otherwise.
+ */
+#ifndef LSB200_H
+#define LSB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSB_OK 0
+#define LSB_EINVAL 1      /* bad sizes / alignment                          */
+#define LSB_ECUDA 2       /* CUDA launch error (see lsb_last_error)         */
+#define LSB_ERANGE 3      /* p above the kernel's column limit              */
+
+/* status codes written to lsb_flags.status (mirrors gmres.py:58-61) */
+#define LSB_RUNNING 0
+#define LSB_CONVERGED 1          /* implicit residual <= target          */
+#define LSB_BREAKDOWN 2          /* HappyBreakdown inside the cycle      */
+#define LSB_STARTUP_BREAKDOWN 3  /* HappyBreakdown outside a solver loop */
+#define LSB_SINGULAR 4           /* SingularHessenberg in back-subst.    */
+
+#define LSB_NO_STOP 0x7fffffff
+
+/* Device-resident control block of one solve (one per rank). */
+typedef struct lsb_flags {
+  int32_t stop_iter;   /* LSB_NO_STOP while running; else last iteration   */
+  int32_t status;      /* LSB_RUNNING / LSB_CONVERGED / ...                 */
+  int32_t broke_iter;  /* iteration whose orthogonalization broke down, -1  */
+  int32_t k;           /* columns consumed by the cycle's least squares     */
+  int32_t nonfinite;   /* spmv produced NaN/Inf (kernels.py:271)            */
+  int32_t restart_ok;  /* restart residual already <= target               */
+  int32_t pad[2];
+} lsb_flags;
+
+/* slots of the device scalar block `scal` */
+#define LSB_S_BETA 0      /* deferred norm / r_diag of the current column   */
+#define LSB_S_TARGET 1    /* rel_tol * beta0 (gmres.py:479)                 */
+#define LSB_S_DENOM 2     /* beta0 or 1 (gmres.py:474)                      */
+#define LSB_S_RNORM 3     /* last true residual norm ||b - A x||            */
+#define LSB_S_RELTOL 4
+#define LSB_S_BTF 5       /* breakdown_tol_factor                           */
+#define LSB_S_AMAX 6      /* norm pass scratch                              */
+#define LSB_S_SSQ 7
+#define LSB_S_TOL 8       /* last breakdown tolerance (for HappyBreakdown)  */
+#define LSB_S_COUNT 16
+
+/* Reduction workspace: partial >= lsb_partial_len() doubles, counter >= 8
+ * zero-initialised uint32 (self-resetting), grid 0 = library default. */
+typedef struct lsb_workspace {
+  double* partial;
+  uint32_t* counter;
+  int32_t grid;
+  int32_t pad;
+} lsb_workspace;
+
+/* CSR matrix with 32-bit indices (the reference keeps int64,
+ * kernels.py:113-115; nnz < 2^31 here).  col_scale (optional) is a right
+ * Jacobi scaling applied to x before the products (gmres.py:121-126). */
+typedef struct lsb_csr {
+  int64_t n_rows, n_cols, nnz;
+  const int32_t* row_ptr;
+  const int32_t* col_idx;
+  const double* values;
+  const double* col_scale;
+  int64_t row0;          /* global index of local row 0 (row-block partition) */
+  int64_t x_lo;          /* x is indexed by (global col - x_lo)               */
+} lsb_csr;
+
+/* Constant-coefficient box stencil, row i = (iz*ny + iy)*nx + ix.
+ * Offsets MUST be listed in increasing linear offset (= CSR column order).
+ * halo_lo/halo_hi: 1 if x holds a ghost z-plane below/above the local slab
+ * at x[-nx*ny .. 0) / x[n .. n+nx*ny) (z-slab row partition), else the
+ * plane is a Dirichlet boundary. */
+#define LSB_MAX_OFF 27
+typedef struct lsb_stencil {
+  int32_t nx, ny, nz;
+  int32_t noff;
+  int32_t halo_lo, halo_hi;
+  int32_t dx[LSB_MAX_OFF], dy[LSB_MAX_OFF], dz[LSB_MAX_OFF];
+  double val[LSB_MAX_OFF];
+  const double* col_scale;   /* optional Jacobi scaling, same layout as x */
+} lsb_stencil;
+
+/* Everything one Arnoldi cycle touches (one rank). */
+typedef struct lsb_arnoldi {
+  double* V;            /* basis, cap columns of stride ld                 */
+  int64_t ld, n;        /* local rows                                      */
+  int64_t n_global;     /* global rows (breakdown tolerance uses sqrt(n))  */
+  int32_t cap, m;       /* basis capacity, restart length                  */
+  double* R;            /* cap*cap: R (upper); its columns hold Hbar       */
+  double* T;            /* cap*cap: compact-WY factor (mgs_lvl2)           */
+  double* L;            /* cap*cap: strictly lower Q^T Q (cgs2_lvl2)        */
+  double* rot;          /* 2*m Givens (c, s)                               */
+  double* g;            /* m+1 rotated rhs                                 */
+  double* tri;          /* (m+1)*m rotated triangle                        */
+  double* coef;         /* cap: projection coefficients c / r / h          */
+  double* coef2;        /* cap: second-pass s / least-squares y            */
+  double* G;            /* reduction result(s), see g_parts                */
+  int32_t g_parts;      /* number of rank partials stacked in G (1 = local) */
+  int32_t g_stride;     /* doubles between two rank partials               */
+  double* Gloc;         /* where this rank's local reduction is written    */
+  double* scal;         /* LSB_S_COUNT scalars                             */
+  double* res;          /* m+1 implicit residual norms |g[i]|              */
+  lsb_flags* flags;
+  lsb_workspace ws;
+} lsb_arnoldi;
+
+/* ---------------------------------------------------------------- info */
+const char* lsb_version(void);
+const char* lsb_last_error(void);
+int lsb_sm_count(void);
+int64_t lsb_partial_len(int32_t pmax);   /* doubles for lsb_workspace.partial */
+int32_t lsb_max_columns(void);           /* largest p one mdot launch takes   */
+
+/* ---------------------------------------------------------------- primitives
+ * (kernels.py:256-362)                                                     */
+
+/* y = A x (or y = b - A x when b != NULL), rows summed exactly as
+ * numpy add.reduceat (kernels.py:256-272): first product + pairwise(rest).
+ * Sets flags->nonfinite on NaN/Inf. */
+int lsb_spmv_csr(const lsb_csr* A, const double* x, const double* b, double* y,
+                 lsb_flags* flags, int32_t it, void* stream);
+int lsb_spmv_stencil(const lsb_stencil* S, const double* x, const double* b, double* y,
+                     lsb_flags* flags, int32_t it, void* stream);
+
+/* out = [X^T u, X^T w] as p x 2 row-major (w != NULL; mdot_pair,
+ * kernels.py:328-347) or out = X^T u (w == NULL; mass_inner_product /
+ * fused_mdot_norm / dot, kernels.py:275-325).  One pass over X. */
+int lsb_mdot(const double* X, int64_t ld, int64_t n, int32_t p, const double* u,
+             const double* w, double* out, const lsb_workspace* ws,
+             const lsb_flags* flags, int32_t it, void* stream);
+
+/* out = y + X alpha (maxpy, kernels.py:350-362); out may alias y.
+ * alpha_sign = -1 applies -alpha (cgs_iterated, gram_schmidt.py:138). */
+int lsb_maxpy(const double* y, const double* X, int64_t ld, int64_t n, int32_t p,
+              const double* alpha, int32_t alpha_sign, double* out,
+              const lsb_flags* flags, int32_t it, void* stream);
+
+/* out2[0] = max|x|, out2[1] = sum x^2 (local, deterministic). */
+int lsb_norm_partial(const double* x, int64_t n, double* out2, const lsb_workspace* ws,
+                     const lsb_flags* flags, int32_t it, void* stream);
+/* *out = ||x||_2 from nparts stacked (amax, ssq) pairs; if max|x| is outside
+ * [2^-450, 2^450] it re-reads x with an exact power-of-two scaling (local
+ * only, nparts == 1) -- the overflow-safe contract of norm2 (kernels.py:283-298). */
+int lsb_norm_finish(const double* parts, int32_t nparts, const double* x, int64_t n,
+                    double* out, const lsb_workspace* ws, const lsb_flags* flags,
+                    int32_t it, void* stream);
+
+/* out = x / (*s) elementwise (device scalar s; e.g. V.push(r / beta)). */
+int lsb_scale_div(const double* x, int64_t n, const double* s, double* out,
+                  const lsb_flags* flags, int32_t it, void* stream);
+
+/* ---------------------------------------------------------------- lagged kernels
+ * mgs_lvl2 (gram_schmidt.py:206-245) = lagged_reduce + mgs_lvl2_small +
+ * lagged_update; cgs2_lvl2 (gram_schmidt.py:248-280) = lagged_reduce +
+ * cgs2_lvl2_small_a + lagged_update + mdot(second pass) + cgs2_lvl2_small_b
+ * + lagged_correct.  `p` = j-1 columns in Q; u = V[:,p-1], w = V[:,p].   */
+
+/* Gloc = [Q^T u, Q^T w] (p x 2): _lagged_reduce (gram_schmidt.py:195-203). */
+int lsb_lagged_reduce(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream);
+
+/* Small-state update of the one-reduce MGS-CWY kernel: beta, breakdown test,
+ * R/T columns, c = T^T y (/beta).  givens_col > 0 also folds Hessenberg
+ * column givens_col-1 = R[0..givens_col, givens_col] into the Givens state
+ * and tests convergence (gmres.py:418-435). */
+int lsb_mgs_lvl2_small(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
+                       int32_t givens_col, void* stream);
+/* cgs2_lvl2 front: beta, breakdown, L row, r = (I - L - L^T) y (/beta). */
+int lsb_cgs2_lvl2_small_a(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
+                          int32_t givens_col, void* stream);
+/* cgs2_lvl2 back: s = sum of rank partials in G, R[:p,p] = r + s. */
+int lsb_cgs2_lvl2_small_b(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream);
+
+/* u <- u/beta; w <- (krylov_scale ? w/beta : w) - Q coef  (one pass). */
+int lsb_lagged_update(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
+                      void* stream);
+/* w <- w - Q coef2 (cgs2_lvl2 second projection, gram_schmidt.py:277). */
+int lsb_lagged_correct(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream);
+
+/* ---------------------------------------------------------------- direct kernels
+ * mgs_level1 (gram_schmidt.py:144-160) and cgs_iterated (118-141) acting in
+ * place on column `col` of V against Q = V[:, :p]. */
+
+/* Level-1 MGS pass k (0 <= k <= p): if k > 0, h_{k-1} = sum of rank
+ * partials in G -> coef[k-1] and z -= h_{k-1} q_{k-1} (two roundings, as
+ * numpy's `work -= h * q`); then if k < p, Gloc[0] = q_k . z, else
+ * Gloc[0..1] = (max|z|, sum z^2).  One pass over z. */
+int lsb_mgs1_pass(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t k, int32_t p,
+                  void* stream);
+/* Sum the p rank partials in G into coef (accumulate != 0: coef += s, and
+ * coef2 = s) -- the r_col bookkeeping of cgs_iterated. */
+int lsb_collect_coef(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t accumulate,
+                     void* stream);
+/* z <- z + Q (-coef2) and, when want_norm, Gloc[0..1] = (max|z|, sum z^2). */
+int lsb_cgs_project(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p,
+                    int32_t want_norm, void* stream);
+/* r_diag from the (amax, ssq) rank partials in G; breakdown test against
+ * coef[0..p); Hbar column (R[:, col]); Givens fold of column col-1;
+ * convergence. */
+int lsb_direct_small(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, void* stream);
+/* V[:, col] /= r_diag unless the column broke down. */
+int lsb_direct_normalize(const lsb_arnoldi* S, int32_t it, int32_t col, void* stream);
+
+/* ---------------------------------------------------------------- cycle control */
+/* Zero R/T/L/rot/tri/g, g[0] = scal[RNORM], flags -> running (gmres.py:392-395). */
+int lsb_cycle_begin(const lsb_arnoldi* S, void* stream);
+/* y = back-substitution of the rotated k x k triangle into coef2, k from
+ * flags (solve_least_squares, gmres.py:184-192). */
+int lsb_cycle_lsq(const lsb_arnoldi* S, void* stream);
+/* x <- x + Mi (V_k y)   (_extract, gmres.py:294-297); col_scale optional. */
+int lsb_cycle_extract(const lsb_arnoldi* S, double* x, const double* col_scale, void* stream);
+/* After the restart residual norm landed in scal[RNORM]:
+ * first != 0 : denom/target set from it (gmres.py:472-479);
+ * always     : flags->restart_ok = rnorm <= target. */
+int lsb_restart_check(const lsb_arnoldi* S, int32_t first, void* stream);
+
+/* Standalone Givens fold of Hessenberg column i (i+1 entries h, device) into
+ * (rot, g, tri) of a restart length m; *res_out = |g[i]| (givens_update,
+ * gmres.py:153-177).  Same device code as the in-cycle fold. */
+int lsb_givens_update(double* rot, double* g, double* tri, int32_t m, const double* h, int32_t i,
+                      double* res_out, void* stream);
+/* y = back-substitution of the rotated k x k triangle (solve_least_squares,
+ * gmres.py:184-192); *status = -1, or the index of a zero diagonal. */
+int lsb_back_substitute(const double* tri, const double* g, int32_t m, int32_t k, double* y,
+                        int32_t* status, void* stream);
+
+/* ---------------------------------------------------------------- diagnostics */
+/* gram[row, 0..ncols) = V[:, :ncols]^T V[:, row] (measurement only). */
+int lsb_gram_row(const lsb_arnoldi* S, int32_t it, int32_t row, int32_t ncols, double* gram,
+                 int64_t gram_ld, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSB200_H */

@@ -1,0 +1,148 @@
+"""ctypes binding of liblsb200.so (include/lsb200.h).
+
+The library is the only compute path: if it is missing or cannot be loaded
+every entry point raises ``LsbUnavailable`` -- there is no CPU fallback.
+Structures below mirror the C structs field for field.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("LSB200_LIB", os.path.join(_HERE, "liblsb200.so"))
+
+OK, EINVAL, ECUDA, ERANGE = 0, 1, 2, 3
+RUNNING, CONVERGED, BREAKDOWN, STARTUP_BREAKDOWN, SINGULAR = 0, 1, 2, 3, 4
+NO_STOP = 0x7FFFFFFF
+
+# scalar slots (LSB_S_*)
+S_BETA, S_TARGET, S_DENOM, S_RNORM, S_RELTOL, S_BTF, S_AMAX, S_SSQ, S_TOL = range(9)
+S_COUNT = 16
+MAX_OFF = 27
+
+
+class LsbUnavailable(RuntimeError):
+    """liblsb200.so is not built / not loadable: no compute path exists."""
+
+
+class LsbError(RuntimeError):
+    """A liblsb200 entry point returned an error status."""
+
+
+class Flags(C.Structure):
+    _fields_ = [("stop_iter", C.c_int32), ("status", C.c_int32), ("broke_iter", C.c_int32),
+                ("k", C.c_int32), ("nonfinite", C.c_int32), ("restart_ok", C.c_int32),
+                ("pad", C.c_int32 * 2)]
+
+
+FLAGS_INTS = C.sizeof(Flags) // 4
+
+
+class Workspace(C.Structure):
+    _fields_ = [("partial", C.c_void_p), ("counter", C.c_void_p), ("grid", C.c_int32),
+                ("pad", C.c_int32)]
+
+
+class Csr(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64),
+                ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p),
+                ("col_scale", C.c_void_p), ("row0", C.c_int64), ("x_lo", C.c_int64)]
+
+
+class Stencil(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("noff", C.c_int32),
+                ("halo_lo", C.c_int32), ("halo_hi", C.c_int32),
+                ("dx", C.c_int32 * MAX_OFF), ("dy", C.c_int32 * MAX_OFF),
+                ("dz", C.c_int32 * MAX_OFF), ("val", C.c_double * MAX_OFF),
+                ("col_scale", C.c_void_p)]
+
+
+class Arnoldi(C.Structure):
+    _fields_ = [("V", C.c_void_p), ("ld", C.c_int64), ("n", C.c_int64), ("n_global", C.c_int64),
+                ("cap", C.c_int32), ("m", C.c_int32),
+                ("R", C.c_void_p), ("T", C.c_void_p), ("L", C.c_void_p),
+                ("rot", C.c_void_p), ("g", C.c_void_p), ("tri", C.c_void_p),
+                ("coef", C.c_void_p), ("coef2", C.c_void_p),
+                ("G", C.c_void_p), ("g_parts", C.c_int32), ("g_stride", C.c_int32),
+                ("Gloc", C.c_void_p), ("scal", C.c_void_p), ("res", C.c_void_p),
+                ("flags", C.c_void_p), ("ws", Workspace)]
+
+
+_P = C.c_void_p
+_I32 = C.c_int32
+_I64 = C.c_int64
+
+_SIGS = {
+    "lsb_version": ([], C.c_char_p),
+    "lsb_last_error": ([], C.c_char_p),
+    "lsb_sm_count": ([], C.c_int),
+    "lsb_partial_len": ([_I32], _I64),
+    "lsb_max_columns": ([], _I32),
+    "lsb_spmv_csr": ([_P, _P, _P, _P, _P, _I32, _P], C.c_int),
+    "lsb_spmv_stencil": ([_P, _P, _P, _P, _P, _I32, _P], C.c_int),
+    "lsb_mdot": ([_P, _I64, _I64, _I32, _P, _P, _P, _P, _P, _I32, _P], C.c_int),
+    "lsb_maxpy": ([_P, _P, _I64, _I64, _I32, _P, _I32, _P, _P, _I32, _P], C.c_int),
+    "lsb_norm_partial": ([_P, _I64, _P, _P, _P, _I32, _P], C.c_int),
+    "lsb_norm_finish": ([_P, _I32, _P, _I64, _P, _P, _P, _I32, _P], C.c_int),
+    "lsb_scale_div": ([_P, _I64, _P, _P, _P, _I32, _P], C.c_int),
+    "lsb_lagged_reduce": ([_P, _I32, _I32, _P], C.c_int),
+    "lsb_mgs_lvl2_small": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_cgs2_lvl2_small_a": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_cgs2_lvl2_small_b": ([_P, _I32, _I32, _P], C.c_int),
+    "lsb_lagged_update": ([_P, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_lagged_correct": ([_P, _I32, _I32, _P], C.c_int),
+    "lsb_mgs1_pass": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_collect_coef": ([_P, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_cgs_project": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_direct_small": ([_P, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_direct_normalize": ([_P, _I32, _I32, _P], C.c_int),
+    "lsb_cycle_begin": ([_P, _P], C.c_int),
+    "lsb_cycle_lsq": ([_P, _P], C.c_int),
+    "lsb_cycle_extract": ([_P, _P, _P, _P], C.c_int),
+    "lsb_restart_check": ([_P, _I32, _P], C.c_int),
+    "lsb_gram_row": ([_P, _I32, _I32, _I32, _P, _I64, _P], C.c_int),
+    "lsb_givens_update": ([_P, _P, _P, _I32, _P, _I32, _P, _P], C.c_int),
+    "lsb_back_substitute": ([_P, _P, _I32, _I32, _P, _P, _P], C.c_int),
+}
+
+EXPORTS = tuple(_SIGS)
+
+_lib = None
+
+
+def load(path=None):
+    """Load (once) and type the library; raises LsbUnavailable if absent."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise LsbUnavailable(
+            f"{p} not found: build it with `python -m paper_1809_05805_b200.build` "
+            "(there is no CPU fallback)")
+    try:
+        lib = C.CDLL(p)
+    except OSError as e:  # pragma: no cover
+        raise LsbUnavailable(f"cannot load {p}: {e}") from e
+    for name, (argt, rest) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argt
+        fn.restype = rest
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(rc, what):
+    if rc != OK:
+        msg = load().lsb_last_error().decode(errors="replace")
+        raise LsbError(f"{what} failed with status {rc}: {msg}")
+
+
+def call(name, *args):
+    rc = getattr(load(), name)(*args)
+    if rc != OK:
+        check(rc, name)
+    return rc

@@ -1,0 +1,244 @@
+// extern "C" entry points of liblsb200 (declared in include/lsb200.h).
+#include <stdio.h>
+#include <string.h>
+
+#include "reduce.cuh"
+
+namespace lsb {
+
+static thread_local char g_err[512] = "";
+static int g_sms = 0;
+
+int sm_count() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms < 1) g_sms = 1;
+  }
+  return g_sms;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof g_err, "%s: %s", what, cudaGetErrorString(e));
+    return LSB_ECUDA;
+  }
+  return LSB_OK;
+}
+
+// launchers defined in the other translation units
+int launch_mdot(const double*, int64_t, int64_t, int, const double*, const double*, double*,
+                const lsb_workspace*, const lsb_flags*, int, cudaStream_t);
+int launch_maxpy(const double*, const double*, int64_t, int64_t, int, const double*, int, double*,
+                 const lsb_flags*, int, cudaStream_t);
+int launch_lagged_update(const lsb_arnoldi&, int, int, int, cudaStream_t);
+int launch_lagged_correct(const lsb_arnoldi&, int, int, cudaStream_t);
+int launch_mgs1_pass(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
+int launch_cgs_project(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
+int launch_norm_partial(const double*, int64_t, double*, const lsb_workspace*, const lsb_flags*,
+                        int, cudaStream_t);
+int launch_norm_finish(const double*, int, const double*, int64_t, double*, const lsb_workspace*,
+                       const lsb_flags*, int, cudaStream_t);
+int launch_scale_div(const double*, int64_t, const double*, double*, const lsb_flags*, int, int,
+                     cudaStream_t);
+int launch_extract(const lsb_arnoldi&, double*, const double*, cudaStream_t);
+int launch_stencil(const lsb_stencil*, const double*, const double*, double*, lsb_flags*, int,
+                   cudaStream_t);
+int launch_csr(const lsb_csr*, const double*, const double*, double*, lsb_flags*, int,
+               cudaStream_t);
+int launch_mgs_lvl2_small(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
+int launch_cgs2_small_a(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
+int launch_cgs2_small_b(const lsb_arnoldi&, int, int, cudaStream_t);
+int launch_collect_coef(const lsb_arnoldi&, int, int, int, cudaStream_t);
+int launch_direct_small(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
+int launch_cycle_begin(const lsb_arnoldi&, cudaStream_t);
+int launch_cycle_lsq(const lsb_arnoldi&, cudaStream_t);
+int launch_restart_check(const lsb_arnoldi&, int, cudaStream_t);
+int launch_givens_update(double*, double*, double*, int, const double*, int, double*, cudaStream_t);
+int launch_back_substitute(const double*, const double*, int, int, double*, int*, cudaStream_t);
+
+static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+}  // namespace lsb
+
+using namespace lsb;
+
+extern "C" {
+
+const char* lsb_version(void) { return "lsb200 0.1 sm_100a"; }
+const char* lsb_last_error(void) { return g_err; }
+int lsb_sm_count(void) { return sm_count(); }
+int32_t lsb_max_columns(void) { return 128; }
+
+int64_t lsb_partial_len(int32_t pmax) {
+  // grid <= sm_count * 8 CTAs (mdot occupancy is lower), entries <= 2*min(pmax,128)
+  int64_t e = 2 * (int64_t)(pmax < 128 ? (pmax > 2 ? pmax : 2) : 128);
+  return (int64_t)sm_count() * 8 * e + 64;
+}
+
+int lsb_spmv_csr(const lsb_csr* A, const double* x, const double* b, double* y, lsb_flags* flags,
+                 int32_t it, void* stream) {
+  if (!A || !x || !y) return LSB_EINVAL;
+  return launch_csr(A, x, b, y, flags, it, S_(stream));
+}
+
+int lsb_spmv_stencil(const lsb_stencil* S, const double* x, const double* b, double* y,
+                     lsb_flags* flags, int32_t it, void* stream) {
+  if (!S || !x || !y) return LSB_EINVAL;
+  return launch_stencil(S, x, b, y, flags, it, S_(stream));
+}
+
+int lsb_mdot(const double* X, int64_t ld, int64_t n, int32_t p, const double* u, const double* w,
+             double* out, const lsb_workspace* ws, const lsb_flags* flags, int32_t it,
+             void* stream) {
+  if (p < 0 || n < 0 || !ws || !out) return LSB_EINVAL;
+  if (p > 0 && (!aligned16(X) || (ld & 1) || !aligned16(u) || (w && !aligned16(w))))
+    return LSB_EINVAL;
+  return launch_mdot(X, ld, n, p, u, w, out, ws, flags, it, S_(stream));
+}
+
+int lsb_maxpy(const double* y, const double* X, int64_t ld, int64_t n, int32_t p,
+              const double* alpha, int32_t alpha_sign, double* out, const lsb_flags* flags,
+              int32_t it, void* stream) {
+  if (p < 0 || n < 0) return LSB_EINVAL;
+  if (!aligned16(y) || !aligned16(out) || (p > 0 && (!aligned16(X) || (ld & 1))))
+    return LSB_EINVAL;
+  return launch_maxpy(y, X, ld, n, p, alpha, alpha_sign, out, flags, it, S_(stream));
+}
+
+int lsb_norm_partial(const double* x, int64_t n, double* out2, const lsb_workspace* ws,
+                     const lsb_flags* flags, int32_t it, void* stream) {
+  if (n < 0 || !ws) return LSB_EINVAL;
+  return launch_norm_partial(x, n, out2, ws, flags, it, S_(stream));
+}
+
+int lsb_norm_finish(const double* parts, int32_t nparts, const double* x, int64_t n, double* out,
+                    const lsb_workspace* ws, const lsb_flags* flags, int32_t it, void* stream) {
+  if (nparts < 1 || !ws) return LSB_EINVAL;
+  return launch_norm_finish(parts, nparts, x, n, out, ws, flags, it, S_(stream));
+}
+
+int lsb_scale_div(const double* x, int64_t n, const double* s, double* out,
+                  const lsb_flags* flags, int32_t it, void* stream) {
+  return launch_scale_div(x, n, s, out, flags, it, 0, S_(stream));
+}
+
+static int check_arnoldi(const lsb_arnoldi* S) {
+  if (!S || !S->V || !S->flags || !S->scal || (S->ld & 1) || !aligned16(S->V)) return LSB_EINVAL;
+  return LSB_OK;
+}
+
+int lsb_lagged_reduce(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (p < 1 || p + 1 > S->cap) return LSB_ERANGE;
+  const double* u = S->V + (int64_t)(p - 1) * S->ld;
+  const double* w = S->V + (int64_t)p * S->ld;
+  return launch_mdot(S->V, S->ld, S->n, p, u, w, S->Gloc, &S->ws, S->flags, it, S_(stream));
+}
+
+int lsb_mgs_lvl2_small(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
+                       int32_t givens_col, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_mgs_lvl2_small(*S, it, p, krylov_scale, givens_col, S_(stream));
+}
+
+int lsb_cgs2_lvl2_small_a(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
+                          int32_t givens_col, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (!S->L) return LSB_EINVAL;
+  return launch_cgs2_small_a(*S, it, p, krylov_scale, givens_col, S_(stream));
+}
+
+int lsb_cgs2_lvl2_small_b(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_cgs2_small_b(*S, it, p, S_(stream));
+}
+
+int lsb_lagged_update(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
+                      void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (p < 1 || p + 1 > S->cap) return LSB_ERANGE;
+  return launch_lagged_update(*S, it, p, krylov_scale, S_(stream));
+}
+
+int lsb_lagged_correct(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (p < 1 || p + 1 > S->cap) return LSB_ERANGE;
+  return launch_lagged_correct(*S, it, p, S_(stream));
+}
+
+int lsb_mgs1_pass(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t k, int32_t p,
+                  void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (k < 0 || k > p || col < p || col >= S->cap) return LSB_ERANGE;
+  return launch_mgs1_pass(*S, it, col, k, p, S_(stream));
+}
+
+int lsb_collect_coef(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t accumulate,
+                     void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_collect_coef(*S, it, p, accumulate, S_(stream));
+}
+
+int lsb_cgs_project(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, int32_t want_norm,
+                    void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (col < p || col >= S->cap) return LSB_ERANGE;
+  return launch_cgs_project(*S, it, col, p, want_norm, S_(stream));
+}
+
+int lsb_direct_small(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  const int gc = S->m > 0 ? col : 0;
+  return launch_direct_small(*S, it, col, p, gc, S_(stream));
+}
+
+int lsb_direct_normalize(const lsb_arnoldi* S, int32_t it, int32_t col, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  double* z = S->V + (int64_t)col * S->ld;
+  return launch_scale_div(z, S->n, S->scal + LSB_S_BETA, z, S->flags, it, 1, S_(stream));
+}
+
+int lsb_cycle_begin(const lsb_arnoldi* S, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_cycle_begin(*S, S_(stream));
+}
+
+int lsb_cycle_lsq(const lsb_arnoldi* S, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_cycle_lsq(*S, S_(stream));
+}
+
+int lsb_cycle_extract(const lsb_arnoldi* S, double* x, const double* col_scale, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_extract(*S, x, col_scale, S_(stream));
+}
+
+int lsb_restart_check(const lsb_arnoldi* S, int32_t first, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_restart_check(*S, first, S_(stream));
+}
+
+int lsb_gram_row(const lsb_arnoldi* S, int32_t it, int32_t row, int32_t ncols, double* gram,
+                 int64_t gram_ld, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (ncols < 1 || row < 0 || row >= S->cap) return LSB_ERANGE;
+  const double* u = S->V + (int64_t)row * S->ld;
+  return launch_mdot(S->V, S->ld, S->n, ncols, u, nullptr, gram + (int64_t)row * gram_ld, &S->ws,
+                     S->flags, it, S_(stream));
+}
+
+int lsb_givens_update(double* rot, double* g, double* tri, int32_t m, const double* h, int32_t i,
+                      double* res_out, void* stream) {
+  return launch_givens_update(rot, g, tri, m, h, i, res_out, S_(stream));
+}
+
+int lsb_back_substitute(const double* tri, const double* g, int32_t m, int32_t k, double* y,
+                        int32_t* status, void* stream) {
+  return launch_back_substitute(tri, g, m, k, y, status, S_(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,333 @@
+// K5: the small (p-sized) state of the orthogonalizers and of GMRES, kept on
+// device: deferred norm, breakdown test, R/T/L columns, the projection
+// coefficients, the Hessenberg column and its Givens fold, the convergence
+// test, and the per-cycle back-substitution.  One CTA; O(p^2) flops.
+//
+// Reference: gram_schmidt.py:96-106 (breakdown), 206-245 (mgs_lvl2),
+// 248-280 (cgs2_lvl2), gmres.py:153-192 (Givens / least squares),
+// gmres.py:407-435 (Hessenberg column assembly and settle).
+#include "reduce.cuh"
+
+namespace lsb {
+
+constexpr int kSmall = 256;  // threads; cap <= kSmall
+
+__device__ __forceinline__ double gsum(const lsb_arnoldi& S, int e) {
+  double v = S.G[e];
+  for (int q = 1; q < S.g_parts; ++q) v += S.G[(int64_t)q * S.g_stride + e];
+  return v;
+}
+
+// tol = btf * eps * sqrt(n) * hypot(r_diag, ||r_col||)   (gram_schmidt.py:96-100)
+__device__ double breakdown_tol(const lsb_arnoldi& S, double r_diag, const double* rcol,
+                                int64_t stride, int len) {
+  double pre = r_diag;
+  if (len > 0) {
+    double ss = 0.0;
+    for (int j = 0; j < len; ++j) { const double v = rcol[j * stride]; ss = fma(v, v, ss); }
+    pre = py_hypot(r_diag, sqrt(ss));
+  }
+  const double btf = S.scal[LSB_S_BTF];
+  return __dmul_rn(__dmul_rn(__dmul_rn(btf, kEps), sqrt((double)S.n_global)), pre);
+}
+
+// Hessenberg column gc-1 = R[0..gc, gc] (R[gc,gc] = 0 after a breakdown),
+// folded into the Givens state; records |g[gc]| and stops the cycle on
+// convergence or breakdown (gmres.py:427-435).
+__device__ void settle(const lsb_arnoldi& S, int it, int gc, bool broke) {
+  double h[kSmall + 4];
+  const int cap = S.cap;
+  for (int j = 0; j <= gc; ++j) h[j] = S.R[(int64_t)j * cap + gc];
+  const double res = givens_fold(h, S.rot, S.g, gc);
+  for (int j = 0; j <= gc; ++j) S.tri[(int64_t)j * S.m + (gc - 1)] = h[j];
+  S.res[gc] = res;
+  const double target = S.scal[LSB_S_TARGET];
+  if (res <= target || broke) {
+    S.flags->stop_iter = it;
+    S.flags->status = res <= target ? LSB_CONVERGED : LSB_BREAKDOWN;
+  }
+}
+
+// ------------------------------------------------------------------ mgs_lvl2
+__global__ void __launch_bounds__(kSmall)
+mgs_lvl2_small_kernel(lsb_arnoldi S, int it, int p, int ks, int gc) {
+  if (gated_off(S.flags, it)) return;
+  __shared__ double sG0[kSmall], sy[kSmall];
+  __shared__ double sbeta;
+  __shared__ int sbroke;
+  const int t = threadIdx.x, cap = S.cap;
+  for (int e = t; e < p; e += blockDim.x) { sG0[e] = gsum(S, 2 * e); sy[e] = gsum(S, 2 * e + 1); }
+  __syncthreads();
+  if (t == 0) {
+    const double bsq = sG0[p - 1];
+    const double beta = bsq > 0.0 ? sqrt(bsq) : 0.0;
+    const double tol = breakdown_tol(S, beta, S.R + (p - 1), cap, p - 1);
+    sbeta = beta;
+    sbroke = beta <= tol;
+    S.scal[LSB_S_BETA] = beta;
+    S.scal[LSB_S_TOL] = tol;
+  }
+  __syncthreads();
+  const double beta = sbeta;
+  if (sbroke) {
+    if (t == 0) {
+      S.flags->broke_iter = it;
+      if (gc > 0) settle(S, it, gc, true);
+      else { S.flags->stop_iter = it; S.flags->status = LSB_STARTUP_BREAKDOWN; }
+    }
+    return;
+  }
+  // T[:p-1, p-1] = -(T[:p-1, :p-1] @ (G[:p-1, 0] / beta));  T[p-1, p-1] = 1
+  for (int e = t; e < p - 1; e += blockDim.x) sG0[e] = __ddiv_rn(sG0[e], beta);
+  __syncthreads();
+  for (int j = t; j < p - 1; j += blockDim.x) {
+    double acc = 0.0;
+    for (int l = j; l < p - 1; ++l) acc = fma(S.T[(int64_t)j * cap + l], sG0[l], acc);
+    S.T[(int64_t)j * cap + (p - 1)] = -acc;
+  }
+  if (t == 0) {
+    S.T[(int64_t)(p - 1) * cap + (p - 1)] = 1.0;
+    S.R[(int64_t)(p - 1) * cap + (p - 1)] = beta;
+    sy[p - 1] = __ddiv_rn(sy[p - 1], beta);
+  }
+  __syncthreads();
+  // c = T[:p,:p]^T y  (/beta);  R[:p, p] = c
+  for (int j = t; j < p; j += blockDim.x) {
+    double acc = 0.0;
+    for (int l = 0; l <= j; ++l) acc = fma(S.T[(int64_t)l * cap + j], sy[l], acc);
+    if (ks) acc = __ddiv_rn(acc, beta);
+    S.coef[j] = acc;
+    S.R[(int64_t)j * cap + p] = acc;
+  }
+  __syncthreads();
+  if (t == 0 && gc > 0) settle(S, it, gc, false);
+}
+
+// ------------------------------------------------------------------ cgs2_lvl2
+__global__ void __launch_bounds__(kSmall)
+cgs2_small_a_kernel(lsb_arnoldi S, int it, int p, int ks, int gc) {
+  if (gated_off(S.flags, it)) return;
+  __shared__ double sG0[kSmall], sy[kSmall];
+  __shared__ double sbeta;
+  __shared__ int sbroke;
+  const int t = threadIdx.x, cap = S.cap;
+  for (int e = t; e < p; e += blockDim.x) { sG0[e] = gsum(S, 2 * e); sy[e] = gsum(S, 2 * e + 1); }
+  __syncthreads();
+  if (t == 0) {
+    const double bsq = sG0[p - 1];
+    const double beta = bsq > 0.0 ? sqrt(bsq) : 0.0;
+    const double tol = breakdown_tol(S, beta, S.R + (p - 1), cap, p - 1);
+    sbeta = beta;
+    sbroke = beta <= tol;
+    S.scal[LSB_S_BETA] = beta;
+    S.scal[LSB_S_TOL] = tol;
+  }
+  __syncthreads();
+  const double beta = sbeta;
+  if (sbroke) {
+    if (t == 0) {
+      S.flags->broke_iter = it;
+      if (gc > 0) settle(S, it, gc, true);
+      else { S.flags->stop_iter = it; S.flags->status = LSB_STARTUP_BREAKDOWN; }
+    }
+    return;
+  }
+  // L[p-1, :p-1] = G[:p-1, 0] / beta  (gram_schmidt.py:266-267)
+  for (int e = t; e < p - 1; e += blockDim.x)
+    S.L[(int64_t)(p - 1) * cap + e] = __ddiv_rn(sG0[e], beta);
+  if (t == 0) {
+    S.R[(int64_t)(p - 1) * cap + (p - 1)] = beta;
+    sy[p - 1] = __ddiv_rn(sy[p - 1], beta);
+  }
+  __syncthreads();
+  // r = y - Ls y - Ls^T y  (/beta)   (gram_schmidt.py:270-274)
+  for (int j = t; j < p; j += blockDim.x) {
+    double a = 0.0, b = 0.0;
+    for (int l = 0; l < j; ++l) a = fma(S.L[(int64_t)j * cap + l], sy[l], a);
+    for (int l = j + 1; l < p; ++l) b = fma(S.L[(int64_t)l * cap + j], sy[l], b);
+    double r = (sy[j] - a) - b;
+    if (ks) r = __ddiv_rn(r, beta);
+    S.coef[j] = r;
+  }
+  __syncthreads();
+  if (t == 0 && gc > 0) settle(S, it, gc, false);
+}
+
+// s = gathered second-pass products; R[:p, p] = r + s   (gram_schmidt.py:276-278)
+__global__ void __launch_bounds__(kSmall)
+cgs2_small_b_kernel(lsb_arnoldi S, int it, int p) {
+  if (gated_off(S.flags, it)) return;
+  if (S.flags->broke_iter == it) return;
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {
+    const double s = gsum(S, j);
+    S.coef2[j] = s;
+    S.R[(int64_t)j * S.cap + p] = S.coef[j] + s;
+  }
+}
+
+// ------------------------------------------------------------------ direct kernels
+// coef = s (or coef += s) and coef2 = s from the gathered products.
+__global__ void __launch_bounds__(kSmall)
+collect_coef_kernel(lsb_arnoldi S, int it, int p, int accumulate) {
+  if (gated_off(S.flags, it)) return;
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {
+    const double s = gsum(S, j);
+    S.coef2[j] = s;
+    S.coef[j] = accumulate ? S.coef[j] + s : s;
+  }
+}
+
+// r_diag (already in scal[BETA] from norm_finish), breakdown test, Hbar
+// column col-1 = [coef[0..p), r_diag] stored in R[:, col], Givens fold
+// (gmres.py:362-381 / gram_schmidt.py:139-141, 158-160).
+__global__ void __launch_bounds__(32)
+direct_small_kernel(lsb_arnoldi S, int it, int col, int p, int gc) {
+  if (gated_off(S.flags, it)) return;
+  if (threadIdx.x != 0) return;
+  const double r_diag = S.scal[LSB_S_BETA];
+  const double tol = breakdown_tol(S, r_diag, S.coef, 1, p);
+  S.scal[LSB_S_TOL] = tol;
+  const bool broke = r_diag <= tol;
+  if (broke) S.flags->broke_iter = it;
+  if (gc > 0) {
+    const int cap = S.cap;
+    for (int j = 0; j < p; ++j) S.R[(int64_t)j * cap + col] = S.coef[j];
+    S.R[(int64_t)col * cap + col] = broke ? 0.0 : r_diag;
+    settle(S, it, gc, broke);
+  } else if (broke) {
+    S.flags->stop_iter = it;
+    S.flags->status = LSB_STARTUP_BREAKDOWN;
+  }
+}
+
+// ------------------------------------------------------------------ cycle control
+__global__ void __launch_bounds__(kSmall)
+cycle_begin_kernel(lsb_arnoldi S) {
+  const int t = threadIdx.x;
+  const int64_t c2 = (int64_t)S.cap * S.cap;
+  for (int64_t e = t; e < c2; e += blockDim.x) { S.R[e] = 0.0; S.T[e] = 0.0; if (S.L) S.L[e] = 0.0; }
+  for (int64_t e = t; e < (int64_t)(S.m + 1) * S.m; e += blockDim.x) S.tri[e] = 0.0;
+  for (int e = t; e < 2 * S.m; e += blockDim.x) S.rot[e] = 0.0;
+  for (int e = t; e <= S.m; e += blockDim.x) { S.g[e] = 0.0; S.res[e] = 0.0; }
+  for (int e = t; e < S.cap; e += blockDim.x) { S.coef[e] = 0.0; S.coef2[e] = 0.0; }
+  __syncthreads();
+  if (t == 0) {
+    S.g[0] = S.scal[LSB_S_RNORM];
+    S.flags->stop_iter = LSB_NO_STOP;
+    S.flags->status = LSB_RUNNING;
+    S.flags->broke_iter = -1;
+    S.flags->k = 0;
+    S.flags->restart_ok = 0;
+  }
+}
+
+// solve_least_squares (gmres.py:184-192) on the rotated k x k triangle.
+__global__ void __launch_bounds__(32)
+cycle_lsq_kernel(lsb_arnoldi S) {
+  if (threadIdx.x != 0) return;
+  const int stop = S.flags->stop_iter;
+  const int k = stop == LSB_NO_STOP ? S.m : stop;
+  S.flags->k = k;
+  const int m = S.m;
+  for (int i = k - 1; i >= 0; --i) {
+    const double d = S.tri[(int64_t)i * m + i];
+    if (d == 0.0) {
+      S.flags->status = LSB_SINGULAR;
+      S.flags->k = i;  // diagnostic: zero diagonal index
+      return;
+    }
+    double acc = 0.0;
+    for (int j = i + 1; j < k; ++j) acc = fma(S.tri[(int64_t)i * m + j], S.coef2[j], acc);
+    S.coef2[i] = __ddiv_rn(S.g[i] - acc, d);
+  }
+}
+
+// First call: denom = beta0 or 1, target = rel_tol * beta0 (gmres.py:472-479).
+__global__ void restart_check_kernel(lsb_arnoldi S, int first) {
+  if (threadIdx.x != 0) return;
+  const double rn = S.scal[LSB_S_RNORM];
+  if (first) {
+    S.scal[LSB_S_DENOM] = rn > 0.0 ? rn : 1.0;
+    S.scal[LSB_S_TARGET] = __dmul_rn(S.scal[LSB_S_RELTOL], rn);
+  }
+  S.flags->restart_ok = rn <= S.scal[LSB_S_TARGET];
+}
+
+// ------------------------------------------------------------------ launchers
+int launch_mgs_lvl2_small(const lsb_arnoldi& S, int it, int p, int ks, int gc, cudaStream_t st) {
+  if (p < 1 || S.cap > kSmall || p >= S.cap) return LSB_ERANGE;
+  mgs_lvl2_small_kernel<<<1, kSmall, 0, st>>>(S, it, p, ks, gc);
+  return check_launch("mgs_lvl2_small");
+}
+int launch_cgs2_small_a(const lsb_arnoldi& S, int it, int p, int ks, int gc, cudaStream_t st) {
+  if (p < 1 || S.cap > kSmall || p >= S.cap) return LSB_ERANGE;
+  cgs2_small_a_kernel<<<1, kSmall, 0, st>>>(S, it, p, ks, gc);
+  return check_launch("cgs2_small_a");
+}
+int launch_cgs2_small_b(const lsb_arnoldi& S, int it, int p, cudaStream_t st) {
+  cgs2_small_b_kernel<<<1, kSmall, 0, st>>>(S, it, p);
+  return check_launch("cgs2_small_b");
+}
+int launch_collect_coef(const lsb_arnoldi& S, int it, int p, int acc, cudaStream_t st) {
+  collect_coef_kernel<<<1, kSmall, 0, st>>>(S, it, p, acc);
+  return check_launch("collect_coef");
+}
+int launch_direct_small(const lsb_arnoldi& S, int it, int col, int p, int gc, cudaStream_t st) {
+  direct_small_kernel<<<1, 32, 0, st>>>(S, it, col, p, gc);
+  return check_launch("direct_small");
+}
+int launch_cycle_begin(const lsb_arnoldi& S, cudaStream_t st) {
+  if (S.cap > kSmall) return LSB_ERANGE;
+  cycle_begin_kernel<<<1, kSmall, 0, st>>>(S);
+  return check_launch("cycle_begin");
+}
+int launch_cycle_lsq(const lsb_arnoldi& S, cudaStream_t st) {
+  cycle_lsq_kernel<<<1, 32, 0, st>>>(S);
+  return check_launch("cycle_lsq");
+}
+int launch_restart_check(const lsb_arnoldi& S, int first, cudaStream_t st) {
+  restart_check_kernel<<<1, 32, 0, st>>>(S, first);
+  return check_launch("restart_check");
+}
+
+
+// ------------------------------------------------------------------ standalone Givens / LSQ
+// givens_update(state, h_col, i) and solve_least_squares(state, k) of the
+// public API (gmres.py:153-192) on device-resident GivensState arrays.
+__global__ void givens_update_kernel(double* rot, double* g, double* tri, int m, const double* hin,
+                                     int i, double* res_out) {
+  if (threadIdx.x != 0) return;
+  double h[kSmall + 4];
+  for (int j = 0; j <= i; ++j) h[j] = hin[j];
+  const double res = givens_fold(h, rot, g, i);
+  for (int j = 0; j <= i; ++j) tri[(int64_t)j * m + (i - 1)] = h[j];
+  *res_out = res;
+}
+
+__global__ void back_substitute_kernel(const double* tri, const double* g, int m, int k, double* y,
+                                       int* status) {
+  if (threadIdx.x != 0) return;
+  *status = -1;
+  for (int i = k - 1; i >= 0; --i) {
+    const double d = tri[(int64_t)i * m + i];
+    if (d == 0.0) { *status = i; return; }
+    double acc = 0.0;
+    for (int j = i + 1; j < k; ++j) acc = fma(tri[(int64_t)i * m + j], y[j], acc);
+    y[i] = __ddiv_rn(g[i] - acc, d);
+  }
+}
+
+int launch_givens_update(double* rot, double* g, double* tri, int m, const double* h, int i,
+                         double* res, cudaStream_t st) {
+  if (i < 1 || i > m || m + 1 > kSmall) return LSB_ERANGE;
+  givens_update_kernel<<<1, 32, 0, st>>>(rot, g, tri, m, h, i, res);
+  return check_launch("givens_update");
+}
+int launch_back_substitute(const double* tri, const double* g, int m, int k, double* y, int* status,
+                           cudaStream_t st) {
+  if (k < 0 || k > m) return LSB_ERANGE;
+  back_substitute_kernel<<<1, 32, 0, st>>>(tri, g, m, k, y, status);
+  return check_launch("back_substitute");
+}
+
+}  // namespace lsb

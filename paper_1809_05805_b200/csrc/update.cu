@@ -1,0 +1,370 @@
+// Row-parallel passes over the basis: MAXPY family (K2/K4/K10), the fused
+// level-1 MGS axpy+dot pass (K8), norms and scalings.  All are HBM-bound
+// streaming kernels: 128-bit loads of row pairs, coefficients broadcast
+// from shared memory, grid-stride persistent CTAs.
+#include "reduce.cuh"
+
+namespace lsb {
+
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+
+static int row_grid(int64_t n, int per_sm = 8) {
+  const int64_t pairs = (n + 1) / 2;
+  int64_t g = (pairs + kThreads - 1) / kThreads;
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// ------------------------------------------------------------------ maxpy
+// out = y + sign * X alpha   (kernels.py:350-362; cgs_iterated uses sign -1)
+__global__ void __launch_bounds__(kThreads)
+maxpy_kernel(const double* __restrict__ y, const double* __restrict__ X, int64_t ld, int64_t n,
+             int p, const double* __restrict__ alpha, double sign, double* out,
+             const lsb_flags* gate, int it) {
+  if (gated_off(gate, it)) return;
+  extern __shared__ double sa[];
+  for (int k = threadIdx.x; k < p; k += blockDim.x) sa[k] = sign * alpha[k];
+  __syncthreads();
+  const int64_t npair = n / 2;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = 2 * j;
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 8
+    for (int k = 0; k < p; ++k) {
+      const double2 q = ld2(X + (int64_t)k * ld + r);
+      acc.x = fma(sa[k], q.x, acc.x);
+      acc.y = fma(sa[k], q.y, acc.y);
+    }
+    const double2 yy = ld2(y + r);
+    st2(out + r, make_double2(yy.x + acc.x, yy.y + acc.y));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t r = n - 1;
+    double acc = 0.0;
+    for (int k = 0; k < p; ++k) acc = fma(sa[k], X[(int64_t)k * ld + r], acc);
+    out[r] = y[r] + acc;
+  }
+}
+
+int launch_maxpy(const double* y, const double* X, int64_t ld, int64_t n, int p,
+                 const double* alpha, int sign, double* out, const lsb_flags* gate, int it,
+                 cudaStream_t st) {
+  if (n <= 0) return LSB_OK;
+  maxpy_kernel<<<row_grid(n), kThreads, sizeof(double) * (p > 0 ? p : 1), st>>>(
+      y, X, ld, n, p, alpha, sign < 0 ? -1.0 : 1.0, out, gate, it);
+  return check_launch("maxpy");
+}
+
+// ------------------------------------------------------------------ lagged update (K2)
+// gram_schmidt.py:230-242:  u /= beta;  (krylov) w /= beta;  w -= Q c
+// with Q's last column already the normalised u.  One pass: reads Q and w,
+// writes u and w.
+__global__ void __launch_bounds__(kThreads)
+lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks) {
+  if (gated_off(S.flags, it)) return;
+  if (S.flags && S.flags->broke_iter == it) return;
+  extern __shared__ double sc[];
+  for (int k = threadIdx.x; k < p; k += blockDim.x) sc[k] = S.coef[k];
+  __syncthreads();
+  const double beta = S.scal[LSB_S_BETA];
+  const int64_t ld = S.ld, n = S.n;
+  double* __restrict__ u = S.V + (int64_t)(p - 1) * ld;
+  double* __restrict__ w = S.V + (int64_t)p * ld;
+  const double cu = sc[p - 1];
+  const int64_t npair = n / 2;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = 2 * j;
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 8
+    for (int k = 0; k < p - 1; ++k) {
+      const double2 q = ld2(S.V + (int64_t)k * ld + r);
+      acc.x = fma(sc[k], q.x, acc.x);
+      acc.y = fma(sc[k], q.y, acc.y);
+    }
+    double2 uu = ld2(u + r);
+    uu.x = __ddiv_rn(uu.x, beta);
+    uu.y = __ddiv_rn(uu.y, beta);
+    st2(u + r, uu);
+    acc.x = fma(cu, uu.x, acc.x);
+    acc.y = fma(cu, uu.y, acc.y);
+    double2 ww = ld2(w + r);
+    if (ks) { ww.x = __ddiv_rn(ww.x, beta); ww.y = __ddiv_rn(ww.y, beta); }
+    st2(w + r, make_double2(ww.x - acc.x, ww.y - acc.y));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t r = n - 1;
+    double acc = 0.0;
+    for (int k = 0; k < p - 1; ++k) acc = fma(sc[k], S.V[(int64_t)k * ld + r], acc);
+    const double uu = __ddiv_rn(u[r], beta);
+    u[r] = uu;
+    acc = fma(cu, uu, acc);
+    double ww = w[r];
+    if (ks) ww = __ddiv_rn(ww, beta);
+    w[r] = ww - acc;
+  }
+}
+
+int launch_lagged_update(const lsb_arnoldi& S, int it, int p, int ks, cudaStream_t st) {
+  if (p < 1) return LSB_OK;
+  lagged_update_kernel<<<row_grid(S.n), kThreads, sizeof(double) * p, st>>>(S, it, p, ks);
+  return check_launch("lagged_update");
+}
+
+// w -= Q coef2   (cgs2_lvl2 second projection, gram_schmidt.py:277)
+__global__ void __launch_bounds__(kThreads)
+lagged_correct_kernel(lsb_arnoldi S, int it, int p) {
+  if (gated_off(S.flags, it)) return;
+  if (S.flags && S.flags->broke_iter == it) return;
+  extern __shared__ double sc[];
+  for (int k = threadIdx.x; k < p; k += blockDim.x) sc[k] = S.coef2[k];
+  __syncthreads();
+  const int64_t ld = S.ld, n = S.n;
+  double* __restrict__ w = S.V + (int64_t)p * ld;
+  const int64_t npair = n / 2;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = 2 * j;
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 8
+    for (int k = 0; k < p; ++k) {
+      const double2 q = ld2(S.V + (int64_t)k * ld + r);
+      acc.x = fma(sc[k], q.x, acc.x);
+      acc.y = fma(sc[k], q.y, acc.y);
+    }
+    const double2 ww = ld2(w + r);
+    st2(w + r, make_double2(ww.x - acc.x, ww.y - acc.y));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t r = n - 1;
+    double acc = 0.0;
+    for (int k = 0; k < p; ++k) acc = fma(sc[k], S.V[(int64_t)k * ld + r], acc);
+    w[r] = w[r] - acc;
+  }
+}
+
+int launch_lagged_correct(const lsb_arnoldi& S, int it, int p, cudaStream_t st) {
+  if (p < 1) return LSB_OK;
+  lagged_correct_kernel<<<row_grid(S.n), kThreads, sizeof(double) * p, st>>>(S, it, p);
+  return check_launch("lagged_correct");
+}
+
+// ------------------------------------------------------------------ level-1 MGS pass (K8)
+// gram_schmidt.py:154-158: pass k applies the (k-1)-th rank-1 update
+// `work -= h * Q[:, k-1]` (numpy: product then difference, two roundings)
+// and produces the k-th dot `Q[:, k] . work` -- or, after the last update,
+// the (max|z|, sum z^2) pair of the norm.  z is read and written once.
+__device__ __forceinline__ double sum_parts(const lsb_arnoldi& S, int e) {
+  double v = S.G[e];
+  for (int q = 1; q < S.g_parts; ++q) v += S.G[(int64_t)q * S.g_stride + e];
+  return v;
+}
+
+__global__ void __launch_bounds__(kThreads)
+mgs1_pass_kernel(lsb_arnoldi S, int it, int col, int k, int p) {
+  if (gated_off(S.flags, it)) return;
+  const int64_t ld = S.ld, n = S.n;
+  double* __restrict__ z = S.V + (int64_t)col * ld;
+  double h = 0.0;
+  const double* qm = nullptr;
+  if (k > 0) {
+    h = sum_parts(S, 0);
+    qm = S.V + (int64_t)(k - 1) * ld;
+    if (blockIdx.x == 0 && threadIdx.x == 0) S.coef[k - 1] = h;
+  }
+  const double* qk = k < p ? S.V + (int64_t)k * ld : nullptr;
+  double a0 = 0.0, a1 = 0.0;  // dot  or  (amax, ssq)
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double zz = z[r];
+    if (qm) { zz = __dsub_rn(zz, __dmul_rn(h, qm[r])); z[r] = zz; }
+    if (qk) a0 = fma(qk[r], zz, a0);
+    else { a0 = fmax(a0, fabs(zz)); a1 = fma(zz, zz, a1); }
+  }
+  if (qk) {
+    const double v[1] = {a0};
+    const int op[1] = {0};
+    grid_reduce<1>(v, op, S.ws.partial, S.ws.counter, S.Gloc);
+  } else {
+    const double v[2] = {a0, a1};
+    const int op[2] = {1, 0};
+    grid_reduce<2>(v, op, S.ws.partial, S.ws.counter, S.Gloc);
+  }
+}
+
+int launch_mgs1_pass(const lsb_arnoldi& S, int it, int col, int k, int p, cudaStream_t st) {
+  int g = row_grid(2 * S.n, 4);
+  mgs1_pass_kernel<<<g, kThreads, 0, st>>>(S, it, col, k, p);
+  return check_launch("mgs1_pass");
+}
+
+// z <- z - Q coef2 (cgs_iterated pass, gram_schmidt.py:136-138), optional
+// (max|z|, sum z^2) of the result for the following norm.
+__global__ void __launch_bounds__(kThreads)
+cgs_project_kernel(lsb_arnoldi S, int it, int col, int p, int want_norm) {
+  if (gated_off(S.flags, it)) return;
+  extern __shared__ double sc[];
+  for (int k = threadIdx.x; k < p; k += blockDim.x) sc[k] = S.coef2[k];
+  __syncthreads();
+  const int64_t ld = S.ld, n = S.n;
+  double* __restrict__ z = S.V + (int64_t)col * ld;
+  double amax = 0.0, ssq = 0.0;
+  const int64_t npair = n / 2;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = 2 * j;
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 8
+    for (int k = 0; k < p; ++k) {
+      const double2 q = ld2(S.V + (int64_t)k * ld + r);
+      acc.x = fma(-sc[k], q.x, acc.x);
+      acc.y = fma(-sc[k], q.y, acc.y);
+    }
+    double2 zz = ld2(z + r);
+    zz.x = zz.x + acc.x;
+    zz.y = zz.y + acc.y;
+    st2(z + r, zz);
+    amax = fmax(amax, fmax(fabs(zz.x), fabs(zz.y)));
+    ssq = fma(zz.x, zz.x, ssq);
+    ssq = fma(zz.y, zz.y, ssq);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t r = n - 1;
+    double acc = 0.0;
+    for (int k = 0; k < p; ++k) acc = fma(-sc[k], S.V[(int64_t)k * ld + r], acc);
+    const double zz = z[r] + acc;
+    z[r] = zz;
+    amax = fmax(amax, fabs(zz));
+    ssq = fma(zz, zz, ssq);
+  }
+  if (want_norm) {
+    const double v[2] = {amax, ssq};
+    const int op[2] = {1, 0};
+    grid_reduce<2>(v, op, S.ws.partial, S.ws.counter, S.Gloc);
+  }
+}
+
+int launch_cgs_project(const lsb_arnoldi& S, int it, int col, int p, int want_norm,
+                       cudaStream_t st) {
+  cgs_project_kernel<<<row_grid(S.n), kThreads, sizeof(double) * (p > 0 ? p : 1), st>>>(
+      S, it, col, p, want_norm);
+  return check_launch("cgs_project");
+}
+
+// ------------------------------------------------------------------ norms
+__global__ void __launch_bounds__(kThreads)
+norm_partial_kernel(const double* __restrict__ x, int64_t n, double* out2, double* partial,
+                    unsigned* counter, const lsb_flags* gate, int it) {
+  if (gated_off(gate, it)) return;
+  double amax = 0.0, ssq = 0.0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[r];
+    amax = fmax(amax, fabs(v));
+    if (isnan(v)) amax = v;
+    ssq = fma(v, v, ssq);
+  }
+  const double v[2] = {amax, ssq};
+  const int op[2] = {1, 0};
+  grid_reduce<2>(v, op, partial, counter, out2);
+}
+
+int launch_norm_partial(const double* x, int64_t n, double* out2, const lsb_workspace* ws,
+                        const lsb_flags* gate, int it, cudaStream_t st) {
+  norm_partial_kernel<<<row_grid(2 * n, 4), kThreads, 0, st>>>(x, n, out2, ws->partial,
+                                                               ws->counter, gate, it);
+  return check_launch("norm_partial");
+}
+
+// ||x|| from stacked (amax, ssq) partials.  In-range magnitudes use
+// sqrt(sum x^2) directly; outside [2^-450, 2^450] every CTA re-reads x with
+// an exact power-of-two scale (no rounding from the scaling itself), the
+// overflow/underflow-safe path of the reference's amax-scaled norm.
+__global__ void __launch_bounds__(kThreads)
+norm_finish_kernel(const double* parts, int nparts, const double* __restrict__ x, int64_t n,
+                   double* out, double* partial, unsigned* counter, const lsb_flags* gate,
+                   int it) {
+  if (gated_off(gate, it)) return;
+  double amax = parts[0], ssq = parts[1];
+  for (int q = 1; q < nparts; ++q) { amax = fmax(amax, parts[2 * q]); ssq += parts[2 * q + 1]; }
+  const double lo = 0x1p-450, hi = 0x1p450;
+  if (amax == 0.0 || isnan(amax) || (amax >= lo && amax <= hi) || nparts > 1) {
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      *out = amax == 0.0 ? 0.0 : (isnan(amax) ? amax : sqrt(ssq));
+    return;
+  }
+  int e;
+  frexp(amax, &e);
+  const double s = ldexp(1.0, -e);
+  double acc = 0.0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[r] * s;
+    acc = fma(v, v, acc);
+  }
+  const double v[1] = {acc};
+  const int op[1] = {0};
+  __shared__ double res;
+  if (grid_reduce<1>(v, op, partial, counter, &res)) {
+    __syncthreads();
+    if (threadIdx.x == 0) *out = sqrt(res) / s;
+  }
+}
+
+int launch_norm_finish(const double* parts, int nparts, const double* x, int64_t n, double* out,
+                       const lsb_workspace* ws, const lsb_flags* gate, int it, cudaStream_t st) {
+  norm_finish_kernel<<<row_grid(2 * n, 4), kThreads, 0, st>>>(parts, nparts, x, n, out,
+                                                              ws->partial, ws->counter, gate, it);
+  return check_launch("norm_finish");
+}
+
+// ------------------------------------------------------------------ scalings
+__global__ void __launch_bounds__(kThreads)
+scale_div_kernel(const double* __restrict__ x, int64_t n, const double* s, double* out,
+                 const lsb_flags* gate, int it, int skip_if_broke) {
+  if (gated_off(gate, it)) return;
+  if (skip_if_broke && gate && gate->broke_iter == it) return;
+  const double d = *s;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    out[r] = __ddiv_rn(x[r], d);
+}
+
+int launch_scale_div(const double* x, int64_t n, const double* s, double* out,
+                     const lsb_flags* gate, int it, int skip_if_broke, cudaStream_t st) {
+  if (n <= 0) return LSB_OK;
+  scale_div_kernel<<<row_grid(2 * n), kThreads, 0, st>>>(x, n, s, out, gate, it, skip_if_broke);
+  return check_launch("scale_div");
+}
+
+// ------------------------------------------------------------------ extract (K10)
+// x <- x + Mi (V_k y), k and y (coef2) produced on device by cycle_lsq
+// (_extract, gmres.py:294-297).
+__global__ void __launch_bounds__(kThreads)
+extract_kernel(lsb_arnoldi S, double* __restrict__ x, const double* __restrict__ d) {
+  const int k = S.flags->k;
+  if (k < 1 || S.flags->status == LSB_SINGULAR) return;
+  extern __shared__ double sy[];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) sy[j] = S.coef2[j];
+  __syncthreads();
+  const int64_t ld = S.ld;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < S.n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (int j = 0; j < k; ++j) acc = fma(sy[j], S.V[(int64_t)j * ld + r], acc);
+    if (d) acc = __dmul_rn(acc, d[r]);
+    x[r] = x[r] + acc;
+  }
+}
+
+int launch_extract(const lsb_arnoldi& S, double* x, const double* d, cudaStream_t st) {
+  extract_kernel<<<row_grid(2 * S.n), kThreads, sizeof(double) * S.cap, st>>>(S, x, d);
+  return check_launch("extract");
+}
+
+}  // namespace lsb

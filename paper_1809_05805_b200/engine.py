@@ -1,0 +1,315 @@
+"""Device-resident GMRES(m) cycle engine.
+
+One restart cycle of the reference driver (gmres.py:309-466) is enqueued as
+a fixed sequence of liblsb200 launches per Arnoldi iteration:
+
+  one_sync_mgs / pipeline2   SpMV -> K1 lagged_reduce -> [allgather] -> K5 -> K2
+  two_sync_cgs2              SpMV -> K1 -> [ag] -> K5a -> K2 -> K1' -> [ag] -> K5b -> K4
+  mgs_l1                     SpMV -> (p+1) x K8 pass -> [ag each] -> norm -> K5d -> scale
+  cgs2                       SpMV -> K1' -> coef -> project -> K1' -> coef -> project+norm -> K5d -> scale
+
+Convergence, breakdown, the Givens fold and the back-substitution are
+device-side (flags block), so a whole cycle -- including the x update and
+the restart residual/norm -- is launch-only: no host synchronisation inside
+a cycle.  On one GPU the cycle is captured once as a CUDA graph and
+replayed; with a communicator (multi-GPU) it is issued eagerly.  The host
+reads one small report (flags, residuals, scalars) per cycle.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _abi
+from . import _dev as D
+from .operators import device_operator
+
+LAGGED = ("one_sync_mgs", "two_sync_cgs2", "pipeline2")
+DIRECT = ("mgs_l1", "cgs2")
+
+
+class CycleReport:
+    """Host copy of what one cycle produced."""
+
+    __slots__ = ("stop_iter", "status", "broke_iter", "k", "nonfinite", "restart_ok", "res",
+                 "scal")
+
+    def __init__(self, flags, res, scal):
+        self.stop_iter, self.status, self.broke_iter, self.k, self.nonfinite, self.restart_ok = (
+            int(v) for v in flags[:6])
+        self.res = res
+        self.scal = scal
+
+
+class Engine:
+    def __init__(self, A, m, method, rel_tol, btf=1.0, inv_diag=None, comm=None,
+                 diagnostics=False, use_graph=True, n_global=None, op=None):
+        self.dev = D.require_cuda()
+        self.lib = _abi.load()
+        base_op = op if op is not None else device_operator(A)
+        self.method = method
+        self.lagged = method in LAGGED
+        self.comm = comm
+        self.m = int(m)
+        self.n = int(base_op.n_rows)
+        self.n_global = int(n_global or self.n)
+        self.cap = self.m + 2 if self.lagged else self.m + 1
+        self.halo = int(getattr(base_op, "halo", 0))
+        self.off = D.round_up(self.halo, 2)
+        self.ld = D.round_up(self.off + self.n + self.halo, 32)
+        f64 = dict(dtype=D.F64, device=self.dev)
+        self.inv_diag = None
+        if inv_diag is not None:
+            self.inv_diag = self._vec_with_halo()
+            self.inv_diag_view().copy_(torch.as_tensor(np.asarray(inv_diag), **f64)
+                                       if not isinstance(inv_diag, torch.Tensor) else inv_diag)
+            if comm is not None and self.halo:
+                comm.halo(self.inv_diag, self.off, self.n, self.halo)
+            self.op = base_op.with_scale(self.inv_diag[self.off:])
+        else:
+            self.op = base_op
+        # storage
+        self.Vstore = torch.zeros((self.cap, self.ld), **f64)
+        cap, m = self.cap, self.m
+        self.R = torch.zeros((cap, cap), **f64)
+        self.T = torch.zeros((cap, cap), **f64)
+        self.L = torch.zeros((cap, cap), **f64)
+        self.rot = torch.zeros(2 * m, **f64)
+        self.g = torch.zeros(m + 1, **f64)
+        self.tri = torch.zeros((m + 1) * m, **f64)
+        self.coef = torch.zeros(cap, **f64)
+        self.coef2 = torch.zeros(cap, **f64)
+        self.Gloc = torch.zeros(2 * cap, **f64)
+        parts = comm.size if comm is not None else 1
+        self.G = self.Gloc if parts == 1 else torch.zeros(parts * 2 * cap, **f64)
+        self.scal = torch.zeros(_abi.S_COUNT, **f64)
+        self.res = torch.zeros(m + 1, **f64)
+        self.flags = torch.zeros(_abi.FLAGS_INTS, dtype=torch.int32, device=self.dev)
+        self.ws = D.Workspace(cap, self.dev)
+        self.x = self._vec_with_halo()
+        self.b = torch.zeros(self.n, **f64)
+        self.rbuf = torch.zeros(self.n, **f64)
+        self.gram = torch.zeros((cap, cap), **f64) if diagnostics else None
+        self.diagnostics = diagnostics
+        self.S = _abi.Arnoldi(
+            V=self.Vstore.data_ptr() + 8 * self.off, ld=self.ld, n=self.n, n_global=self.n_global,
+            cap=cap, m=m, R=self.R.data_ptr(), T=self.T.data_ptr(), L=self.L.data_ptr(),
+            rot=self.rot.data_ptr(), g=self.g.data_ptr(), tri=self.tri.data_ptr(),
+            coef=self.coef.data_ptr(), coef2=self.coef2.data_ptr(), G=self.G.data_ptr(),
+            g_parts=parts, g_stride=2 * cap, Gloc=self.Gloc.data_ptr(), scal=self.scal.data_ptr(),
+            res=self.res.data_ptr(), flags=self.flags.data_ptr(),
+            ws=_abi.Workspace(self.ws.partial.data_ptr(), self.ws.counter.data_ptr(), 0, 0))
+        self.Sref = C.byref(self.S)
+        self.scal[_abi.S_RELTOL] = float(rel_tol)
+        self.scal[_abi.S_BTF] = float(btf)
+        # host report buffers (pinned)
+        self.h_flags = torch.zeros(_abi.FLAGS_INTS, dtype=torch.int32).pin_memory()
+        self.h_res = torch.zeros(m + 1, dtype=D.F64).pin_memory()
+        self.h_scal = torch.zeros(_abi.S_COUNT, dtype=D.F64).pin_memory()
+        self.use_graph = use_graph and comm is None
+        self.graph = None
+        self.cycles_run = 0
+        self.launches_per_cycle = 0
+        self._count = 0
+        self.timer = None   # list -> CUDA events around K1/K2/SpMV launches (bench.py)
+
+    # ---------------------------------------------------------------- helpers
+    def _vec_with_halo(self):
+        return torch.zeros(self.off + self.n + self.halo + 2, dtype=D.F64, device=self.dev)
+
+    def inv_diag_view(self):
+        return self.inv_diag[self.off:self.off + self.n]
+
+    def x_view(self):
+        return self.x[self.off:self.off + self.n]
+
+    def col_ptr(self, j):
+        return C.c_void_p(self.Vstore.data_ptr() + 8 * (self.off + self.ld * j))
+
+    def col(self, j):
+        return self.Vstore[j, self.off:self.off + self.n]
+
+    _TIMED = {"lsb_lagged_reduce": "lagged_reduce", "lsb_lagged_update": "lagged_update"}
+
+    def _call(self, name, *args):
+        self._count += 1
+        tm = self.timer is not None and name in self._TIMED
+        if tm:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        rc = getattr(self.lib, name)(*args)
+        if rc:
+            _abi.check(rc, name)
+        if tm:
+            e1.record()
+            self.timer.append((self._TIMED[name], int(args[2]), e0, e1))
+
+    def _gather(self, count):
+        """All ranks' local reduction results -> G (one collective)."""
+        if self.comm is not None:
+            self.comm.allgather(self.Gloc, self.G)
+
+    def _apply_op(self, src_tensor_base, src_ptr, dst_ptr, b_ptr, it):
+        if self.comm is not None and self.halo:
+            self.comm.halo(src_tensor_base[0], src_tensor_base[1], self.n, self.halo)
+        self._count += 1
+        tm = self.timer is not None and b_ptr is None
+        if tm:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        self.op.apply_ptr(src_ptr, dst_ptr, b_ptr, C.c_void_p(self.flags.data_ptr()), it,
+                          D.stream())
+        if tm:
+            e1.record()
+            self.timer.append(("spmv", 0, e0, e1))
+
+    def _op_col(self, src_j, dst_j, it):
+        self._apply_op((self.Vstore[src_j], self.off), self.col_ptr(src_j), self.col_ptr(dst_j),
+                       None, it)
+
+    # ---------------------------------------------------------------- phases
+    def load(self, b, x0=None):
+        """Place b and x0 in device memory (H2D when they live on the host)."""
+        self.b.copy_(torch.as_tensor(b) if not isinstance(b, torch.Tensor) else b,
+                     non_blocking=True)
+        xv = self.x_view()
+        if x0 is None:
+            xv.zero_()
+        else:
+            xv.copy_(torch.as_tensor(x0) if not isinstance(x0, torch.Tensor) else x0,
+                     non_blocking=True)
+
+    def _residual_and_norm(self):
+        """rbuf = b - A x; scal[RNORM] = ||rbuf|| (gmres.py:472-473 / 498-500)."""
+        st = D.stream()
+        xp = C.c_void_p(self.x.data_ptr() + 8 * self.off)
+        self._apply_op((self.x, self.off), xp, D.ptr(self.rbuf), D.ptr(self.b), -1)
+        self._call("lsb_norm_partial", D.ptr(self.rbuf), self.n, D.ptr(self.Gloc), self.ws.ref(),
+                   None, -1, st)
+        self._gather(2)
+        self._call("lsb_norm_finish", D.ptr(self.G), self.S.g_parts, D.ptr(self.rbuf), self.n,
+                   C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_RNORM), self.ws.ref(), None, -1,
+                   st)
+
+    def enqueue_prologue(self):
+        self._residual_and_norm()
+        self._call("lsb_restart_check", self.Sref, 1, D.stream())
+
+    def enqueue_cycle(self):
+        st = D.stream()
+        S = self.Sref
+        self._count = 0
+        # V[:,0] = r / beta (gmres.py:396 / 313), fresh small state (392-395)
+        self._call("lsb_scale_div", D.ptr(self.rbuf), self.n,
+                   C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_RNORM), self.col_ptr(0), None, -1, st)
+        self._call("lsb_cycle_begin", S, st)
+        if self.lagged:
+            self._lagged_body(st)
+        else:
+            self._direct_body(st)
+        self._call("lsb_cycle_lsq", S, st)
+        xp = C.c_void_p(self.x.data_ptr() + 8 * self.off)
+        self._call("lsb_cycle_extract", S, xp,
+                   None if self.inv_diag is None else C.c_void_p(self.inv_diag.data_ptr() + 8 * self.off),
+                   st)
+        self._residual_and_norm()
+        self._call("lsb_restart_check", S, 0, st)
+        self.launches_per_cycle = self._count
+
+    def _lagged_body(self, st):
+        S, m = self.Sref, self.m
+        two = self.method == "two_sync_cgs2"
+        for i in range(0, m + 1):
+            p = i + 1
+            self._op_col(i, i + 1, i)                        # V.push(A v_i)
+            self._call("lsb_lagged_reduce", S, i, p, st)     # one pass: [Q^T u, Q^T w]
+            self._gather(2 * p)
+            if not two:
+                self._call("lsb_mgs_lvl2_small", S, i, p, 1, i, st)
+                self._call("lsb_lagged_update", S, i, p, 1, st)
+            else:
+                self._call("lsb_cgs2_lvl2_small_a", S, i, p, 1, i, st)
+                self._call("lsb_lagged_update", S, i, p, 1, st)
+                self._call("lsb_mdot", self.col_ptr(0), self.ld, self.n, p, self.col_ptr(p), None,
+                           D.ptr(self.Gloc), self.ws.ref(), D.ptr(self.flags), i, st)
+                self._gather(p)
+                self._call("lsb_cgs2_lvl2_small_b", S, i, p, st)
+                self._call("lsb_lagged_correct", S, i, p, st)
+            if self.diagnostics:
+                self._call("lsb_gram_row", S, i, i, i + 1, D.ptr(self.gram), self.cap, st)
+
+    def _direct_body(self, st):
+        S, m = self.Sref, self.m
+        if self.diagnostics:
+            self._call("lsb_gram_row", S, 0, 0, 1, D.ptr(self.gram), self.cap, st)
+        for i in range(1, m + 1):
+            p = i
+            self._op_col(i - 1, i, i)                        # z = A v_{i-1}, in place in V[:, i]
+            if self.method == "mgs_l1":
+                for k in range(p + 1):
+                    self._call("lsb_mgs1_pass", S, i, i, k, p, st)
+                    self._gather(2)
+            else:
+                for accumulate in (0, 1):
+                    self._call("lsb_mdot", self.col_ptr(0), self.ld, self.n, p, self.col_ptr(i),
+                               None, D.ptr(self.Gloc), self.ws.ref(), D.ptr(self.flags), i, st)
+                    self._gather(p)
+                    self._call("lsb_collect_coef", S, i, p, accumulate, st)
+                    self._call("lsb_cgs_project", S, i, i, p, accumulate, st)
+                self._gather(2)
+            self._call("lsb_norm_finish", D.ptr(self.G), self.S.g_parts, self.col_ptr(i), self.n,
+                       C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_BETA), self.ws.ref(),
+                       D.ptr(self.flags), i, st)
+            self._call("lsb_direct_small", S, i, i, p, st)
+            self._call("lsb_direct_normalize", S, i, i, st)
+            if self.diagnostics:
+                self._call("lsb_gram_row", S, i, i, i + 1, D.ptr(self.gram), self.cap, st)
+
+    # ---------------------------------------------------------------- driving
+    def prologue(self):
+        self.enqueue_prologue()
+        return self.report()
+
+    def cycle(self):
+        if self.use_graph and self.cycles_run >= 1:
+            if self.graph is None:
+                self.graph = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    with torch.cuda.graph(self.graph, stream=side):
+                        self.enqueue_cycle()
+                torch.cuda.current_stream().wait_stream(side)
+            self.graph.replay()
+        else:
+            self.enqueue_cycle()
+        self.cycles_run += 1
+        return self.report()
+
+    def report(self):
+        self.h_flags.copy_(self.flags, non_blocking=True)
+        self.h_res.copy_(self.res, non_blocking=True)
+        self.h_scal.copy_(self.scal, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return CycleReport(self.h_flags.tolist(), self.h_res.numpy().copy(),
+                           self.h_scal.numpy().copy())
+
+    def hessenberg(self, k):
+        """Hbar_k from the R columns (R[:, j+1] rows 0..j+1 = H[:, j])."""
+        R = self.R.cpu().numpy()
+        H = np.zeros((k + 1, k))
+        for j in range(k):
+            H[: j + 2, j] = R[: j + 2, j + 1]
+        return H
+
+    def basis(self, k, ncols):
+        B = np.zeros((self.n, k + 1))
+        c = min(ncols, k + 1)
+        if c > 0:
+            B[:, :c] = self.Vstore[:c, self.off:self.off + self.n].t().cpu().numpy()
+        return B

@@ -1,0 +1,451 @@
+"""Drop-in GMRES drivers of lowsync.gmres (reference gmres.py), on B200.
+
+The restart shell, history and ledger stay on the host exactly as in the
+reference (gmres.py:470-516); each restart cycle runs on the device
+(engine.Engine) with one host synchronisation per cycle.  The ledger is
+reconstructed from the cycle report with the reference's exact event
+schedule (kind, scalar_count, iteration attribution, overlap_eligible),
+including pipeline2's depth-2 look-ahead.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from . import _abi
+from . import _dev as D
+from .diagnostics import gram_orthogonality_loss, gram_paige_metric
+from .engine import Engine
+from .errors import HappyBreakdown, NonFiniteError, SingularHessenberg
+from .kernels import DOT, FUSED, MDOT, NORM, ReductionLedger
+
+CONVERGED = "converged"
+STALLED_MAXITER = "stalled_maxiter"
+BREAKDOWN = "breakdown"
+CANCELLATION_FAILURE = "cancellation_failure"
+
+METHODS = ("mgs_l1", "cgs1_ghysels", "cgs2", "two_sync_cgs2", "one_sync_mgs", "pipeline2")
+_ALIASES = {
+    "mgs-l1": "mgs_l1", "mgs": "mgs_l1",
+    "cgs1-ghysels": "cgs1_ghysels", "ghysels": "cgs1_ghysels",
+    "two-sync": "two_sync_cgs2", "two_sync": "two_sync_cgs2",
+    "one-sync": "one_sync_mgs", "one_sync": "one_sync_mgs",
+}
+DEVICE_METHODS = ("mgs_l1", "cgs2", "two_sync_cgs2", "one_sync_mgs", "pipeline2")
+
+
+def canonical_method(name):
+    """gmres.py:78-84."""
+    key = name.strip().lower()
+    key = _ALIASES.get(key, key)
+    if key not in METHODS:
+        raise ValueError(f"unknown method {name!r}; choose from {METHODS}")
+    return key
+
+
+@dataclass
+class GmresConfig:
+    """gmres.py:87-103."""
+    restart_m: int = 50
+    max_restarts: int = 10
+    rel_tol: float = 1e-6
+    method: str = "one_sync_mgs"
+    precond: str = "none"
+    breakdown_tol_factor: float = 1.0
+
+    def __post_init__(self):
+        if self.restart_m < 1:
+            raise ValueError("restart_m must be >= 1")
+        if not self.rel_tol > 0.0:
+            raise ValueError("rel_tol must be positive")
+        self.method = canonical_method(self.method)
+        if self.precond not in ("none", "jacobi"):
+            raise ValueError("precond must be 'none' or 'jacobi'")
+
+
+class Preconditioner:
+    """Right preconditioner: identity or Jacobi (gmres.py:106-118)."""
+
+    def __init__(self, kind, A=None):
+        if kind not in ("none", "jacobi"):
+            raise ValueError("precond must be 'none' or 'jacobi'")
+        self.kind = kind
+        self.inv_diag = None
+        if kind == "jacobi":
+            d = np.asarray(A.diagonal_values(), dtype=np.float64)
+            if np.any(d == 0.0):
+                raise ValueError("jacobi preconditioner requires a zero-free diagonal")
+            self.inv_diag = 1.0 / d
+
+
+def apply_preconditioner(precond, v):
+    """M^{-1} v (gmres.py:121-126); elementwise product on the device."""
+    host = D.is_host(v)
+    vv = D.to_device_vector(v)
+    if precond is None or precond.kind == "none":
+        return D.out_like(vv, host)
+    d = D.to_device_vector(precond.inv_diag, vv.shape[0])
+    out = torch.empty_like(vv)
+    # v * inv_diag (one rounding) through K6's column-scaling path: a
+    # one-point identity stencil computes 1.0 * (v[r] * d[r]) exactly.
+    from .operators import StencilMatrix
+    S = StencilMatrix((vv.shape[0], 1, 1), [((0, 0, 0), 1.0)])
+    S.device_op().with_scale(d).apply(vv, out)
+    return D.out_like(out, host)
+
+
+class GivensState:
+    """Rotations, rotated triangle and rhs on the device (gmres.py:129-140)."""
+
+    def __init__(self, m, beta):
+        dev = D.require_cuda()
+        self.m = int(m)
+        self._rot = torch.zeros(2 * max(m, 1), dtype=D.F64, device=dev)
+        self.g = torch.zeros(m + 1, dtype=D.F64, device=dev)
+        self.g[0] = float(beta)
+        self.tri = torch.zeros((m + 1, m), dtype=D.F64, device=dev)
+        self._count = 0
+
+    @property
+    def rotations(self):
+        r = self._rot[: 2 * self._count].cpu().numpy()
+        return [(float(r[2 * k]), float(r[2 * k + 1])) for k in range(self._count)]
+
+
+def givens_update(state, h_col, i):
+    """Fold Hessenberg column i (1-based, i+1 entries); returns |g[i]|
+    (gmres.py:153-177) -- the same device code the solver cycle runs."""
+    if state._count != i - 1:
+        raise ValueError(f"expected {i - 1} prior rotations, have {state._count}")
+    h = D.to_device_vector(h_col)
+    if h.shape[0] != i + 1:
+        raise ValueError(f"column {i} must have {i + 1} entries")
+    res = torch.empty(1, dtype=D.F64, device=h.device)
+    _abi.call("lsb_givens_update", D.ptr(state._rot), D.ptr(state.g), D.ptr(state.tri),
+              state.m, D.ptr(h), i, D.ptr(res), D.stream())
+    state._count += 1
+    return float(res.item())
+
+
+def solve_least_squares(state, k):
+    """Back-substitution of the rotated k x k triangle (gmres.py:184-192)."""
+    y = torch.zeros(max(k, 1), dtype=D.F64, device=state.g.device)
+    st = torch.zeros(1, dtype=torch.int32, device=state.g.device)
+    _abi.call("lsb_back_substitute", D.ptr(state.tri.contiguous()), D.ptr(state.g), state.m, k,
+              D.ptr(y), D.ptr(st), D.stream())
+    bad = int(st.item())
+    if bad >= 0:
+        raise SingularHessenberg(f"zero diagonal at {bad}")
+    return y[:k].cpu().numpy()
+
+
+@dataclass
+class IterationRecord:
+    iteration: int
+    implicit_rel_res: float
+    true_rel_res: float | None = None
+    s_norm: float | None = None
+    orth_loss: float | None = None
+    reductions: int = 0
+
+
+class ConvergenceHistory:
+    """Per-iteration records (gmres.py:205-236).  ``basis`` / ``hessenberg``
+    are materialised from the device on first access (the reference copies
+    V every cycle, 5.5 s/cycle at 256^3; here it costs nothing unless read)."""
+
+    def __init__(self):
+        self.records: list[IterationRecord] = []
+        self.outcome: str | None = None
+        self.denom = 1.0
+        self.cycle_starts: list[int] = []
+        self.k = 0
+        self.final_true_rel_res = None
+        self.method = None
+        self._stash = None
+        self._basis = None
+        self._hess = None
+
+    @property
+    def iterations(self):
+        return len(self.records)
+
+    def implicit_curve(self):
+        return np.array([r.implicit_rel_res for r in self.records])
+
+    def stall_iteration(self, level=0.99):
+        for rec in self.records:
+            if rec.s_norm is not None and rec.s_norm >= level:
+                return rec.iteration
+        return None
+
+    @property
+    def basis(self):
+        if self._basis is None and self._stash is not None:
+            eng, k, ncols = self._stash
+            self._basis = eng.basis(k, ncols)
+        return self._basis
+
+    @basis.setter
+    def basis(self, v):
+        self._basis = v
+
+    @property
+    def hessenberg(self):
+        if self._hess is None and self._stash is not None:
+            eng, k, _ = self._stash
+            self._hess = eng.hessenberg(k)
+        return self._hess
+
+    @hessenberg.setter
+    def hessenberg(self, v):
+        self._hess = v
+
+    def release(self):
+        """Drop the device basis kept alive for lazy ``basis`` access
+        (without copying it: unread attachments are simply discarded)."""
+        self._stash = None
+
+
+class _DeviceSolve:
+    """One solve: host restart shell over device cycles (gmres.py:239-516)."""
+
+    def __init__(self, A, b, x0, config, ledger, diagnostics_every, true_residual_every,
+                 use_graph=True):
+        if A.n_rows != A.n_cols:
+            raise ValueError("GMRES needs a square matrix")
+        if config.method not in DEVICE_METHODS:
+            raise NotImplementedError(
+                f"method {config.method!r} is outside the B200 hot path (SURVEY §8f)")
+        if true_residual_every:
+            raise NotImplementedError("true_residual_every is not supported on the device path")
+        self.A = A
+        self.n = A.n_rows
+        self.host = D.is_host(b)
+        self.b = D.to_device_vector(b, self.n)
+        if not bool((self.b != 0).any()):
+            raise ValueError("right-hand side must be nonzero")
+        self.x0 = None if x0 is None else D.to_device_vector(x0, self.n)
+        self.config = config
+        self.ledger = ledger if ledger is not None else ReductionLedger()
+        self.pc = Preconditioner(config.precond, A)
+        self.m = min(config.restart_m, self.n)
+        self.diag_every = diagnostics_every
+        self.history = ConvergenceHistory()
+        self.history.method = config.method
+        self.global_it = 0
+        self.use_graph = use_graph
+
+    def _events_lagged(self, base, k, stop, broke_iter, two, pipeline):
+        """Ledger events + per-iteration reduction counts of one lagged cycle
+        (gmres.py:397-462)."""
+        led = self.ledger
+        led.iteration = base
+        led.record(FUSED, 2)
+        if two:
+            led.record(MDOT, 1)
+        nred = {}
+
+        def advance(i, eligible):
+            led.iteration = base + i
+            mark = len(led)
+            led.record(FUSED, 2 * (i + 1), eligible)
+            if two and broke_iter != i:
+                led.record(MDOT, i + 1, eligible)
+            nred[i] = len(led) - mark
+            return broke_iter == i
+
+        if not pipeline:
+            for i in range(1, k + 1):
+                advance(i, False)
+        else:
+            i, done = 1, False
+            while i <= self.m and not done:
+                pair = [i] if i == self.m else [i, i + 1]
+                for t in pair:
+                    br = advance(t, True)
+                    if br:
+                        break
+                if stop is not None and stop in pair:
+                    done = True
+                i += len(pair)
+        return nred
+
+    def _events_direct(self, i, two_pass):
+        led = self.ledger
+        mark = len(led)
+        if two_pass:
+            led.record(MDOT, i)
+            led.record(MDOT, i)
+        else:
+            for _ in range(i):
+                led.record(DOT, 1)
+        led.record(NORM, 1)
+        return len(led) - mark
+
+    def run(self):
+        cfg = self.config
+        led = self.ledger
+        hist = self.history
+        inv = self.pc.inv_diag
+        eng = Engine(self.A, self.m, cfg.method, cfg.rel_tol, cfg.breakdown_tol_factor,
+                     inv_diag=inv, diagnostics=bool(self.diag_every), use_graph=self.use_graph)
+        self.engine = eng
+        eng.load(self.b, self.x0)
+        led.iteration = 0
+        rep = eng.prologue()
+        if rep.nonfinite:
+            raise NonFiniteError("spmv result contains NaN or Inf")
+        beta = float(rep.scal[_abi.S_RNORM])
+        if np.isnan(beta):
+            raise NonFiniteError("norm2 input contains NaN")
+        led.record(NORM, 1)
+        hist.denom = beta if beta > 0.0 else 1.0
+        if beta == 0.0:
+            hist.outcome = CONVERGED
+            hist.final_true_rel_res = 0.0
+            return self._result(eng)
+        target = cfg.rel_tol * beta
+        outcome = None
+        lagged = cfg.method in ("one_sync_mgs", "two_sync_cgs2", "pipeline2")
+        for _cycle in range(cfg.max_restarts):
+            hist.cycle_starts.append(self.global_it)
+            rep = eng.cycle()
+            if rep.nonfinite:
+                raise NonFiniteError("spmv result contains NaN or Inf")
+            if rep.status == _abi.STARTUP_BREAKDOWN:
+                raise HappyBreakdown(0, float(rep.scal[_abi.S_BETA]), float(rep.scal[_abi.S_TOL]),
+                                     r_col=np.zeros(0))
+            if rep.status == _abi.SINGULAR:
+                raise SingularHessenberg(f"zero diagonal at {rep.k}")
+            stopped = rep.stop_iter != _abi.NO_STOP
+            k = rep.stop_iter if stopped else self.m
+            broke = rep.broke_iter if rep.broke_iter >= 1 else None
+            gram = eng.gram.cpu().numpy() if self.diag_every else None
+            base = self.global_it
+            if lagged:
+                nred = self._events_lagged(base, k, k if stopped else None, broke,
+                                           cfg.method == "two_sync_cgs2",
+                                           cfg.method == "pipeline2")
+                for i in range(1, k + 1):
+                    self.global_it = base + i
+                    ncols = i if broke == i else i + 1
+                    self._record(rep.res[i], nred[i], gram, ncols)
+            else:
+                for i in range(1, k + 1):
+                    self.global_it += 1
+                    led.iteration = self.global_it
+                    nr = self._events_direct(i, cfg.method == "cgs2")
+                    ncols = i if broke == i else i + 1
+                    self._record(rep.res[i], nr, gram, ncols)
+            if stopped:
+                status = CONVERGED if rep.status == _abi.CONVERGED else BREAKDOWN
+            else:
+                status = "full"
+            if lagged:
+                ncols_norm = k + (0 if status == BREAKDOWN else 1)
+            else:
+                ncols_norm = k if broke == k else k + 1
+            hist.k = k
+            hist._stash = (eng, k, ncols_norm)
+            hist._basis = hist._hess = None
+            if status in (CONVERGED, BREAKDOWN):
+                outcome = status
+                break
+            led.iteration = self.global_it
+            led.record(NORM, 1)
+            beta = float(rep.scal[_abi.S_RNORM])
+            rel = beta / hist.denom
+            if hist.records:
+                hist.records[-1].true_rel_res = rel
+            if beta <= target:
+                outcome = CONVERGED
+                break
+        if outcome is None:
+            outcome = STALLED_MAXITER
+        led.iteration = self.global_it
+        led.record(NORM, 1)
+        final_rel = float(rep.scal[_abi.S_RNORM]) / hist.denom
+        hist.final_true_rel_res = final_rel
+        if hist.records:
+            hist.records[-1].true_rel_res = final_rel
+        hist.outcome = outcome
+        return self._result(eng)
+
+    def _record(self, res, nred, gram, ncols):
+        s = o = None
+        if self.diag_every and self.global_it % self.diag_every == 0:
+            Gm = gram[:ncols, :ncols]
+            Gm = np.triu(Gm.T, 0) + np.triu(Gm.T, 1).T  # rows hold Q^T q_row: symmetrise
+            s, o = gram_paige_metric(Gm), gram_orthogonality_loss(Gm)
+        self.history.records.append(IterationRecord(
+            iteration=self.global_it, implicit_rel_res=float(res) / self.history.denom,
+            s_norm=s, orth_loss=o, reductions=nred))
+
+    def _result(self, eng):
+        x = eng.x_view().clone()
+        return D.out_like(x, self.host), self.history
+
+
+def _run(method, A, b, x0, config, ledger, diagnostics_every, true_residual_every):
+    config = replace(config, method=method) if config is not None else GmresConfig(method=method)
+    if method == "cgs1_ghysels":
+        raise NotImplementedError("cgs1_ghysels is outside the B200 hot path (SURVEY §8f)")
+    return _DeviceSolve(A, b, x0, config, ledger, diagnostics_every, true_residual_every).run()
+
+
+def gmres_mgs_l1(A, b, x0=None, config=None, ledger=None, diagnostics_every=1,
+                 true_residual_every=0):
+    """Level-1 MGS GMRES: i + 1 reductions at iteration i (gmres.py:526-530)."""
+    return _run("mgs_l1", A, b, x0, config, ledger, diagnostics_every, true_residual_every)
+
+
+def gmres_cgs2(A, b, x0=None, config=None, ledger=None, diagnostics_every=1,
+               true_residual_every=0):
+    """Two-pass classical GS GMRES: 3 reductions per iteration (gmres.py:533-537)."""
+    return _run("cgs2", A, b, x0, config, ledger, diagnostics_every, true_residual_every)
+
+
+def gmres_cgs1_ghysels(A, b, x0=None, config=None, ledger=None, diagnostics_every=1,
+                       true_residual_every=0):
+    """Not on the B200 path: raises NotImplementedError."""
+    return _run("cgs1_ghysels", A, b, x0, config, ledger, diagnostics_every, true_residual_every)
+
+
+def gmres_two_sync(A, b, x0=None, config=None, ledger=None, diagnostics_every=1,
+                   true_residual_every=0):
+    """Lagged two-pass classical GMRES: 2 reductions per iteration (gmres.py:551-555)."""
+    return _run("two_sync_cgs2", A, b, x0, config, ledger, diagnostics_every, true_residual_every)
+
+
+def gmres_one_sync(A, b, x0=None, config=None, ledger=None, diagnostics_every=1,
+                   true_residual_every=0):
+    """Lagged compact-WY MGS GMRES: 1 reduction per iteration (gmres.py:558-562)."""
+    return _run("one_sync_mgs", A, b, x0, config, ledger, diagnostics_every, true_residual_every)
+
+
+def gmres_pipeline2(A, b, x0=None, config=None, ledger=None, diagnostics_every=1,
+                    true_residual_every=0):
+    """Depth-2 schedule of one_sync; bitwise-identical history, reductions
+    tagged overlap_eligible (gmres.py:565-576)."""
+    return _run("pipeline2", A, b, x0, config, ledger, diagnostics_every, true_residual_every)
+
+
+_DISPATCH = {
+    "mgs_l1": gmres_mgs_l1,
+    "cgs2": gmres_cgs2,
+    "cgs1_ghysels": gmres_cgs1_ghysels,
+    "two_sync_cgs2": gmres_two_sync,
+    "one_sync_mgs": gmres_one_sync,
+    "pipeline2": gmres_pipeline2,
+}
+
+
+def solve(A, b, x0=None, config=None, ledger=None, diagnostics_every=1, true_residual_every=0):
+    """Dispatch on config.method (gmres.py:589-594)."""
+    config = config if config is not None else GmresConfig()
+    return _DISPATCH[config.method](A, b, x0, config, ledger, diagnostics_every,
+                                    true_residual_every)

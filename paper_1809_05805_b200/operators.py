@@ -1,0 +1,236 @@
+"""Device operators that feed the Arnoldi loop: K7 CSR and K6 box stencils.
+
+Both reproduce the reference SpMV (kernels.py:256-272) bit for bit.  The
+stencil operators are matrix-free (16 B/row of compulsory HBM traffic) and
+duck-type the reference CsrMatrix (n_rows, n_cols, nnz, row_ptr, col_idx,
+values, to_dense, diagonal_values, frobenius_norm), materialising the CSR
+arrays only if a caller asks for them.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _abi
+from . import _dev as D
+
+
+class CsrOperator:
+    """Device copy of a CsrMatrix with 32-bit indices."""
+
+    def __init__(self, A, col_scale=None):
+        dev = D.require_cuda()
+        if A.nnz >= 2 ** 31 or A.n_rows >= 2 ** 31:
+            raise ValueError("CSR kernel supports nnz < 2^31")
+        self.n_rows, self.n_cols = A.n_rows, A.n_cols
+        self.row_ptr = torch.as_tensor(A.row_ptr.astype(np.int32), device=dev)
+        self.col_idx = torch.as_tensor(A.col_idx.astype(np.int32), device=dev)
+        self.values = torch.as_tensor(A.values, device=dev)
+        self.col_scale = col_scale
+        self.halo = 0
+        self.c = _abi.Csr(A.n_rows, A.n_cols, A.nnz, self.row_ptr.data_ptr(),
+                          self.col_idx.data_ptr(), self.values.data_ptr(),
+                          col_scale.data_ptr() if col_scale is not None else None, 0, 0)
+
+    def with_scale(self, col_scale):
+        op = object.__new__(CsrOperator)
+        op.__dict__.update(self.__dict__)
+        op.col_scale = col_scale
+        op.c = _abi.Csr(self.c.n_rows, self.c.n_cols, self.c.nnz, self.c.row_ptr, self.c.col_idx,
+                        self.c.values, col_scale.data_ptr() if col_scale is not None else None,
+                        0, 0)
+        return op
+
+    @property
+    def h2d_bytes(self):
+        return 4 * (self.n_rows + 1) + 12 * int(self.values.shape[0])
+
+    def apply_ptr(self, xp, yp, bp=None, flagsp=None, it=-1, stream=None):
+        _abi.call("lsb_spmv_csr", C.byref(self.c), xp, bp, yp, flagsp, it, stream or D.stream())
+
+    def apply(self, x, y, b=None, flags=None, it=-1):
+        self.apply_ptr(D.ptr(x), D.ptr(y), D.ptr(b), D.ptr(flags), it)
+
+
+def _offsets_7():
+    offs = [((0, 0, 0), 6.0)]
+    for ax in range(3):
+        for s in (-1, 1):
+            d = [0, 0, 0]
+            d[ax] = s
+            offs.append((tuple(d), -1.0))
+    return offs
+
+
+def _offsets_5():
+    return [((0, 0, 0), 4.0), ((-1, 0, 0), -1.0), ((1, 0, 0), -1.0), ((0, -1, 0), -1.0),
+            ((0, 1, 0), -1.0)]
+
+
+def convdiff27_offsets(pe=0.5):
+    """27-point convection-diffusion: centre 26,
+    every neighbour -1, face neighbours also carry central convection
+    pe*(dx+dy+dz), i.e. -1+pe downstream and -1-pe upstream."""
+    offs = []
+    for dz in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                if dx == dy == dz == 0:
+                    offs.append(((0, 0, 0), 26.0))
+                elif abs(dx) + abs(dy) + abs(dz) == 1:
+                    offs.append(((dx, dy, dz), -1.0 + pe * (dx + dy + dz)))
+                else:
+                    offs.append(((dx, dy, dz), -1.0))
+    return offs
+
+
+class StencilMatrix:
+    """Constant-coefficient Dirichlet stencil on an nx x ny x nz box,
+    row i = (iz*ny + iy)*nx + ix; the CSR it stands for has each row's
+    columns in increasing order, exactly what CsrMatrix.from_coo builds
+    from the same triples (so gen_laplace2d's matrix is reproduced)."""
+
+    def __init__(self, dims, offsets, name="stencil"):
+        self.dims = tuple(int(d) for d in dims)
+        nx, ny, nz = self.dims
+        self.name = name
+        key = lambda o: (o[0][2] * ny + o[0][1]) * nx + o[0][0]  # noqa: E731
+        self.offsets = sorted(offsets, key=key)
+        self.n_rows = self.n_cols = nx * ny * nz
+        self._csr = None
+        self._dev = None
+
+    # -- CsrMatrix duck typing (materialised lazily, host only)
+    def _materialise(self):
+        if self._csr is None:
+            from .kernels import CsrMatrix
+            nx, ny, nz = self.dims
+            ix = np.arange(nx); iy = np.arange(ny); iz = np.arange(nz)
+            pres, lins, vals = [], [], []
+            for (dx, dy, dz), v in self.offsets:
+                mx = (ix + dx >= 0) & (ix + dx < nx)
+                my = (iy + dy >= 0) & (iy + dy < ny)
+                mz = (iz + dz >= 0) & (iz + dz < nz)
+                pres.append((mz[:, None, None] & my[None, :, None] & mx[None, None, :]).ravel())
+                lins.append((dz * ny + dy) * nx + dx)
+                vals.append(v)
+            P = np.stack(pres, axis=1)
+            ptr = np.zeros(self.n_rows + 1, dtype=np.int64)
+            np.cumsum(P.sum(axis=1), out=ptr[1:])
+            cols = (np.arange(self.n_rows, dtype=np.int64)[:, None] + np.array(lins)[None, :])[P]
+            v = np.broadcast_to(np.array(vals, dtype=np.float64)[None, :], P.shape)[P]
+            self._csr = CsrMatrix(self.n_rows, self.n_cols, ptr, cols, v)
+        return self._csr
+
+    @property
+    def nnz(self):
+        nx, ny, nz = self.dims
+        tot = 0
+        for (dx, dy, dz), _ in self.offsets:
+            tot += (nx - abs(dx)) * (ny - abs(dy)) * (nz - abs(dz))
+        return tot
+
+    @property
+    def shape(self):
+        return (self.n_rows, self.n_cols)
+
+    @property
+    def row_ptr(self):
+        return self._materialise().row_ptr
+
+    @property
+    def col_idx(self):
+        return self._materialise().col_idx
+
+    @property
+    def values(self):
+        return self._materialise().values
+
+    def to_csr(self):
+        return self._materialise()
+
+    def to_dense(self):
+        return self._materialise().to_dense()
+
+    def diagonal_values(self):
+        c = [v for (o, v) in self.offsets if o == (0, 0, 0)]
+        return np.full(self.n_rows, c[0] if c else 0.0)
+
+    def frobenius_norm(self):
+        nx, ny, nz = self.dims
+        s = 0.0
+        for (dx, dy, dz), v in self.offsets:
+            s += (nx - abs(dx)) * (ny - abs(dy)) * (nz - abs(dz)) * v * v
+        return float(np.sqrt(s))
+
+    def device_op(self):
+        if self._dev is None:
+            self._dev = StencilOperator(self)
+        return self._dev
+
+
+class StencilOperator:
+    """K6 launcher; optional z-slab partition (rows of planes [z0, z0+nzl))
+    with ghost planes supplied by the caller next to x."""
+
+    def __init__(self, S, col_scale=None, z0=0, nz_local=None):
+        D.require_cuda()
+        nx, ny, nz = S.dims
+        nzl = nz if nz_local is None else nz_local
+        self.stencil = S
+        self.n_rows = self.n_cols = nx * ny * nzl
+        self.plane = nx * ny
+        self.halo_lo = int(z0 > 0)
+        self.halo_hi = int(z0 + nzl < nz)
+        self.halo = self.plane if (self.halo_lo or self.halo_hi) else 0
+        self.col_scale = col_scale
+        c = _abi.Stencil()
+        c.nx, c.ny, c.nz, c.noff = nx, ny, nzl, len(S.offsets)
+        c.halo_lo, c.halo_hi = self.halo_lo, self.halo_hi
+        for k, ((dx, dy, dz), v) in enumerate(S.offsets):
+            c.dx[k], c.dy[k], c.dz[k], c.val[k] = dx, dy, dz, v
+        c.col_scale = col_scale.data_ptr() if col_scale is not None else None
+        self.c = c
+        self.h2d_bytes = 0
+
+    def with_scale(self, col_scale):
+        op = object.__new__(StencilOperator)
+        op.__dict__.update(self.__dict__)
+        c = _abi.Stencil()
+        C.pointer(c)[0] = self.c
+        c.col_scale = col_scale.data_ptr() if col_scale is not None else None
+        op.c = c
+        op.col_scale = col_scale
+        return op
+
+    def apply_ptr(self, xp, yp, bp=None, flagsp=None, it=-1, stream=None):
+        _abi.call("lsb_spmv_stencil", C.byref(self.c), xp, bp, yp, flagsp, it, stream or D.stream())
+
+    def apply(self, x, y, b=None, flags=None, it=-1):
+        self.apply_ptr(D.ptr(x), D.ptr(y), D.ptr(b), D.ptr(flags), it)
+
+
+def laplace2d(nx):
+    """5-point Laplacian (reference harness.py:119-136) as a stencil."""
+    return StencilMatrix((nx, nx, 1), _offsets_5(), "laplace2d")
+
+
+def laplace3d(N, dims=None):
+    """7-point Laplacian, the 3D analogue."""
+    return StencilMatrix(dims or (N, N, N), _offsets_7(), "laplace3d")
+
+
+def convdiff27(N, pe=0.5, dims=None):
+    """27-point convection-diffusion."""
+    return StencilMatrix(dims or (N, N, N), convdiff27_offsets(pe), "convdiff27")
+
+
+def device_operator(A):
+    if hasattr(A, "device_op"):
+        return A.device_op()
+    if hasattr(A, "apply_ptr"):
+        return A
+    raise TypeError(f"unsupported operator {type(A).__name__}")
