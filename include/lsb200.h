@@ -165,11 +165,12 @@ int lsb_maxpy(const double* y, const double* X, int64_t ld, int64_t n, int32_t p
 /* out2[0] = max|x|, out2[1] = sum x^2 (local, deterministic). */
 int lsb_norm_partial(const double* x, int64_t n, double* out2, const lsb_workspace* ws,
                      const lsb_flags* flags, int32_t it, void* stream);
-/* *out = ||x||_2 from nparts stacked (amax, ssq) pairs; if max|x| is outside
- * [2^-450, 2^450] it re-reads x with an exact power-of-two scaling (local
- * only, nparts == 1) -- the overflow-safe contract of norm2 (kernels.py:283-298). */
-int lsb_norm_finish(const double* parts, int32_t nparts, const double* x, int64_t n,
-                    double* out, const lsb_workspace* ws, const lsb_flags* flags,
+/* *out = ||x||_2 from nparts (amax, ssq) pairs stacked part_stride doubles
+ * apart; if max|x| is outside [2^-450, 2^450] it re-reads x with an exact
+ * power-of-two scaling (local only, nparts == 1) -- the overflow-safe
+ * contract of norm2 (kernels.py:283-298). */
+int lsb_norm_finish(const double* parts, int32_t nparts, int32_t part_stride, const double* x,
+                    int64_t n, double* out, const lsb_workspace* ws, const lsb_flags* flags,
                     int32_t it, void* stream);
 
 /* out = x / (*s) elementwise (device scalar s; e.g. V.push(r / beta)). */

@@ -85,7 +85,7 @@ _SIGS = {
     "lsb_mdot": ([_P, _I64, _I64, _I32, _P, _P, _P, _P, _P, _I32, _P], C.c_int),
     "lsb_maxpy": ([_P, _P, _I64, _I64, _I32, _P, _I32, _P, _P, _I32, _P], C.c_int),
     "lsb_norm_partial": ([_P, _I64, _P, _P, _P, _I32, _P], C.c_int),
-    "lsb_norm_finish": ([_P, _I32, _P, _I64, _P, _P, _P, _I32, _P], C.c_int),
+    "lsb_norm_finish": ([_P, _I32, _I32, _P, _I64, _P, _P, _P, _I32, _P], C.c_int),
     "lsb_scale_div": ([_P, _I64, _P, _P, _P, _I32, _P], C.c_int),
     "lsb_lagged_reduce": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_mgs_lvl2_small": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),

@@ -49,7 +49,8 @@ def to_device_vector(x, n=None, copy=False):
     if isinstance(x, torch.Tensor):
         t = x.to(device=dev, dtype=F64)
     else:
-        t = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=dev)
+        a = np.ascontiguousarray(x, dtype=np.float64)
+        t = h2d(a, dev) if a.ndim == 1 and a.size >= _STAGE_MIN else torch.as_tensor(a, device=dev)
     if t.dim() != 1:
         raise DimensionError(f"expected a vector, got shape {tuple(t.shape)}")
     if n is not None and t.shape[0] != n:
@@ -91,8 +92,40 @@ def colmajor(X):
 def out_like(t, like_host):
     """Return a device result in the caller's world (numpy in -> numpy out)."""
     if like_host:
+        if t.dim() == 1 and t.numel() >= _STAGE_MIN:
+            return d2h(t)
         return t.detach().cpu().numpy()
     return t
+
+
+# Large host<->device vector copies go through one cached pinned staging
+# buffer: pageable cudaMemcpy of a 134 MB vector runs at ~2 GB/s on the
+# B200 host, pinned DMA at ~50 GB/s plus a ~40 GB/s host memcpy.
+_STAGE_MIN = 1 << 16
+_stage = None
+
+
+def _staging(n):
+    global _stage
+    if _stage is None or _stage.numel() < n:
+        _stage = torch.empty(max(n, 1 << 20), dtype=F64).pin_memory()
+    return _stage[:n]
+
+
+def h2d(a, dev):
+    st = _staging(a.size)
+    st.numpy()[:] = a
+    out = torch.empty(a.size, dtype=F64, device=dev)
+    out.copy_(st, non_blocking=True)
+    torch.cuda.current_stream().synchronize()   # staging buffer is reused
+    return out
+
+
+def d2h(t):
+    st = _staging(t.numel())
+    st.copy_(t.detach(), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return st.numpy().copy()
 
 
 class Workspace:

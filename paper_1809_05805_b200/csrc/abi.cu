@@ -39,8 +39,8 @@ int launch_mgs1_pass(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int launch_cgs_project(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int launch_norm_partial(const double*, int64_t, double*, const lsb_workspace*, const lsb_flags*,
                         int, cudaStream_t);
-int launch_norm_finish(const double*, int, const double*, int64_t, double*, const lsb_workspace*,
-                       const lsb_flags*, int, cudaStream_t);
+int launch_norm_finish(const double*, int, int, const double*, int64_t, double*,
+                       const lsb_workspace*, const lsb_flags*, int, cudaStream_t);
 int launch_scale_div(const double*, int64_t, const double*, double*, const lsb_flags*, int, int,
                      cudaStream_t);
 int launch_extract(const lsb_arnoldi&, double*, const double*, cudaStream_t);
@@ -115,10 +115,11 @@ int lsb_norm_partial(const double* x, int64_t n, double* out2, const lsb_workspa
   return launch_norm_partial(x, n, out2, ws, flags, it, S_(stream));
 }
 
-int lsb_norm_finish(const double* parts, int32_t nparts, const double* x, int64_t n, double* out,
-                    const lsb_workspace* ws, const lsb_flags* flags, int32_t it, void* stream) {
-  if (nparts < 1 || !ws) return LSB_EINVAL;
-  return launch_norm_finish(parts, nparts, x, n, out, ws, flags, it, S_(stream));
+int lsb_norm_finish(const double* parts, int32_t nparts, int32_t part_stride, const double* x,
+                    int64_t n, double* out, const lsb_workspace* ws, const lsb_flags* flags,
+                    int32_t it, void* stream) {
+  if (nparts < 1 || !ws || (nparts > 1 && part_stride < 2)) return LSB_EINVAL;
+  return launch_norm_finish(parts, nparts, part_stride, x, n, out, ws, flags, it, S_(stream));
 }
 
 int lsb_scale_div(const double* x, int64_t n, const double* s, double* out,

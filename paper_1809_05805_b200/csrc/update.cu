@@ -285,12 +285,15 @@ int launch_norm_partial(const double* x, int64_t n, double* out2, const lsb_work
 // an exact power-of-two scale (no rounding from the scaling itself), the
 // overflow/underflow-safe path of the reference's amax-scaled norm.
 __global__ void __launch_bounds__(kThreads)
-norm_finish_kernel(const double* parts, int nparts, const double* __restrict__ x, int64_t n,
-                   double* out, double* partial, unsigned* counter, const lsb_flags* gate,
-                   int it) {
+norm_finish_kernel(const double* parts, int nparts, int stride, const double* __restrict__ x,
+                   int64_t n, double* out, double* partial, unsigned* counter,
+                   const lsb_flags* gate, int it) {
   if (gated_off(gate, it)) return;
   double amax = parts[0], ssq = parts[1];
-  for (int q = 1; q < nparts; ++q) { amax = fmax(amax, parts[2 * q]); ssq += parts[2 * q + 1]; }
+  for (int q = 1; q < nparts; ++q) {
+    amax = fmax(amax, parts[(int64_t)q * stride]);
+    ssq += parts[(int64_t)q * stride + 1];
+  }
   const double lo = 0x1p-450, hi = 0x1p450;
   if (amax == 0.0 || isnan(amax) || (amax >= lo && amax <= hi) || nparts > 1) {
     if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -315,9 +318,10 @@ norm_finish_kernel(const double* parts, int nparts, const double* __restrict__ x
   }
 }
 
-int launch_norm_finish(const double* parts, int nparts, const double* x, int64_t n, double* out,
-                       const lsb_workspace* ws, const lsb_flags* gate, int it, cudaStream_t st) {
-  norm_finish_kernel<<<row_grid(2 * n, 4), kThreads, 0, st>>>(parts, nparts, x, n, out,
+int launch_norm_finish(const double* parts, int nparts, int stride, const double* x, int64_t n,
+                       double* out, const lsb_workspace* ws, const lsb_flags* gate, int it,
+                       cudaStream_t st) {
+  norm_finish_kernel<<<row_grid(2 * n, 4), kThreads, 0, st>>>(parts, nparts, stride, x, n, out,
                                                               ws->partial, ws->counter, gate, it);
   return check_launch("norm_finish");
 }

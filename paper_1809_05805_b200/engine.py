@@ -44,6 +44,19 @@ class CycleReport:
         self.scal = scal
 
 
+_REPORT = {}
+
+
+def _report_buffers(m):
+    import threading
+    key = (m, threading.get_ident())
+    if key not in _REPORT:
+        _REPORT[key] = (torch.zeros(_abi.FLAGS_INTS, dtype=torch.int32).pin_memory(),
+                        torch.zeros(m + 1, dtype=D.F64).pin_memory(),
+                        torch.zeros(_abi.S_COUNT, dtype=D.F64).pin_memory())
+    return _REPORT[key]
+
+
 class Engine:
     def __init__(self, A, m, method, rel_tol, btf=1.0, inv_diag=None, comm=None,
                  diagnostics=False, use_graph=True, n_global=None, op=None):
@@ -71,8 +84,12 @@ class Engine:
             self.op = base_op.with_scale(self.inv_diag[self.off:])
         else:
             self.op = base_op
-        # storage
-        self.Vstore = torch.zeros((self.cap, self.ld), **f64)
+        # storage: every basis column is written before it is read; only the
+        # ghost-plane padding must start at zero (Dirichlet planes never read)
+        self.Vstore = torch.empty((self.cap, self.ld), **f64)
+        if self.halo:
+            self.Vstore[:, : self.off].zero_()
+            self.Vstore[:, self.off + self.n:].zero_()
         cap, m = self.cap, self.m
         self.R = torch.zeros((cap, cap), **f64)
         self.T = torch.zeros((cap, cap), **f64)
@@ -105,10 +122,8 @@ class Engine:
         self.Sref = C.byref(self.S)
         self.scal[_abi.S_RELTOL] = float(rel_tol)
         self.scal[_abi.S_BTF] = float(btf)
-        # host report buffers (pinned)
-        self.h_flags = torch.zeros(_abi.FLAGS_INTS, dtype=torch.int32).pin_memory()
-        self.h_res = torch.zeros(m + 1, dtype=D.F64).pin_memory()
-        self.h_scal = torch.zeros(_abi.S_COUNT, dtype=D.F64).pin_memory()
+        # host report buffers (pinned, cached across engines of the same m)
+        self.h_flags, self.h_res, self.h_scal = _report_buffers(m)
         self.use_graph = use_graph and comm is None
         self.graph = None
         self.cycles_run = 0
@@ -192,7 +207,7 @@ class Engine:
         self._call("lsb_norm_partial", D.ptr(self.rbuf), self.n, D.ptr(self.Gloc), self.ws.ref(),
                    None, -1, st)
         self._gather(2)
-        self._call("lsb_norm_finish", D.ptr(self.G), self.S.g_parts, D.ptr(self.rbuf), self.n,
+        self._call("lsb_norm_finish", D.ptr(self.G), self.S.g_parts, self.S.g_stride, D.ptr(self.rbuf), self.n,
                    C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_RNORM), self.ws.ref(), None, -1,
                    st)
 
@@ -262,7 +277,7 @@ class Engine:
                     self._call("lsb_collect_coef", S, i, p, accumulate, st)
                     self._call("lsb_cgs_project", S, i, i, p, accumulate, st)
                 self._gather(2)
-            self._call("lsb_norm_finish", D.ptr(self.G), self.S.g_parts, self.col_ptr(i), self.n,
+            self._call("lsb_norm_finish", D.ptr(self.G), self.S.g_parts, self.S.g_stride, self.col_ptr(i), self.n,
                        C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_BETA), self.ws.ref(),
                        D.ptr(self.flags), i, st)
             self._call("lsb_direct_small", S, i, i, p, st)

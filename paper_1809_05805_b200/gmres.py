@@ -214,7 +214,7 @@ class _DeviceSolve:
     """One solve: host restart shell over device cycles (gmres.py:239-516)."""
 
     def __init__(self, A, b, x0, config, ledger, diagnostics_every, true_residual_every,
-                 use_graph=True):
+                 use_graph=True, comm=None, n_global=None):
         if A.n_rows != A.n_cols:
             raise ValueError("GMRES needs a square matrix")
         if config.method not in DEVICE_METHODS:
@@ -223,16 +223,20 @@ class _DeviceSolve:
         if true_residual_every:
             raise NotImplementedError("true_residual_every is not supported on the device path")
         self.A = A
+        self.comm = comm
         self.n = A.n_rows
+        self.n_global = int(n_global or self.n)
         self.host = D.is_host(b)
         self.b = D.to_device_vector(b, self.n)
-        if not bool((self.b != 0).any()):
+        if comm is None and not bool((self.b != 0).any()):
             raise ValueError("right-hand side must be nonzero")
         self.x0 = None if x0 is None else D.to_device_vector(x0, self.n)
         self.config = config
         self.ledger = ledger if ledger is not None else ReductionLedger()
+        if comm is not None and config.precond != "none":
+            raise NotImplementedError("jacobi preconditioning on the multi-rank path")
         self.pc = Preconditioner(config.precond, A)
-        self.m = min(config.restart_m, self.n)
+        self.m = min(config.restart_m, self.n_global)
         self.diag_every = diagnostics_every
         self.history = ConvergenceHistory()
         self.history.method = config.method
@@ -292,7 +296,8 @@ class _DeviceSolve:
         hist = self.history
         inv = self.pc.inv_diag
         eng = Engine(self.A, self.m, cfg.method, cfg.rel_tol, cfg.breakdown_tol_factor,
-                     inv_diag=inv, diagnostics=bool(self.diag_every), use_graph=self.use_graph)
+                     inv_diag=inv, diagnostics=bool(self.diag_every), use_graph=self.use_graph,
+                     comm=self.comm, n_global=self.n_global)
         self.engine = eng
         eng.load(self.b, self.x0)
         led.iteration = 0
@@ -449,3 +454,18 @@ def solve(A, b, x0=None, config=None, ledger=None, diagnostics_every=1, true_res
     config = config if config is not None else GmresConfig()
     return _DISPATCH[config.method](A, b, x0, config, ledger, diagnostics_every,
                                     true_residual_every)
+
+
+def solve_distributed(op, b_local, comm, n_global, x0_local=None, config=None, ledger=None,
+                      diagnostics_every=0):
+    """Row-partitioned solve (one rank per GPU): `op` is this rank's slab
+    operator (parallel.slab_problem), b_local/x0_local its rows.  Every rank
+    runs the same host restart shell on bit-identical device reports, so
+    histories and ledgers agree across ranks; returns (x_local, history)."""
+    config = config if config is not None else GmresConfig()
+    if config.method == "cgs1_ghysels":
+        raise NotImplementedError("cgs1_ghysels is outside the B200 hot path (SURVEY §8f)")
+    if diagnostics_every:
+        raise NotImplementedError("per-iteration diagnostics on the multi-rank path")
+    return _DeviceSolve(op, b_local, x0_local, config, ledger, diagnostics_every, 0,
+                        use_graph=False, comm=comm, n_global=n_global).run()

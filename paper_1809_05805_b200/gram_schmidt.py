@@ -186,7 +186,7 @@ def _direct(Q, a, ledger, btf, passes):
         if not p:
             _abi.call("lsb_norm_partial", zp, n, D.ptr(sc.G), sc.ws.ref(), None, 0, st)
     ledger.record(NORM, 1)
-    _abi.call("lsb_norm_finish", D.ptr(sc.G), 1, zp, n,
+    _abi.call("lsb_norm_finish", D.ptr(sc.G), 1, 2, zp, n,
               C.c_void_p(sc.scal.data_ptr() + 8 * _abi.S_BETA), sc.ws.ref(), None, 0, st)
     _abi.call("lsb_direct_small", ref, 0, p, p, st)
     fl = sc.flags.cpu()

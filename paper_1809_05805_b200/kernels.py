@@ -344,7 +344,7 @@ def _device_norm(v, ws=None):
     out = torch.empty(1, dtype=D.F64, device=v.device)
     n = v.shape[0]
     _abi.call("lsb_norm_partial", D.ptr(v), n, D.ptr(parts), ws.ref(), None, 0, D.stream())
-    _abi.call("lsb_norm_finish", D.ptr(parts), 1, D.ptr(v), n, D.ptr(out), ws.ref(), None, 0,
+    _abi.call("lsb_norm_finish", D.ptr(parts), 1, 2, D.ptr(v), n, D.ptr(out), ws.ref(), None, 0,
               D.stream())
     return out
 

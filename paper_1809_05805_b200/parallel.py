@@ -71,6 +71,112 @@ class Comm:
             dist.destroy_process_group()
 
 
+class ThreadGroup:
+    """Shared state of P in-process ranks (one Python thread per rank)."""
+
+    def __init__(self, size):
+        import threading
+        self.size = size
+        self.barrier = threading.Barrier(size)
+        self.slots = [None] * size
+        self.done = [None] * size
+
+
+class ThreadComm:
+    """Single-process communicator: P ranks = P threads, each issuing its
+    kernels on its own CUDA stream (same or different devices).  A
+    collective publishes the rank's buffer with a CUDA event, meets the
+    other ranks at a host barrier, copies the peers' data device-to-device
+    after waiting on their events, and fences again so no rank overwrites a
+    published buffer before every peer has copied it.  Same interface and
+    data movement as Comm, so the engine runs unchanged; used to exercise
+    the multi-rank kernels (g_parts > 1, ghost planes, slab operators) on a
+    single GPU, and usable as a one-process multi-GPU driver."""
+
+    def __init__(self, group, rank):
+        self.g = group
+        self.rank = rank
+        self.size = group.size
+
+    def _exchange(self, publish, consume):
+        g, r = self.g, self.rank
+        ev = torch.cuda.Event()
+        ev.record()
+        g.slots[r] = (publish, ev)
+        g.barrier.wait()
+        st = torch.cuda.current_stream()
+        for q in range(self.size):
+            st.wait_event(g.slots[q][1])
+        consume(g.slots)
+        ev2 = torch.cuda.Event()
+        ev2.record()
+        g.done[r] = ev2
+        g.barrier.wait()
+        for q in range(self.size):
+            st.wait_event(g.done[q])
+        g.barrier.wait()   # slots may be reused only after everyone fenced
+
+    def allgather(self, local, out):
+        L = local.numel()
+
+        def consume(slots):
+            for q in range(self.size):
+                out[q * L:(q + 1) * L].copy_(slots[q][0], non_blocking=True)
+        self._exchange(local, consume)
+
+    def halo(self, vec, off, n, plane):
+        r, s = self.rank, self.size
+        pub = (vec[off:off + plane], vec[off + n - plane:off + n])
+
+        def consume(slots):
+            if r > 0:
+                vec[off - plane:off].copy_(slots[r - 1][0][1], non_blocking=True)
+            if r < s - 1:
+                vec[off + n:off + n + plane].copy_(slots[r + 1][0][0], non_blocking=True)
+        self._exchange(pub, consume)
+
+    def max_scalar(self, v):
+        g = self.g
+        g.slots[self.rank] = (float(v), None)
+        g.barrier.wait()
+        m = max(x[0] for x in g.slots)
+        g.barrier.wait()
+        return m
+
+    def barrier(self):
+        self.g.barrier.wait()
+
+    def close(self):
+        pass
+
+
+def run_threads(size, fn, *args):
+    """Run fn(comm, *args) on `size` in-process ranks; returns per-rank results."""
+    import threading
+    grp = ThreadGroup(size)
+    out = [None] * size
+    err = []
+
+    def body(r):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                out[r] = fn(ThreadComm(grp, r), *args)
+            s.synchronize()
+        except BaseException as e:  # pragma: no cover
+            err.append(e)
+            grp.barrier.abort()
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(size)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if err:
+        raise err[0]
+    return out
+
+
 def slab_bounds(nz, size, rank):
     """Planes [z0, z0+nzl) of rank `rank` (contiguous, as equal as possible)."""
     base, extra = divmod(nz, size)
