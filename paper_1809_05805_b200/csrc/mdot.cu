@@ -4,20 +4,24 @@
 // (reference kernels.py:275-347), whose numpy form reads X twice (two
 // dgemv-T calls, kernels.py:345-346).  Here X is streamed from HBM exactly
 // once:
-//   * persistent CTAs walk row tiles of kTile rows;
-//   * the tile of u (and w) is staged once in shared memory;
-//   * warp `wp` owns columns k = wp, wp+8, ... and keeps one register
-//     accumulator per (owned column, vector) across all its tiles, so the
-//     per-tile work is 16 independent 128-bit loads per lane per column with
-//     no shuffles at all;
-//   * the CTA totals are butterfly-reduced once at the end and the last CTA
-//     sums the per-CTA partials in a fixed order (deterministic).
+//   * persistent CTAs (8 warps) walk row tiles of kTile rows; the u/w tile
+//     is staged in shared memory with cp.async, double-buffered so the next
+//     tile's u/w load overlaps the current tile's column sweep;
+//   * each tile column is cut into R row parts (R | 8) and the p*R
+//     (column, part) items are dealt round-robin to the 8 warps; R is chosen
+//     per p so the deal is (nearly) even -- e.g. p = 26 -> R = 4, 13 items
+//     per warp -- and since 8 is a multiple of R a warp always owns the same
+//     (column, part) set, so it keeps one register accumulator per item
+//     across all of its tiles: per item only independent 128-bit streaming
+//     loads + FMAs, no shuffles, no atomics;
+//   * at the end one butterfly per item, parts combined in fixed order in
+//     shared memory, and the last CTA sums the per-CTA partials in a fixed
+//     order: deterministic, bitwise reproducible run to run.
 #include "reduce.cuh"
 
 namespace lsb {
 
-constexpr int kTile = 1024;                  // rows per tile
-constexpr int kLoads = kTile / 64;           // double2 loads per lane per column
+constexpr int kTile = 1024;  // rows per tile
 
 __device__ __forceinline__ double2 ld_stream(const double* p) {
   double2 r;
@@ -26,15 +30,48 @@ __device__ __forceinline__ double2 ld_stream(const double* p) {
   return r;
 }
 
-template <int NV, int SLOTS>
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// stage tile t's u/w rows into buf (async when the tile is full)
+template <int NV>
+__device__ __forceinline__ void stage_tile(double2 (*buf)[kTile / 2], const double* y0,
+                                           const double* y1, int64_t n, int64_t t) {
+  const int64_t r0 = t * kTile;
+  if (r0 + kTile <= n) {
+    for (int j = threadIdx.x; j < kTile / 2; j += kThreads)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) cp_async16(&buf[v][j], (v == 0 ? y0 : y1) + r0 + 2 * j);
+  } else {
+    for (int j = threadIdx.x; j < kTile / 2; j += kThreads) {
+      const int64_t r = r0 + 2 * j;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const double* y = v == 0 ? y0 : y1;
+        buf[v][j] = make_double2(r < n ? y[r] : 0.0, r + 1 < n ? y[r + 1] : 0.0);
+      }
+    }
+  }
+}
+
+template <int NV, int R, int SLOTS>
 __global__ void __launch_bounds__(kThreads, 2)
 mdot_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
             const double* __restrict__ y0, const double* __restrict__ y1,
             double* __restrict__ out, double* __restrict__ partial, unsigned* counter,
             const lsb_flags* gate, int it) {
   if (gated_off(gate, it)) return;
-  __shared__ __align__(16) double2 sy[NV][kTile / 2];
+  constexpr int kRows = kTile / R;       // rows per item
+  constexpr int kLd = kRows / 64;        // double2 loads per lane per item
+  __shared__ __align__(16) double2 sy[2][NV][kTile / 2];
+  __shared__ double red[kWarps * SLOTS][NV];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int part = warp % R;             // fixed per warp because R | 8
   double acc[SLOTS][NV];
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s)
@@ -42,56 +79,48 @@ mdot_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
     for (int v = 0; v < NV; ++v) acc[s][v] = 0.0;
 
   const int64_t ntiles = (n + kTile - 1) / kTile;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  int64_t t = blockIdx.x;
+  int buf = 0;
+  if (t < ntiles) stage_tile<NV>(sy[0], y0, y1, n, t);
+  cp_async_commit();
+  for (; t < ntiles; t += gridDim.x) {
+    const int64_t tn = t + gridDim.x;
+    if (tn < ntiles) stage_tile<NV>(sy[buf ^ 1], y0, y1, n, tn);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
     const int64_t r0 = t * kTile;
     const bool full = r0 + kTile <= n;
-    // stage the u/w tile (coalesced, once per tile)
-    for (int j = threadIdx.x; j < kTile / 2; j += kThreads) {
-      const int64_t r = r0 + 2 * j;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const double* y = v == 0 ? y0 : y1;
-        double2 val;
-        if (full) {
-          val = *reinterpret_cast<const double2*>(y + r);
-        } else {
-          val.x = r < n ? y[r] : 0.0;
-          val.y = r + 1 < n ? y[r + 1] : 0.0;
-        }
-        sy[v][j] = val;
-      }
-    }
-    __syncthreads();
+    const int jbase = part * (kRows / 2);
 #pragma unroll
     for (int s = 0; s < SLOTS; ++s) {
-      const int k = warp + kWarps * s;
+      const int k = (warp + kWarps * s) / R;
       if (k < p) {
-        const double* col = X + (int64_t)k * ld + r0;
+        const double* col = X + (int64_t)k * ld + r0 + part * kRows;
         double a[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) a[v] = 0.0;
         if (full) {
-          double2 xv[kLoads];
+          double2 xv[kLd];
 #pragma unroll
-          for (int q = 0; q < kLoads; ++q) xv[q] = ld_stream(col + 2 * (lane + 32 * q));
+          for (int q = 0; q < kLd; ++q) xv[q] = ld_stream(col + 2 * (lane + 32 * q));
 #pragma unroll
-          for (int q = 0; q < kLoads; ++q) {
+          for (int q = 0; q < kLd; ++q)
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-              const double2 yy = sy[v][lane + 32 * q];
+              const double2 yy = sy[buf][v][jbase + lane + 32 * q];
               a[v] = fma(xv[q].x, yy.x, a[v]);
               a[v] = fma(xv[q].y, yy.y, a[v]);
             }
-          }
         } else {
-          for (int q = 0; q < kLoads; ++q) {
+          for (int q = 0; q < kLd; ++q) {
             const int j = lane + 32 * q;
-            const int64_t r = r0 + 2 * j;
+            const int64_t r = r0 + part * kRows + 2 * j;
             const double xa = r < n ? col[2 * j] : 0.0;
             const double xb = r + 1 < n ? col[2 * j + 1] : 0.0;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-              const double2 yy = sy[v][j];
+              const double2 yy = sy[buf][v][jbase + j];
               a[v] = fma(xa, yy.x, a[v]);
               a[v] = fma(xb, yy.y, a[v]);
             }
@@ -102,20 +131,27 @@ mdot_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
       }
     }
     __syncthreads();
+    buf ^= 1;
   }
+  cp_async_wait<0>();
 
-  // CTA partials: one butterfly per owned (column, vector)
-  const int G = gridDim.x;
+  // CTA totals: butterfly per item, then the R parts of a column in order
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) {
-    const int k = warp + kWarps * s;
-    if (k < p) {
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const double x = warp_sum(acc[s][v]);
-        if (lane == 0) partial[(size_t)(k * NV + v) * G + blockIdx.x] = x;
-      }
+    for (int v = 0; v < NV; ++v) {
+      const double x = warp_sum(acc[s][v]);
+      if (lane == 0) red[warp + kWarps * s][v] = x;   // item index q = warp + 8 s
     }
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  for (int e = threadIdx.x; e < p * NV; e += kThreads) {
+    const int k = e / NV, v = e % NV;
+    double x = red[k * R][v];
+#pragma unroll
+    for (int pr = 1; pr < R; ++pr) x += red[k * R + pr][v];
+    partial[(size_t)e * G + blockIdx.x] = x;
   }
   __shared__ bool is_last;
   __threadfence();
@@ -134,13 +170,13 @@ mdot_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
   if (threadIdx.x == 0) *counter = 0u;
 }
 
-template <int NV, int SLOTS>
+template <int NV, int R, int SLOTS>
 static int launch_mdot_t(const double* X, int64_t ld, int64_t n, int p, const double* u,
                          const double* w, double* out, const lsb_workspace* ws,
                          const lsb_flags* gate, int it, cudaStream_t st) {
   static int occ = 0;
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mdot_kernel<NV, SLOTS>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mdot_kernel<NV, R, SLOTS>, kThreads, 0);
     if (occ < 1) occ = 1;
   }
   const int64_t ntiles = (n + kTile - 1) / kTile;
@@ -148,20 +184,51 @@ static int launch_mdot_t(const double* X, int64_t ld, int64_t n, int p, const do
   if (ws->grid > 0 && ws->grid < grid) grid = ws->grid;
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
-  mdot_kernel<NV, SLOTS><<<(unsigned)grid, kThreads, 0, st>>>(X, ld, n, p, u, w, out, ws->partial,
-                                                             ws->counter, gate, it);
+  mdot_kernel<NV, R, SLOTS><<<(unsigned)grid, kThreads, 0, st>>>(X, ld, n, p, u, w, out,
+                                                                ws->partial, ws->counter, gate, it);
   return check_launch("mdot");
+}
+
+// slots needed for p columns cut in R parts over 8 warps
+static inline int slots_for(int p, int R) { return (p * R + kWarps - 1) / kWarps; }
+
+template <int NV, int R>
+static int launch_mdot_r(const double* X, int64_t ld, int64_t n, int p, const double* u,
+                         const double* w, double* out, const lsb_workspace* ws,
+                         const lsb_flags* gate, int it, cudaStream_t st) {
+  const int s = slots_for(p, R);
+  if (s <= 1) return launch_mdot_t<NV, R, 1>(X, ld, n, p, u, w, out, ws, gate, it, st);
+  if (s <= 2) return launch_mdot_t<NV, R, 2>(X, ld, n, p, u, w, out, ws, gate, it, st);
+  if (s <= 4) return launch_mdot_t<NV, R, 4>(X, ld, n, p, u, w, out, ws, gate, it, st);
+  if (s <= 8) return launch_mdot_t<NV, R, 8>(X, ld, n, p, u, w, out, ws, gate, it, st);
+  if (s <= 13) return launch_mdot_t<NV, R, 13>(X, ld, n, p, u, w, out, ws, gate, it, st);
+  return launch_mdot_t<NV, R, 16>(X, ld, n, p, u, w, out, ws, gate, it, st);
+}
+
+// Choose R in {1,2,4,8}: least idle (column, part) slots, at most 16 slots
+// per warp, ties to the smaller R (longer contiguous runs per item).
+static int choose_parts(int p) {
+  int best = 1;
+  double best_eff = 0.0;
+  for (int R = 1; R <= 8; R *= 2) {
+    const int s = slots_for(p, R);
+    if (s > 16) break;
+    const double eff = (double)(p * R) / (double)(s * kWarps);
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = R; }
+  }
+  return best;
 }
 
 template <int NV>
 static int launch_mdot_nv(const double* X, int64_t ld, int64_t n, int p, const double* u,
                           const double* w, double* out, const lsb_workspace* ws,
                           const lsb_flags* gate, int it, cudaStream_t st) {
-  if (p <= 8) return launch_mdot_t<NV, 1>(X, ld, n, p, u, w, out, ws, gate, it, st);
-  if (p <= 16) return launch_mdot_t<NV, 2>(X, ld, n, p, u, w, out, ws, gate, it, st);
-  if (p <= 32) return launch_mdot_t<NV, 4>(X, ld, n, p, u, w, out, ws, gate, it, st);
-  if (p <= 64) return launch_mdot_t<NV, 8>(X, ld, n, p, u, w, out, ws, gate, it, st);
-  return launch_mdot_t<NV, 16>(X, ld, n, p, u, w, out, ws, gate, it, st);
+  switch (choose_parts(p)) {
+    case 8: return launch_mdot_r<NV, 8>(X, ld, n, p, u, w, out, ws, gate, it, st);
+    case 4: return launch_mdot_r<NV, 4>(X, ld, n, p, u, w, out, ws, gate, it, st);
+    case 2: return launch_mdot_r<NV, 2>(X, ld, n, p, u, w, out, ws, gate, it, st);
+    default: return launch_mdot_r<NV, 1>(X, ld, n, p, u, w, out, ws, gate, it, st);
+  }
 }
 
 constexpr int kMaxCols = 128;

@@ -3,6 +3,11 @@
 // coefficients, the Hessenberg column and its Givens fold, the convergence
 // test, and the per-cycle back-substitution.  One CTA; O(p^2) flops.
 //
+// Everything the serial parts touch (the R column, the rotations) is first
+// pulled into shared memory by all threads in parallel, so the serial chain
+// (hypot, the Givens sweep) runs at shared-memory latency instead of one L2
+// round trip per element.
+//
 // Reference: gram_schmidt.py:96-106 (breakdown), 206-245 (mgs_lvl2),
 // 248-280 (cgs2_lvl2), gmres.py:153-192 (Givens / least squares),
 // gmres.py:407-435 (Hessenberg column assembly and settle).
@@ -18,139 +23,143 @@ __device__ __forceinline__ double gsum(const lsb_arnoldi& S, int e) {
   return v;
 }
 
+struct SmallShared {
+  double a[kSmall];     // G[:,0] / scaled
+  double y[kSmall];     // G[:,1] / y
+  double col[kSmall + 2];  // R column (r_col, then the Hessenberg column)
+  double rot[2 * kSmall];
+  double beta, tol;
+  int broke;
+};
+
 // tol = btf * eps * sqrt(n) * hypot(r_diag, ||r_col||)   (gram_schmidt.py:96-100)
-__device__ double breakdown_tol(const lsb_arnoldi& S, double r_diag, const double* rcol,
-                                int64_t stride, int len) {
+__device__ double breakdown_tol(const lsb_arnoldi& S, double r_diag, const double* rcol, int len) {
   double pre = r_diag;
   if (len > 0) {
     double ss = 0.0;
-    for (int j = 0; j < len; ++j) { const double v = rcol[j * stride]; ss = fma(v, v, ss); }
+    for (int j = 0; j < len; ++j) ss = fma(rcol[j], rcol[j], ss);
     pre = py_hypot(r_diag, sqrt(ss));
   }
   const double btf = S.scal[LSB_S_BTF];
   return __dmul_rn(__dmul_rn(__dmul_rn(btf, kEps), sqrt((double)S.n_global)), pre);
 }
 
-// Hessenberg column gc-1 = R[0..gc, gc] (R[gc,gc] = 0 after a breakdown),
-// folded into the Givens state; records |g[gc]| and stops the cycle on
-// convergence or breakdown (gmres.py:427-435).
-__device__ void settle(const lsb_arnoldi& S, int it, int gc, bool broke) {
-  double h[kSmall + 4];
-  const int cap = S.cap;
-  for (int j = 0; j <= gc; ++j) h[j] = S.R[(int64_t)j * cap + gc];
-  const double res = givens_fold(h, S.rot, S.g, gc);
-  for (int j = 0; j <= gc; ++j) S.tri[(int64_t)j * S.m + (gc - 1)] = h[j];
-  S.res[gc] = res;
-  const double target = S.scal[LSB_S_TARGET];
-  if (res <= target || broke) {
-    S.flags->stop_iter = it;
-    S.flags->status = res <= target ? LSB_CONVERGED : LSB_BREAKDOWN;
+// Block-cooperative settle (gmres.py:427-435): Hessenberg column gc-1 is
+// sh.col[0..gc] (= R[0..gc, gc], with R[gc,gc] = 0 after a breakdown);
+// fold it into the Givens state, record |g[gc]|, stop on convergence or
+// breakdown.  All threads must call it.
+__device__ void settle_block(const lsb_arnoldi& S, SmallShared& sh, int it, int gc, bool broke) {
+  const int t = threadIdx.x;
+  for (int e = t; e < 2 * (gc - 1); e += blockDim.x) sh.rot[e] = S.rot[e];
+  __syncthreads();
+  if (t == 0) {
+    const double res = givens_fold(sh.col, sh.rot, S.g, gc);
+    S.rot[2 * (gc - 1)] = sh.rot[2 * (gc - 1)];
+    S.rot[2 * (gc - 1) + 1] = sh.rot[2 * (gc - 1) + 1];
+    S.res[gc] = res;
+    const double target = S.scal[LSB_S_TARGET];
+    if (res <= target || broke) {
+      S.flags->stop_iter = it;
+      S.flags->status = res <= target ? LSB_CONVERGED : LSB_BREAKDOWN;
+    }
   }
+  __syncthreads();
+  for (int j = t; j <= gc; j += blockDim.x) S.tri[(int64_t)j * S.m + (gc - 1)] = sh.col[j];
+}
+
+// Shared front of both lagged kernels: gathered G, deferred norm beta,
+// breakdown test against R[:p-1, p-1] (gram_schmidt.py:227-229 / 261-263).
+__device__ bool lagged_front(const lsb_arnoldi& S, SmallShared& sh, int it, int p, int gc) {
+  const int t = threadIdx.x, cap = S.cap;
+  for (int e = t; e < p; e += blockDim.x) {
+    sh.a[e] = gsum(S, 2 * e);
+    sh.y[e] = gsum(S, 2 * e + 1);
+    if (e < p - 1) sh.col[e] = S.R[(int64_t)e * cap + (p - 1)];
+  }
+  __syncthreads();
+  if (t == 0) {
+    const double bsq = sh.a[p - 1];
+    const double beta = bsq > 0.0 ? sqrt(bsq) : 0.0;
+    const double tol = breakdown_tol(S, beta, sh.col, p - 1);
+    sh.beta = beta;
+    sh.tol = tol;
+    sh.broke = beta <= tol;
+    S.scal[LSB_S_BETA] = beta;
+    S.scal[LSB_S_TOL] = tol;
+    if (sh.broke) {
+      S.flags->broke_iter = it;
+      if (gc == 0) { S.flags->stop_iter = it; S.flags->status = LSB_STARTUP_BREAKDOWN; }
+      sh.col[p - 1] = 0.0;   // H[i, i-1] = 0 (gmres.py:416)
+    } else {
+      sh.col[p - 1] = beta;  // H[i, i-1] = R[i, i] = beta (gmres.py:418)
+      S.R[(int64_t)(p - 1) * cap + (p - 1)] = beta;
+    }
+  }
+  __syncthreads();
+  return sh.broke;
 }
 
 // ------------------------------------------------------------------ mgs_lvl2
 __global__ void __launch_bounds__(kSmall)
 mgs_lvl2_small_kernel(lsb_arnoldi S, int it, int p, int ks, int gc) {
   if (gated_off(S.flags, it)) return;
-  __shared__ double sG0[kSmall], sy[kSmall];
-  __shared__ double sbeta;
-  __shared__ int sbroke;
+  __shared__ SmallShared sh;
   const int t = threadIdx.x, cap = S.cap;
-  for (int e = t; e < p; e += blockDim.x) { sG0[e] = gsum(S, 2 * e); sy[e] = gsum(S, 2 * e + 1); }
-  __syncthreads();
-  if (t == 0) {
-    const double bsq = sG0[p - 1];
-    const double beta = bsq > 0.0 ? sqrt(bsq) : 0.0;
-    const double tol = breakdown_tol(S, beta, S.R + (p - 1), cap, p - 1);
-    sbeta = beta;
-    sbroke = beta <= tol;
-    S.scal[LSB_S_BETA] = beta;
-    S.scal[LSB_S_TOL] = tol;
-  }
-  __syncthreads();
-  const double beta = sbeta;
-  if (sbroke) {
-    if (t == 0) {
-      S.flags->broke_iter = it;
-      if (gc > 0) settle(S, it, gc, true);
-      else { S.flags->stop_iter = it; S.flags->status = LSB_STARTUP_BREAKDOWN; }
-    }
+  const bool broke = lagged_front(S, sh, it, p, gc);
+  if (broke) {
+    if (gc > 0) settle_block(S, sh, it, gc, true);
     return;
   }
+  const double beta = sh.beta;
   // T[:p-1, p-1] = -(T[:p-1, :p-1] @ (G[:p-1, 0] / beta));  T[p-1, p-1] = 1
-  for (int e = t; e < p - 1; e += blockDim.x) sG0[e] = __ddiv_rn(sG0[e], beta);
+  for (int e = t; e < p - 1; e += blockDim.x) sh.a[e] = __ddiv_rn(sh.a[e], beta);
+  if (t == 0) sh.y[p - 1] = __ddiv_rn(sh.y[p - 1], beta);
   __syncthreads();
   for (int j = t; j < p - 1; j += blockDim.x) {
     double acc = 0.0;
-    for (int l = j; l < p - 1; ++l) acc = fma(S.T[(int64_t)j * cap + l], sG0[l], acc);
+    for (int l = j; l < p - 1; ++l) acc = fma(S.T[(int64_t)j * cap + l], sh.a[l], acc);
     S.T[(int64_t)j * cap + (p - 1)] = -acc;
   }
-  if (t == 0) {
-    S.T[(int64_t)(p - 1) * cap + (p - 1)] = 1.0;
-    S.R[(int64_t)(p - 1) * cap + (p - 1)] = beta;
-    sy[p - 1] = __ddiv_rn(sy[p - 1], beta);
-  }
+  if (t == 0) S.T[(int64_t)(p - 1) * cap + (p - 1)] = 1.0;
   __syncthreads();
-  // c = T[:p,:p]^T y  (/beta);  R[:p, p] = c
+  // c = T[:p,:p]^T y  (/beta);  R[:p, p] = c  (coalesced column reads)
   for (int j = t; j < p; j += blockDim.x) {
     double acc = 0.0;
-    for (int l = 0; l <= j; ++l) acc = fma(S.T[(int64_t)l * cap + j], sy[l], acc);
+    for (int l = 0; l <= j; ++l) acc = fma(S.T[(int64_t)l * cap + j], sh.y[l], acc);
     if (ks) acc = __ddiv_rn(acc, beta);
     S.coef[j] = acc;
     S.R[(int64_t)j * cap + p] = acc;
   }
-  __syncthreads();
-  if (t == 0 && gc > 0) settle(S, it, gc, false);
+  if (gc > 0) settle_block(S, sh, it, gc, false);
 }
 
 // ------------------------------------------------------------------ cgs2_lvl2
 __global__ void __launch_bounds__(kSmall)
 cgs2_small_a_kernel(lsb_arnoldi S, int it, int p, int ks, int gc) {
   if (gated_off(S.flags, it)) return;
-  __shared__ double sG0[kSmall], sy[kSmall];
-  __shared__ double sbeta;
-  __shared__ int sbroke;
+  __shared__ SmallShared sh;
   const int t = threadIdx.x, cap = S.cap;
-  for (int e = t; e < p; e += blockDim.x) { sG0[e] = gsum(S, 2 * e); sy[e] = gsum(S, 2 * e + 1); }
-  __syncthreads();
-  if (t == 0) {
-    const double bsq = sG0[p - 1];
-    const double beta = bsq > 0.0 ? sqrt(bsq) : 0.0;
-    const double tol = breakdown_tol(S, beta, S.R + (p - 1), cap, p - 1);
-    sbeta = beta;
-    sbroke = beta <= tol;
-    S.scal[LSB_S_BETA] = beta;
-    S.scal[LSB_S_TOL] = tol;
-  }
-  __syncthreads();
-  const double beta = sbeta;
-  if (sbroke) {
-    if (t == 0) {
-      S.flags->broke_iter = it;
-      if (gc > 0) settle(S, it, gc, true);
-      else { S.flags->stop_iter = it; S.flags->status = LSB_STARTUP_BREAKDOWN; }
-    }
+  const bool broke = lagged_front(S, sh, it, p, gc);
+  if (broke) {
+    if (gc > 0) settle_block(S, sh, it, gc, true);
     return;
   }
+  const double beta = sh.beta;
   // L[p-1, :p-1] = G[:p-1, 0] / beta  (gram_schmidt.py:266-267)
   for (int e = t; e < p - 1; e += blockDim.x)
-    S.L[(int64_t)(p - 1) * cap + e] = __ddiv_rn(sG0[e], beta);
-  if (t == 0) {
-    S.R[(int64_t)(p - 1) * cap + (p - 1)] = beta;
-    sy[p - 1] = __ddiv_rn(sy[p - 1], beta);
-  }
+    S.L[(int64_t)(p - 1) * cap + e] = __ddiv_rn(sh.a[e], beta);
+  if (t == 0) sh.y[p - 1] = __ddiv_rn(sh.y[p - 1], beta);
   __syncthreads();
   // r = y - Ls y - Ls^T y  (/beta)   (gram_schmidt.py:270-274)
   for (int j = t; j < p; j += blockDim.x) {
     double a = 0.0, b = 0.0;
-    for (int l = 0; l < j; ++l) a = fma(S.L[(int64_t)j * cap + l], sy[l], a);
-    for (int l = j + 1; l < p; ++l) b = fma(S.L[(int64_t)l * cap + j], sy[l], b);
-    double r = (sy[j] - a) - b;
+    for (int l = 0; l < j; ++l) a = fma(S.L[(int64_t)j * cap + l], sh.y[l], a);
+    for (int l = j + 1; l < p; ++l) b = fma(S.L[(int64_t)l * cap + j], sh.y[l], b);
+    double r = (sh.y[j] - a) - b;
     if (ks) r = __ddiv_rn(r, beta);
     S.coef[j] = r;
   }
-  __syncthreads();
-  if (t == 0 && gc > 0) settle(S, it, gc, false);
+  if (gc > 0) settle_block(S, sh, it, gc, false);
 }
 
 // s = gathered second-pass products; R[:p, p] = r + s   (gram_schmidt.py:276-278)
@@ -180,23 +189,26 @@ collect_coef_kernel(lsb_arnoldi S, int it, int p, int accumulate) {
 // r_diag (already in scal[BETA] from norm_finish), breakdown test, Hbar
 // column col-1 = [coef[0..p), r_diag] stored in R[:, col], Givens fold
 // (gmres.py:362-381 / gram_schmidt.py:139-141, 158-160).
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(kSmall)
 direct_small_kernel(lsb_arnoldi S, int it, int col, int p, int gc) {
   if (gated_off(S.flags, it)) return;
-  if (threadIdx.x != 0) return;
-  const double r_diag = S.scal[LSB_S_BETA];
-  const double tol = breakdown_tol(S, r_diag, S.coef, 1, p);
-  S.scal[LSB_S_TOL] = tol;
-  const bool broke = r_diag <= tol;
-  if (broke) S.flags->broke_iter = it;
+  __shared__ SmallShared sh;
+  const int t = threadIdx.x, cap = S.cap;
+  for (int j = t; j < p; j += blockDim.x) sh.col[j] = S.coef[j];
+  __syncthreads();
+  if (t == 0) {
+    const double r_diag = S.scal[LSB_S_BETA];
+    const double tol = breakdown_tol(S, r_diag, sh.col, p);
+    S.scal[LSB_S_TOL] = tol;
+    sh.broke = r_diag <= tol;
+    if (sh.broke) S.flags->broke_iter = it;
+    sh.col[p] = sh.broke ? 0.0 : r_diag;
+    if (gc == 0 && sh.broke) { S.flags->stop_iter = it; S.flags->status = LSB_STARTUP_BREAKDOWN; }
+  }
+  __syncthreads();
   if (gc > 0) {
-    const int cap = S.cap;
-    for (int j = 0; j < p; ++j) S.R[(int64_t)j * cap + col] = S.coef[j];
-    S.R[(int64_t)col * cap + col] = broke ? 0.0 : r_diag;
-    settle(S, it, gc, broke);
-  } else if (broke) {
-    S.flags->stop_iter = it;
-    S.flags->status = LSB_STARTUP_BREAKDOWN;
+    for (int j = t; j <= p; j += blockDim.x) S.R[(int64_t)j * cap + col] = sh.col[j];
+    settle_block(S, sh, it, gc, sh.broke);
   }
 }
 
@@ -221,25 +233,29 @@ cycle_begin_kernel(lsb_arnoldi S) {
   }
 }
 
-// solve_least_squares (gmres.py:184-192) on the rotated k x k triangle.
+// solve_least_squares (gmres.py:184-192) on the rotated k x k triangle:
+// row-oriented back substitution, one warp per row dot (fixed lane order).
 __global__ void __launch_bounds__(32)
 cycle_lsq_kernel(lsb_arnoldi S) {
-  if (threadIdx.x != 0) return;
+  __shared__ double sy[kSmall];
+  const int lane = threadIdx.x;
   const int stop = S.flags->stop_iter;
   const int k = stop == LSB_NO_STOP ? S.m : stop;
-  S.flags->k = k;
+  if (lane == 0) S.flags->k = k;
   const int m = S.m;
   for (int i = k - 1; i >= 0; --i) {
     const double d = S.tri[(int64_t)i * m + i];
     if (d == 0.0) {
-      S.flags->status = LSB_SINGULAR;
-      S.flags->k = i;  // diagnostic: zero diagonal index
+      if (lane == 0) { S.flags->status = LSB_SINGULAR; S.flags->k = i; }
       return;
     }
     double acc = 0.0;
-    for (int j = i + 1; j < k; ++j) acc = fma(S.tri[(int64_t)i * m + j], S.coef2[j], acc);
-    S.coef2[i] = __ddiv_rn(S.g[i] - acc, d);
+    for (int j = i + 1 + lane; j < k; j += 32) acc = fma(S.tri[(int64_t)i * m + j], sy[j], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) sy[i] = __ddiv_rn(S.g[i] - acc, d);
+    __syncwarp();
   }
+  for (int j = lane; j < k; j += 32) S.coef2[j] = sy[j];
 }
 
 // First call: denom = beta0 or 1, target = rel_tol * beta0 (gmres.py:472-479).
@@ -273,7 +289,8 @@ int launch_collect_coef(const lsb_arnoldi& S, int it, int p, int acc, cudaStream
   return check_launch("collect_coef");
 }
 int launch_direct_small(const lsb_arnoldi& S, int it, int col, int p, int gc, cudaStream_t st) {
-  direct_small_kernel<<<1, 32, 0, st>>>(S, it, col, p, gc);
+  if (p + 1 > kSmall) return LSB_ERANGE;
+  direct_small_kernel<<<1, kSmall, 0, st>>>(S, it, col, p, gc);
   return check_launch("direct_small");
 }
 int launch_cycle_begin(const lsb_arnoldi& S, cudaStream_t st) {
@@ -290,18 +307,24 @@ int launch_restart_check(const lsb_arnoldi& S, int first, cudaStream_t st) {
   return check_launch("restart_check");
 }
 
-
 // ------------------------------------------------------------------ standalone Givens / LSQ
 // givens_update(state, h_col, i) and solve_least_squares(state, k) of the
-// public API (gmres.py:153-192) on device-resident GivensState arrays.
+// public API (gmres.py:153-192) on device-resident GivensState arrays --
+// the same fold the cycle kernels run.
 __global__ void givens_update_kernel(double* rot, double* g, double* tri, int m, const double* hin,
                                      int i, double* res_out) {
-  if (threadIdx.x != 0) return;
-  double h[kSmall + 4];
-  for (int j = 0; j <= i; ++j) h[j] = hin[j];
-  const double res = givens_fold(h, rot, g, i);
-  for (int j = 0; j <= i; ++j) tri[(int64_t)j * m + (i - 1)] = h[j];
-  *res_out = res;
+  __shared__ double h[kSmall + 2];
+  __shared__ double r[2 * kSmall];
+  for (int j = threadIdx.x; j <= i; j += blockDim.x) h[j] = hin[j];
+  for (int j = threadIdx.x; j < 2 * (i - 1); j += blockDim.x) r[j] = rot[j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *res_out = givens_fold(h, r, g, i);
+    rot[2 * (i - 1)] = r[2 * (i - 1)];
+    rot[2 * (i - 1) + 1] = r[2 * (i - 1) + 1];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j <= i; j += blockDim.x) tri[(int64_t)j * m + (i - 1)] = h[j];
 }
 
 __global__ void back_substitute_kernel(const double* tri, const double* g, int m, int k, double* y,
@@ -320,7 +343,7 @@ __global__ void back_substitute_kernel(const double* tri, const double* g, int m
 int launch_givens_update(double* rot, double* g, double* tri, int m, const double* h, int i,
                          double* res, cudaStream_t st) {
   if (i < 1 || i > m || m + 1 > kSmall) return LSB_ERANGE;
-  givens_update_kernel<<<1, 32, 0, st>>>(rot, g, tri, m, h, i, res);
+  givens_update_kernel<<<1, 128, 0, st>>>(rot, g, tri, m, h, i, res);
   return check_launch("givens_update");
 }
 int launch_back_substitute(const double* tri, const double* g, int m, int k, double* y, int* status,
