@@ -186,6 +186,13 @@ int lsb_scale_div(const double* x, int64_t n, const double* s, double* out,
 /* Gloc = [Q^T u, Q^T w] (p x 2): _lagged_reduce (gram_schmidt.py:195-203). */
 int lsb_lagged_reduce(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream);
 
+/* Fused V[:,p] = A V[:,p-1] (7-point stencil in laplace3d's canonical
+ * column order, bitwise = spmv, kernels.py:256-272) and Gloc = [Q^T u, Q^T w]
+ * in one pass: the `V.push(_op(V.column(i)))` + `_lagged_reduce` pair of
+ * gmres.py:411-414.  Ghost planes (multi-rank) must already be in place. */
+int lsb_lagged_reduce_spmv7(const lsb_arnoldi* S, const lsb_stencil* A, int32_t it, int32_t p,
+                            void* stream);
+
 /* Small-state update of the one-reduce MGS-CWY kernel: beta, breakdown test,
  * R/T columns, c = T^T y (/beta).  givens_col > 0 also folds Hessenberg
  * column givens_col-1 = R[0..givens_col, givens_col] into the Givens state

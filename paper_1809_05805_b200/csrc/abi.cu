@@ -57,6 +57,7 @@ int launch_cycle_begin(const lsb_arnoldi&, cudaStream_t);
 int launch_cycle_lsq(const lsb_arnoldi&, cudaStream_t);
 int launch_restart_check(const lsb_arnoldi&, int, cudaStream_t);
 int launch_givens_update(double*, double*, double*, int, const double*, int, double*, cudaStream_t);
+int launch_lagged_reduce_spmv7(const lsb_arnoldi&, const lsb_stencil*, int, int, cudaStream_t);
 int launch_back_substitute(const double*, const double*, int, int, double*, int*, cudaStream_t);
 
 static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -138,6 +139,13 @@ int lsb_lagged_reduce(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream)
   const double* u = S->V + (int64_t)(p - 1) * S->ld;
   const double* w = S->V + (int64_t)p * S->ld;
   return launch_mdot(S->V, S->ld, S->n, p, u, w, S->Gloc, &S->ws, S->flags, it, S_(stream));
+}
+
+int lsb_lagged_reduce_spmv7(const lsb_arnoldi* S, const lsb_stencil* A, int32_t it, int32_t p,
+                            void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (!A) return LSB_EINVAL;
+  return launch_lagged_reduce_spmv7(*S, A, it, p, S_(stream));
 }
 
 int lsb_mgs_lvl2_small(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,

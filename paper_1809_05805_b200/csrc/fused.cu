@@ -1,0 +1,263 @@
+// K1+K6 fused: w = A u (7-point stencil, bitwise as the reference SpMV) and
+// G = [Q^T u, Q^T w] in one pass over the basis.
+//
+// In the lagged loop the SpMV input u = V[:, p-1] is also the last column
+// of Q, and its output w = V[:, p] is immediately reduced against Q
+// (gmres.py:411-414 -> gram_schmidt.py:195-203).  Separately that costs the
+// SpMV 16n bytes (read u, write w) plus K1 re-reading w: 8n(p+1) + 16n.
+// Fused, each persistent CTA stages, with cp.async double-buffered one tile
+// ahead, its u tile together with the stencil's halo -- nx rows either side
+// and the two z-neighbour tiles (hot in L2: other CTAs of the same wave
+// stream them) -- computes the tile's w rows entirely from shared memory,
+// writes w once to HBM and keeps it in shared memory for the column sweep:
+// 8n(p+1) bytes of compulsory HBM traffic, w never read back.
+#include "tile.cuh"
+
+namespace lsb {
+
+struct Stencil7 {
+  int nx, ny, zlo, zhi, plane;
+  double c0, c1, c2, c3, c4, c5, c6;
+  FastDiv fx, fy;
+  int64_t lo_valid, hi_valid;  // u rows that exist in memory (ghost planes included)
+};
+
+// stage rows [a, a + len) of u into dst (len even, a even); rows outside
+// [lo, hi) are zero-filled (never consumed: their presence flag is false)
+__device__ __forceinline__ void stage_rows(double* dst, const double* u, int64_t a, int len,
+                                           int64_t lo, int64_t hi) {
+  for (int j = threadIdx.x; j < len / 2; j += kThreads) {
+    const int64_t r = a + 2 * j;
+    if (r >= lo && r + 1 < hi) {
+      cp_async16(dst + 2 * j, u + r);
+    } else {
+      dst[2 * j] = (r >= lo && r < hi) ? u[r] : 0.0;
+      dst[2 * j + 1] = (r + 1 >= lo && r + 1 < hi) ? u[r + 1] : 0.0;
+    }
+  }
+}
+
+template <int R, int SLOTS>
+__global__ void __launch_bounds__(kThreads, 2)
+mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
+                  double* __restrict__ wout, const Stencil7 K, double* __restrict__ out,
+                  double* __restrict__ partial, unsigned* counter, lsb_flags* flags, int it) {
+  if (gated_off(flags, it)) return;
+  constexpr int kRows = kTile / R;
+  constexpr int kLd = kRows / 64;
+  extern __shared__ __align__(16) double smem[];
+  const int H = K.nx;                          // row halo each side
+  const int span = kTile + 2 * H;              // u tile with halo
+  const int stage = span + 2 * kTile;          // + z-1 and z+1 tiles
+  double* sw = smem + 2 * stage;               // w tile
+  __shared__ double red[kWarps * SLOTS][2];
+  const double* __restrict__ u = X + (int64_t)(p - 1) * ld;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int part = warp % R;
+  double acc[SLOTS][2];
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) acc[s][0] = acc[s][1] = 0.0;
+  bool bad = false;
+
+  auto stage_all = [&](int b, int64_t t) {
+    double* base = smem + b * stage;
+    const int64_t r0 = t * kTile;
+    stage_rows(base, u, r0 - H, span, K.lo_valid, K.hi_valid);
+    stage_rows(base + span, u, r0 - K.plane, kTile, K.lo_valid, K.hi_valid);
+    stage_rows(base + span + kTile, u, r0 + K.plane, kTile, K.lo_valid, K.hi_valid);
+  };
+
+  const int64_t ntiles = (n + kTile - 1) / kTile;
+  int64_t t = blockIdx.x;
+  int buf = 0;
+  if (t < ntiles) stage_all(0, t);
+  cp_async_commit();
+  for (; t < ntiles; t += gridDim.x) {
+    // two barriers per tile: (A) tile t staged and every warp done with
+    // tile t-1 (so buf^1 and sw are free), (B) w of tile t complete
+    cp_async_wait<0>();
+    __syncthreads();
+    const int64_t tn = t + gridDim.x;
+    if (tn < ntiles) stage_all(buf ^ 1, tn);
+    cp_async_commit();
+    const int64_t r0 = t * kTile;
+    const double* ut = smem + buf * stage + H;   // ut[lr] = u[r0 + lr], lr in [-H, kTile+H)
+    const double* zt = smem + buf * stage + span;
+    const double* pt = zt + kTile;
+    // ---- w = A u for the tile rows (row pairs; nx even keeps pairs in a line)
+    for (int j = threadIdx.x; j < kTile / 2; j += kThreads) {
+      const int lr = 2 * j;
+      const int64_t r = r0 + lr;
+      if (r >= n) { sw[lr] = sw[lr + 1] = 0.0; continue; }
+      const uint32_t line = K.fx.div((uint32_t)r);
+      const int ix = (int)((uint32_t)r - line * (uint32_t)K.nx);
+      const uint32_t iz = K.fy.div(line);
+      const int iy = (int)(line - iz * (uint32_t)K.ny);
+      const bool pzm = (int)iz - 1 >= K.zlo, pzp = (int)iz + 1 <= K.zhi;
+      const bool pym = iy >= 1, pyp = iy + 1 < K.ny;
+      const bool pxm = ix >= 1, pxp = ix + 2 < K.nx;
+      const double2 zm = *reinterpret_cast<const double2*>(zt + lr);
+      const double2 zp = *reinterpret_cast<const double2*>(pt + lr);
+      const double2 ym = *reinterpret_cast<const double2*>(ut + lr - K.nx);
+      const double2 yp = *reinterpret_cast<const double2*>(ut + lr + K.nx);
+      const double2 cc = *reinterpret_cast<const double2*>(ut + lr);
+      const double xm = ut[lr - 1], xp = ut[lr + 2];
+      double f0 = 0.0, a0 = -0.0, f1 = 0.0, a1 = -0.0;
+      bool h0 = false, h1 = false;
+#define LSB_T(pres, c, v, f, a, h)                 \
+      if (pres) {                                   \
+        const double pv = __dmul_rn(c, v);          \
+        if (h) a = __dadd_rn(a, pv); else f = pv;   \
+        h = true;                                   \
+      }
+      LSB_T(pzm, K.c0, zm.x, f0, a0, h0) LSB_T(pzm, K.c0, zm.y, f1, a1, h1)
+      LSB_T(pym, K.c1, ym.x, f0, a0, h0) LSB_T(pym, K.c1, ym.y, f1, a1, h1)
+      LSB_T(pxm, K.c2, xm, f0, a0, h0)   LSB_T(true, K.c2, cc.x, f1, a1, h1)
+      LSB_T(true, K.c3, cc.x, f0, a0, h0) LSB_T(true, K.c3, cc.y, f1, a1, h1)
+      LSB_T(true, K.c4, cc.y, f0, a0, h0) LSB_T(pxp, K.c4, xp, f1, a1, h1)
+      LSB_T(pyp, K.c5, yp.x, f0, a0, h0) LSB_T(pyp, K.c5, yp.y, f1, a1, h1)
+      LSB_T(pzp, K.c6, zp.x, f0, a0, h0) LSB_T(pzp, K.c6, zp.y, f1, a1, h1)
+#undef LSB_T
+      const double s0 = __dadd_rn(f0, a0), s1 = __dadd_rn(f1, a1);
+      if (!isfinite(s0) || !isfinite(s1)) bad = true;
+      sw[lr] = s0;
+      sw[lr + 1] = s1;
+      *reinterpret_cast<double2*>(wout + r) = make_double2(s0, s1);
+    }
+    __syncthreads();
+    // ---- column sweep: [Q^T u, Q^T w] partials (same item deal as mdot_kernel)
+    const bool full = r0 + kTile <= n;
+    const int rbase = part * kRows;
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const int k = (warp + kWarps * s) / R;
+      if (k < p) {
+        const double* col = X + (int64_t)k * ld + r0 + rbase;
+        double a0 = 0.0, a1 = 0.0;
+        if (full) {
+          double2 xv[kLd];
+#pragma unroll
+          for (int q = 0; q < kLd; ++q) xv[q] = ld_stream(col + 2 * (lane + 32 * q));
+#pragma unroll
+          for (int q = 0; q < kLd; ++q) {
+            const int lr = rbase + 2 * (lane + 32 * q);
+            const double2 yu = *reinterpret_cast<const double2*>(ut + lr);
+            const double2 yw = *reinterpret_cast<const double2*>(sw + lr);
+            a0 = fma(xv[q].x, yu.x, a0);
+            a0 = fma(xv[q].y, yu.y, a0);
+            a1 = fma(xv[q].x, yw.x, a1);
+            a1 = fma(xv[q].y, yw.y, a1);
+          }
+        } else {
+          for (int q = 0; q < kLd; ++q) {
+            const int lr = rbase + 2 * (lane + 32 * q);
+            const int64_t r = r0 + lr;
+            const double xa = r < n ? col[lr - rbase] : 0.0;
+            const double xb = r + 1 < n ? col[lr - rbase + 1] : 0.0;
+            const double ua = r < n ? ut[lr] : 0.0, ub = r + 1 < n ? ut[lr + 1] : 0.0;
+            a0 = fma(xa, ua, a0);
+            a0 = fma(xb, ub, a0);
+            a1 = fma(xa, sw[lr], a1);
+            a1 = fma(xb, sw[lr + 1], a1);
+          }
+        }
+        acc[s][0] += a0;
+        acc[s][1] += a1;
+      }
+    }
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+  if (bad && flags) flags->nonfinite = 1;
+
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const double x = warp_sum(acc[s][v]);
+      if (lane == 0) red[warp + kWarps * s][v] = x;
+    }
+  __syncthreads();
+  const int G = gridDim.x;
+  for (int e = threadIdx.x; e < p * 2; e += kThreads) {
+    const int k = e / 2, v = e % 2;
+    double x = red[k * R][v];
+#pragma unroll
+    for (int pr = 1; pr < R; ++pr) x += red[k * R + pr][v];
+    partial[(size_t)e * G + blockIdx.x] = x;
+  }
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(counter, 1u) == (unsigned)G - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int e = warp; e < 2 * p; e += kWarps) {
+    double x = 0.0;
+    for (int c = lane; c < G; c += 32) x += __ldcg(partial + (size_t)e * G + c);
+    x = warp_sum(x);
+    if (lane == 0) out[e] = x;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+static size_t smem_bytes(int nx) { return sizeof(double) * (2 * (kTile + 2 * nx + 2 * kTile) + kTile); }
+
+template <int R, int SLOTS>
+static int launch_t(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cudaStream_t st) {
+  static int occ_nx = -1, occ = 0;
+  const size_t sm = smem_bytes(K.nx);
+  if (occ_nx != K.nx) {
+    cudaFuncSetAttribute(mdot_spmv7_kernel<R, SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mdot_spmv7_kernel<R, SLOTS>, kThreads, sm);
+    if (occ < 1) occ = 1;
+    occ_nx = K.nx;
+  }
+  const int64_t ntiles = (S.n + kTile - 1) / kTile;
+  int64_t grid = (int64_t)sm_count() * occ;
+  if (S.ws.grid > 0 && S.ws.grid < grid) grid = S.ws.grid;
+  if (grid > ntiles) grid = ntiles;
+  if (grid < 1) grid = 1;
+  mdot_spmv7_kernel<R, SLOTS><<<(unsigned)grid, kThreads, sm, st>>>(
+      S.V, S.ld, S.n, p, S.V + (int64_t)p * S.ld, K, S.Gloc, S.ws.partial, S.ws.counter,
+      S.flags, it);
+  return check_launch("mdot_spmv7");
+}
+
+template <int R>
+static int launch_r(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cudaStream_t st) {
+  const int s = slots_for(p, R);
+  if (s <= 1) return launch_t<R, 1>(S, K, p, it, st);
+  if (s <= 2) return launch_t<R, 2>(S, K, p, it, st);
+  if (s <= 4) return launch_t<R, 4>(S, K, p, it, st);
+  if (s <= 8) return launch_t<R, 8>(S, K, p, it, st);
+  if (s <= 13) return launch_t<R, 13>(S, K, p, it, st);
+  return launch_t<R, 16>(S, K, p, it, st);
+}
+
+int launch_lagged_reduce_spmv7(const lsb_arnoldi& S, const lsb_stencil* A, int it, int p,
+                               cudaStream_t st) {
+  if (!canonical7(A) || A->nx > kTile) return LSB_EINVAL;
+  if ((int64_t)A->nx * A->ny * A->nz != S.n || (S.n & 1) || p < 1 || p > 128 || p + 1 > S.cap)
+    return LSB_ERANGE;
+  Stencil7 K;
+  K.nx = A->nx; K.ny = A->ny; K.plane = A->nx * A->ny;
+  K.zlo = A->halo_lo ? -1 : 0;
+  K.zhi = A->halo_hi ? A->nz : A->nz - 1;
+  K.c0 = A->val[0]; K.c1 = A->val[1]; K.c2 = A->val[2]; K.c3 = A->val[3];
+  K.c4 = A->val[4]; K.c5 = A->val[5]; K.c6 = A->val[6];
+  K.fx = FastDiv::make((uint32_t)A->nx);
+  K.fy = FastDiv::make((uint32_t)A->ny);
+  K.lo_valid = A->halo_lo ? -(int64_t)K.plane : 0;
+  K.hi_valid = S.n + (A->halo_hi ? K.plane : 0);
+  switch (choose_parts(p)) {
+    case 8: return launch_r<8>(S, K, p, it, st);
+    case 4: return launch_r<4>(S, K, p, it, st);
+    case 2: return launch_r<2>(S, K, p, it, st);
+    default: return launch_r<1>(S, K, p, it, st);
+  }
+}
+
+}  // namespace lsb

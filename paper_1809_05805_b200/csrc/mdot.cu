@@ -17,47 +17,9 @@
 //   * at the end one butterfly per item, parts combined in fixed order in
 //     shared memory, and the last CTA sums the per-CTA partials in a fixed
 //     order: deterministic, bitwise reproducible run to run.
-#include "reduce.cuh"
+#include "tile.cuh"
 
 namespace lsb {
-
-constexpr int kTile = 1024;  // rows per tile
-
-__device__ __forceinline__ double2 ld_stream(const double* p) {
-  double2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
-               : "=d"(r.x), "=d"(r.y) : "l"(p));
-  return r;
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
-
-// stage tile t's u/w rows into buf (async when the tile is full)
-template <int NV>
-__device__ __forceinline__ void stage_tile(double2 (*buf)[kTile / 2], const double* y0,
-                                           const double* y1, int64_t n, int64_t t) {
-  const int64_t r0 = t * kTile;
-  if (r0 + kTile <= n) {
-    for (int j = threadIdx.x; j < kTile / 2; j += kThreads)
-#pragma unroll
-      for (int v = 0; v < NV; ++v) cp_async16(&buf[v][j], (v == 0 ? y0 : y1) + r0 + 2 * j);
-  } else {
-    for (int j = threadIdx.x; j < kTile / 2; j += kThreads) {
-      const int64_t r = r0 + 2 * j;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const double* y = v == 0 ? y0 : y1;
-        buf[v][j] = make_double2(r < n ? y[r] : 0.0, r + 1 < n ? y[r + 1] : 0.0);
-      }
-    }
-  }
-}
 
 template <int NV, int R, int SLOTS>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -84,11 +46,13 @@ mdot_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
   if (t < ntiles) stage_tile<NV>(sy[0], y0, y1, n, t);
   cp_async_commit();
   for (; t < ntiles; t += gridDim.x) {
+    // one barrier per tile: tile t staged and every warp done with tile
+    // t-1, so buf^1 can be refilled while tile t is swept
+    cp_async_wait<0>();
+    __syncthreads();
     const int64_t tn = t + gridDim.x;
     if (tn < ntiles) stage_tile<NV>(sy[buf ^ 1], y0, y1, n, tn);
     cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
     const int64_t r0 = t * kTile;
     const bool full = r0 + kTile <= n;
     const int jbase = part * (kRows / 2);
@@ -130,7 +94,6 @@ mdot_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
         for (int v = 0; v < NV; ++v) acc[s][v] += a[v];
       }
     }
-    __syncthreads();
     buf ^= 1;
   }
   cp_async_wait<0>();
@@ -189,9 +152,6 @@ static int launch_mdot_t(const double* X, int64_t ld, int64_t n, int p, const do
   return check_launch("mdot");
 }
 
-// slots needed for p columns cut in R parts over 8 warps
-static inline int slots_for(int p, int R) { return (p * R + kWarps - 1) / kWarps; }
-
 template <int NV, int R>
 static int launch_mdot_r(const double* X, int64_t ld, int64_t n, int p, const double* u,
                          const double* w, double* out, const lsb_workspace* ws,
@@ -203,20 +163,6 @@ static int launch_mdot_r(const double* X, int64_t ld, int64_t n, int p, const do
   if (s <= 8) return launch_mdot_t<NV, R, 8>(X, ld, n, p, u, w, out, ws, gate, it, st);
   if (s <= 13) return launch_mdot_t<NV, R, 13>(X, ld, n, p, u, w, out, ws, gate, it, st);
   return launch_mdot_t<NV, R, 16>(X, ld, n, p, u, w, out, ws, gate, it, st);
-}
-
-// Choose R in {1,2,4,8}: least idle (column, part) slots, at most 16 slots
-// per warp, ties to the smaller R (longer contiguous runs per item).
-static int choose_parts(int p) {
-  int best = 1;
-  double best_eff = 0.0;
-  for (int R = 1; R <= 8; R *= 2) {
-    const int s = slots_for(p, R);
-    if (s > 16) break;
-    const double eff = (double)(p * R) / (double)(s * kWarps);
-    if (eff > best_eff + 1e-9) { best_eff = eff; best = R; }
-  }
-  return best;
 }
 
 template <int NV>

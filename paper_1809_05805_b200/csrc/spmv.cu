@@ -13,26 +13,9 @@
 // 7-point operator additionally works on row pairs with 128-bit loads.
 // Boundary rows fall back to a packed generic path.  K7 is a general CSR
 // kernel with 32-bit indices.
-#include "reduce.cuh"
+#include "tile.cuh"
 
 namespace lsb {
-
-struct FastDiv {  // unsigned 32-bit division by an invariant d (n < 2^31)
-  uint32_t d, m, s;
-  static FastDiv make(uint32_t d) {
-    FastDiv f;
-    f.d = d;
-    f.s = 0;
-    while ((1u << f.s) < d) ++f.s;
-    const uint64_t one = 1;
-    f.m = (uint32_t)(((one << 32) * ((one << f.s) - d)) / d + 1);
-    return f;
-  }
-  __device__ __forceinline__ uint32_t div(uint32_t n) const {
-    const uint32_t t = __umulhi(n, m);
-    return (t + n) >> s;
-  }
-};
 
 struct StencilK {
   int nx, ny, nz, noff, halo_lo, halo_hi;

@@ -1,0 +1,92 @@
+// Streaming / staging helpers shared by the reduction kernels.
+#pragma once
+#include "reduce.cuh"
+
+namespace lsb {
+
+constexpr int kTile = 1024;  // rows per K1 tile
+
+// 128-bit streaming load that does not allocate in L1 (basis columns are
+// read exactly once per pass).
+__device__ __forceinline__ double2 ld_stream(const double* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// Stage rows [t*kTile, (t+1)*kTile) of y0 (and y1) into buf: cp.async for a
+// full tile, zero-padded synchronous loads for the ragged last tile.
+template <int NV>
+__device__ __forceinline__ void stage_tile(double2 (*buf)[kTile / 2], const double* y0,
+                                           const double* y1, int64_t n, int64_t t) {
+  const int64_t r0 = t * kTile;
+  if (r0 + kTile <= n) {
+    for (int j = threadIdx.x; j < kTile / 2; j += kThreads)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) cp_async16(&buf[v][j], (v == 0 ? y0 : y1) + r0 + 2 * j);
+  } else {
+    for (int j = threadIdx.x; j < kTile / 2; j += kThreads) {
+      const int64_t r = r0 + 2 * j;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const double* y = v == 0 ? y0 : y1;
+        buf[v][j] = make_double2(r < n ? y[r] : 0.0, r + 1 < n ? y[r + 1] : 0.0);
+      }
+    }
+  }
+}
+
+// Unsigned 32-bit division by an invariant d (valid for n < 2^31).
+struct FastDiv {
+  uint32_t d, m, s;
+  static FastDiv make(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    f.s = 0;
+    while ((1u << f.s) < d) ++f.s;
+    const uint64_t one = 1;
+    f.m = (uint32_t)(((one << 32) * ((one << f.s) - d)) / d + 1);
+    return f;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    const uint32_t t = __umulhi(n, m);
+    return (t + n) >> s;
+  }
+};
+
+// The 7-point operator in the canonical column order laplace3d emits
+// (-plane, -nx, -1, 0, +1, +nx, +plane), nx even, no column scaling: the
+// layout the row-pair SpMV kernels (and the fused K1+SpMV) handle.
+inline bool canonical7(const lsb_stencil* S) {
+  return S->noff == 7 && S->dz[0] == -1 && S->dx[0] == 0 && S->dy[0] == 0 && S->dy[1] == -1 &&
+         S->dx[1] == 0 && S->dz[1] == 0 && S->dx[2] == -1 && S->dy[2] == 0 && S->dz[2] == 0 &&
+         S->dx[3] == 0 && S->dy[3] == 0 && S->dz[3] == 0 && S->dx[4] == 1 && S->dy[4] == 0 &&
+         S->dz[4] == 0 && S->dy[5] == 1 && S->dx[5] == 0 && S->dz[5] == 0 && S->dz[6] == 1 &&
+         S->dx[6] == 0 && S->dy[6] == 0 && (S->nx % 2 == 0) && S->nx >= 4 && !S->col_scale;
+}
+
+// Choose R in {1,2,4,8} row parts per tile column so the p*R (column,
+// part) items deal evenly over 8 warps with at most 16 items per warp.
+inline int slots_for(int p, int R) { return (p * R + kWarps - 1) / kWarps; }
+inline int choose_parts(int p) {
+  int best = 1;
+  double best_eff = 0.0;
+  for (int R = 1; R <= 8; R *= 2) {
+    const int s = slots_for(p, R);
+    if (s > 16) break;
+    const double eff = (double)(p * R) / (double)(s * kWarps);
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = R; }
+  }
+  return best;
+}
+
+}  // namespace lsb

@@ -44,6 +44,18 @@ class CycleReport:
         self.scal = scal
 
 
+_CANON7 = [(0, 0, -1), (0, -1, 0), (-1, 0, 0), (0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)]
+
+
+def _canonical7(op):
+    """7-point stencil in laplace3d's column order, nx even, unscaled:
+    eligible for the fused K1+SpMV kernel (tile.cuh canonical7)."""
+    c = getattr(op, "c", None)
+    if not isinstance(c, _abi.Stencil) or c.noff != 7 or c.col_scale or c.nx % 2 or c.nx < 4:
+        return False
+    return [(c.dx[k], c.dy[k], c.dz[k]) for k in range(7)] == _CANON7
+
+
 _REPORT = {}
 
 
@@ -59,7 +71,7 @@ def _report_buffers(m):
 
 class Engine:
     def __init__(self, A, m, method, rel_tol, btf=1.0, inv_diag=None, comm=None,
-                 diagnostics=False, use_graph=True, n_global=None, op=None):
+                 diagnostics=False, use_graph=True, n_global=None, op=None, fuse=True):
         self.dev = D.require_cuda()
         self.lib = _abi.load()
         base_op = op if op is not None else device_operator(A)
@@ -130,6 +142,9 @@ class Engine:
         self.launches_per_cycle = 0
         self._count = 0
         self.timer = None   # list -> CUDA events around K1/K2/SpMV launches (bench.py)
+        # fuse the 7-point SpMV into K1 when the operator allows it
+        self.fused7 = bool(fuse) and self.lagged and _canonical7(self.op) and self.n % 2 == 0 \
+            and self.cap - 1 <= 128
 
     # ---------------------------------------------------------------- helpers
     def _vec_with_halo(self):
@@ -147,7 +162,10 @@ class Engine:
     def col(self, j):
         return self.Vstore[j, self.off:self.off + self.n]
 
-    _TIMED = {"lsb_lagged_reduce": "lagged_reduce", "lsb_lagged_update": "lagged_update"}
+    # kernel -> (bench label, index of p in the argument list)
+    _TIMED = {"lsb_lagged_reduce": ("lagged_reduce", 2),
+              "lsb_lagged_reduce_spmv7": ("lagged_reduce_spmv", 3),
+              "lsb_lagged_update": ("lagged_update", 2)}
 
     def _call(self, name, *args):
         self._count += 1
@@ -161,7 +179,8 @@ class Engine:
             _abi.check(rc, name)
         if tm:
             e1.record()
-            self.timer.append((self._TIMED[name], int(args[2]), e0, e1))
+            label, ip = self._TIMED[name]
+            self.timer.append((label, int(args[ip]), e0, e1))
 
     def _gather(self, count):
         """All ranks' local reduction results -> G (one collective)."""
@@ -241,8 +260,13 @@ class Engine:
         two = self.method == "two_sync_cgs2"
         for i in range(0, m + 1):
             p = i + 1
-            self._op_col(i, i + 1, i)                        # V.push(A v_i)
-            self._call("lsb_lagged_reduce", S, i, p, st)     # one pass: [Q^T u, Q^T w]
+            if self.fused7:                                  # w = A u and [Q^T u, Q^T w], one pass
+                if self.comm is not None and self.halo:
+                    self.comm.halo(self.Vstore[i], self.off, self.n, self.halo)
+                self._call("lsb_lagged_reduce_spmv7", S, C.byref(self.op.c), i, p, st)
+            else:
+                self._op_col(i, i + 1, i)                    # V.push(A v_i)
+                self._call("lsb_lagged_reduce", S, i, p, st)  # one pass: [Q^T u, Q^T w]
             self._gather(2 * p)
             if not two:
                 self._call("lsb_mgs_lvl2_small", S, i, p, 1, i, st)

@@ -363,6 +363,27 @@ def test_device_inputs_stay_on_device(P):
     assert float(torch.linalg.vector_norm(r)) <= 1.01e-8
 
 
+@pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2"])
+def test_fused_spmv_k1_bitwise_equals_unfused(P, meth):
+    """The fused K1+SpMV kernel computes the same w bits (reference SpMV
+    order) and the same reduction tree as SpMV followed by K1."""
+    from paper_1809_05805_b200.engine import Engine
+    A = P.gen_laplace3d(40)
+    b = torch.as_tensor(P.gen_rhs("random", A, 7), device="cuda")
+    reps = []
+    for fuse in (True, False):
+        eng = Engine(A, 30, meth, 1e-12, fuse=fuse, use_graph=False)
+        assert eng.fused7 == fuse
+        eng.load(b)
+        eng.prologue()
+        r = [eng.cycle() for _ in range(2)]
+        reps.append((np.concatenate([x.res for x in r]), eng.x_view().cpu().numpy(),
+                     eng.Vstore[:31, : eng.n].cpu().numpy()))
+    assert np.array_equal(reps[0][0], reps[1][0])
+    assert np.array_equal(reps[0][1], reps[1][1])
+    assert np.array_equal(reps[0][2], reps[1][2])
+
+
 # ------------------------------------------------------------------ full-size properties
 def test_c2_scale_one_cycle_properties(P):
     """n = 16.7M (256^3), one GMRES(50) cycle: the basis stays orthonormal,
