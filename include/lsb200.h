@@ -243,6 +243,12 @@ int lsb_cycle_begin(const lsb_arnoldi* S, void* stream);
 int lsb_cycle_lsq(const lsb_arnoldi* S, void* stream);
 /* x <- x + Mi (V_k y)   (_extract, gmres.py:294-297); col_scale optional. */
 int lsb_cycle_extract(const lsb_arnoldi* S, double* x, const double* col_scale, void* stream);
+/* True-residual probe of iteration `it` (true_residual_every,
+ * gmres.py:273-283): y = back-substitution of the first `it` rotated
+ * columns; xt = x + Mi (V_it y).  The caller then forms ||b - A xt||. */
+int lsb_trial_lsq(const lsb_arnoldi* S, int32_t it, double* y, void* stream);
+int lsb_trial_combine(const lsb_arnoldi* S, int32_t it, const double* x, const double* y,
+                      double* xt, const double* col_scale, void* stream);
 /* After the restart residual norm landed in scal[RNORM]:
  * first != 0 : denom/target set from it (gmres.py:472-479);
  * always     : flags->restart_ok = rnorm <= target. */

@@ -103,6 +103,8 @@ _SIGS = {
     "lsb_cycle_lsq": ([_P, _P], C.c_int),
     "lsb_cycle_extract": ([_P, _P, _P, _P], C.c_int),
     "lsb_restart_check": ([_P, _I32, _P], C.c_int),
+    "lsb_trial_lsq": ([_P, _I32, _P, _P], C.c_int),
+    "lsb_trial_combine": ([_P, _I32, _P, _P, _P, _P, _P], C.c_int),
     "lsb_gram_row": ([_P, _I32, _I32, _I32, _P, _I64, _P], C.c_int),
     "lsb_givens_update": ([_P, _P, _P, _I32, _P, _I32, _P, _P], C.c_int),
     "lsb_back_substitute": ([_P, _P, _I32, _I32, _P, _P, _P], C.c_int),

@@ -114,7 +114,7 @@ def _staging(n):
 
 def h2d(a, dev):
     st = _staging(a.size)
-    st.numpy()[:] = a
+    st.copy_(torch.from_numpy(a))               # multi-threaded host copy
     out = torch.empty(a.size, dtype=F64, device=dev)
     out.copy_(st, non_blocking=True)
     torch.cuda.current_stream().synchronize()   # staging buffer is reused
@@ -125,7 +125,9 @@ def d2h(t):
     st = _staging(t.numel())
     st.copy_(t.detach(), non_blocking=True)
     torch.cuda.current_stream().synchronize()
-    return st.numpy().copy()
+    out = torch.empty(t.numel(), dtype=F64)     # fresh result owned by numpy
+    out.copy_(st)                               # multi-threaded host copy
+    return out.numpy()
 
 
 class Workspace:

@@ -58,6 +58,9 @@ int launch_cycle_lsq(const lsb_arnoldi&, cudaStream_t);
 int launch_restart_check(const lsb_arnoldi&, int, cudaStream_t);
 int launch_givens_update(double*, double*, double*, int, const double*, int, double*, cudaStream_t);
 int launch_lagged_reduce_spmv7(const lsb_arnoldi&, const lsb_stencil*, int, int, cudaStream_t);
+int launch_trial_lsq(const lsb_arnoldi&, int, double*, cudaStream_t);
+int launch_trial_combine(const lsb_arnoldi&, int, const double*, const double*, double*,
+                         const double*, cudaStream_t);
 int launch_back_substitute(const double*, const double*, int, int, double*, int*, cudaStream_t);
 
 static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -224,6 +227,17 @@ int lsb_cycle_lsq(const lsb_arnoldi* S, void* stream) {
 int lsb_cycle_extract(const lsb_arnoldi* S, double* x, const double* col_scale, void* stream) {
   if (int rc = check_arnoldi(S)) return rc;
   return launch_extract(*S, x, col_scale, S_(stream));
+}
+
+int lsb_trial_lsq(const lsb_arnoldi* S, int32_t it, double* y, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_trial_lsq(*S, it, y, S_(stream));
+}
+
+int lsb_trial_combine(const lsb_arnoldi* S, int32_t it, const double* x, const double* y,
+                      double* xt, const double* col_scale, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_trial_combine(*S, it, x, y, xt, col_scale, S_(stream));
 }
 
 int lsb_restart_check(const lsb_arnoldi* S, int32_t first, void* stream) {

@@ -258,6 +258,34 @@ cycle_lsq_kernel(lsb_arnoldi S) {
   for (int j = lane; j < k; j += 32) S.coef2[j] = sy[j];
 }
 
+// Trial least squares of iteration `it` (k = it columns) into y, for the
+// true-residual probe (gmres.py:273-278); a zero diagonal marks y[0] NaN.
+__global__ void __launch_bounds__(32)
+trial_lsq_kernel(lsb_arnoldi S, int it, double* y) {
+  if (gated_off(S.flags, it)) return;
+  __shared__ double sy[kSmall];
+  const int lane = threadIdx.x, k = it, m = S.m;
+  for (int i = k - 1; i >= 0; --i) {
+    const double d = S.tri[(int64_t)i * m + i];
+    if (d == 0.0) {
+      if (lane == 0) y[0] = nan("");
+      return;
+    }
+    double acc = 0.0;
+    for (int j = i + 1 + lane; j < k; j += 32) acc = fma(S.tri[(int64_t)i * m + j], sy[j], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) sy[i] = __ddiv_rn(S.g[i] - acc, d);
+    __syncwarp();
+  }
+  for (int j = lane; j < k; j += 32) y[j] = sy[j];
+}
+
+int launch_trial_lsq(const lsb_arnoldi& S, int it, double* y, cudaStream_t st) {
+  if (it < 1 || it > S.m) return LSB_ERANGE;
+  trial_lsq_kernel<<<1, 32, 0, st>>>(S, it, y);
+  return check_launch("trial_lsq");
+}
+
 // First call: denom = beta0 or 1, target = rel_tol * beta0 (gmres.py:472-479).
 __global__ void restart_check_kernel(lsb_arnoldi S, int first) {
   if (threadIdx.x != 0) return;

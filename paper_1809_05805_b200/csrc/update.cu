@@ -371,4 +371,34 @@ int launch_extract(const lsb_arnoldi& S, double* x, const double* d, cudaStream_
   return check_launch("extract");
 }
 
+// xt = x + Mi (V_k y) with k = it: the trial iterate of the true-residual
+// probe (gmres.py:273-278).  y[0] NaN (singular trial) propagates.
+__global__ void __launch_bounds__(kThreads)
+trial_combine_kernel(lsb_arnoldi S, int it, const double* __restrict__ x,
+                     const double* __restrict__ y, double* __restrict__ xt,
+                     const double* __restrict__ d) {
+  if (gated_off(S.flags, it)) return;
+  extern __shared__ double sy[];
+  const int k = it;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) sy[j] = y[j];
+  __syncthreads();
+  const int64_t ld = S.ld;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < S.n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (int j = 0; j < k; ++j) acc = fma(sy[j], S.V[(int64_t)j * ld + r], acc);
+    if (d) acc = __dmul_rn(acc, d[r]);
+    xt[r] = x[r] + acc;
+  }
+}
+
+int launch_trial_combine(const lsb_arnoldi& S, int it, const double* x, const double* y,
+                         double* xt, const double* d, cudaStream_t st) {
+  if (it < 1 || it >= S.cap) return LSB_ERANGE;
+  trial_combine_kernel<<<row_grid(2 * S.n), kThreads, sizeof(double) * S.cap, st>>>(S, it, x, y,
+                                                                                  xt, d);
+  return check_launch("trial_combine");
+}
+
 }  // namespace lsb

@@ -35,13 +35,14 @@ class CycleReport:
     """Host copy of what one cycle produced."""
 
     __slots__ = ("stop_iter", "status", "broke_iter", "k", "nonfinite", "restart_ok", "res",
-                 "scal")
+                 "scal", "true_res")
 
-    def __init__(self, flags, res, scal):
+    def __init__(self, flags, res, scal, true_res=None):
         self.stop_iter, self.status, self.broke_iter, self.k, self.nonfinite, self.restart_ok = (
             int(v) for v in flags[:6])
         self.res = res
         self.scal = scal
+        self.true_res = true_res
 
 
 _CANON7 = [(0, 0, -1), (0, -1, 0), (-1, 0, 0), (0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)]
@@ -71,7 +72,8 @@ def _report_buffers(m):
 
 class Engine:
     def __init__(self, A, m, method, rel_tol, btf=1.0, inv_diag=None, comm=None,
-                 diagnostics=False, use_graph=True, n_global=None, op=None, fuse=True):
+                 diagnostics=False, use_graph=True, n_global=None, op=None, fuse=True,
+                 true_residual=False):
         self.dev = D.require_cuda()
         self.lib = _abi.load()
         base_op = op if op is not None else device_operator(A)
@@ -123,6 +125,14 @@ class Engine:
         self.rbuf = torch.zeros(self.n, **f64)
         self.gram = torch.zeros((cap, cap), **f64) if diagnostics else None
         self.diagnostics = diagnostics
+        # true-residual probe buffers (true_residual_every > 0)
+        self.true_residual = bool(true_residual)
+        if self.true_residual:
+            self.ytrial = torch.zeros(cap, **f64)
+            self.xt = self._vec_with_halo()
+            self.rtrial = torch.zeros(self.n, **f64)
+            self.true_res = torch.zeros(m + 1, **f64)
+            self.h_true = torch.zeros(m + 1, dtype=D.F64).pin_memory()
         self.S = _abi.Arnoldi(
             V=self.Vstore.data_ptr() + 8 * self.off, ld=self.ld, n=self.n, n_global=self.n_global,
             cap=cap, m=m, R=self.R.data_ptr(), T=self.T.data_ptr(), L=self.L.data_ptr(),
@@ -281,6 +291,27 @@ class Engine:
                 self._call("lsb_lagged_correct", S, i, p, st)
             if self.diagnostics:
                 self._call("lsb_gram_row", S, i, i, i + 1, D.ptr(self.gram), self.cap, st)
+            if self.true_residual and i >= 1:
+                self._trial(i, st)
+
+    def _trial(self, i, st):
+        """||b - A (x + Mi V_i y_i)|| of iteration i into true_res[i]
+        (gmres.py:273-283), gated like every other kernel of iteration i."""
+        S = self.Sref
+        xo = 8 * self.off
+        self._call("lsb_trial_lsq", S, i, D.ptr(self.ytrial), st)
+        self._call("lsb_trial_combine", S, i, C.c_void_p(self.x.data_ptr() + xo),
+                   D.ptr(self.ytrial), C.c_void_p(self.xt.data_ptr() + xo),
+                   None if self.inv_diag is None else C.c_void_p(self.inv_diag.data_ptr() + xo),
+                   st)
+        self._apply_op((self.xt, self.off), C.c_void_p(self.xt.data_ptr() + xo),
+                       D.ptr(self.rtrial), D.ptr(self.b), i)
+        self._call("lsb_norm_partial", D.ptr(self.rtrial), self.n, D.ptr(self.Gloc),
+                   self.ws.ref(), D.ptr(self.flags), i, st)
+        self._gather(2)
+        self._call("lsb_norm_finish", D.ptr(self.G), self.S.g_parts, self.S.g_stride,
+                   D.ptr(self.rtrial), self.n, C.c_void_p(self.true_res.data_ptr() + 8 * i),
+                   self.ws.ref(), D.ptr(self.flags), i, st)
 
     def _direct_body(self, st):
         S, m = self.Sref, self.m
@@ -308,6 +339,8 @@ class Engine:
             self._call("lsb_direct_normalize", S, i, i, st)
             if self.diagnostics:
                 self._call("lsb_gram_row", S, i, i, i + 1, D.ptr(self.gram), self.cap, st)
+            if self.true_residual:
+                self._trial(i, st)
 
     # ---------------------------------------------------------------- driving
     def prologue(self):
@@ -334,9 +367,12 @@ class Engine:
         self.h_flags.copy_(self.flags, non_blocking=True)
         self.h_res.copy_(self.res, non_blocking=True)
         self.h_scal.copy_(self.scal, non_blocking=True)
+        if self.true_residual:
+            self.h_true.copy_(self.true_res, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return CycleReport(self.h_flags.tolist(), self.h_res.numpy().copy(),
-                           self.h_scal.numpy().copy())
+                           self.h_scal.numpy().copy(),
+                           self.h_true.numpy().copy() if self.true_residual else None)
 
     def hessenberg(self, k):
         """Hbar_k from the R columns (R[:, j+1] rows 0..j+1 = H[:, j])."""

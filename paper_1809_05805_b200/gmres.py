@@ -220,8 +220,10 @@ class _DeviceSolve:
         if config.method not in DEVICE_METHODS:
             raise NotImplementedError(
                 f"method {config.method!r} is outside the B200 hot path (SURVEY §8f)")
-        if true_residual_every:
-            raise NotImplementedError("true_residual_every is not supported on the device path")
+        self.true_every = int(true_residual_every or 0)
+        import os
+        import time
+        self._trace = [("start", time.perf_counter())] if os.environ.get("LSB_TRACE") else None
         self.A = A
         self.comm = comm
         self.n = A.n_rows
@@ -242,6 +244,7 @@ class _DeviceSolve:
         self.history.method = config.method
         self.global_it = 0
         self.use_graph = use_graph
+        self._mark("setup")
 
     def _events_lagged(self, base, k, stop, broke_iter, two, pipeline):
         """Ledger events + per-iteration reduction counts of one lagged cycle
@@ -297,11 +300,13 @@ class _DeviceSolve:
         inv = self.pc.inv_diag
         eng = Engine(self.A, self.m, cfg.method, cfg.rel_tol, cfg.breakdown_tol_factor,
                      inv_diag=inv, diagnostics=bool(self.diag_every), use_graph=self.use_graph,
-                     comm=self.comm, n_global=self.n_global)
+                     comm=self.comm, n_global=self.n_global, true_residual=bool(self.true_every))
         self.engine = eng
+        self._mark("engine")
         eng.load(self.b, self.x0)
         led.iteration = 0
         rep = eng.prologue()
+        self._mark("prologue")
         if rep.nonfinite:
             raise NonFiniteError("spmv result contains NaN or Inf")
         beta = float(rep.scal[_abi.S_RNORM])
@@ -319,6 +324,7 @@ class _DeviceSolve:
         for _cycle in range(cfg.max_restarts):
             hist.cycle_starts.append(self.global_it)
             rep = eng.cycle()
+            self._mark("cycle")
             if rep.nonfinite:
                 raise NonFiniteError("spmv result contains NaN or Inf")
             if rep.status == _abi.STARTUP_BREAKDOWN:
@@ -338,14 +344,14 @@ class _DeviceSolve:
                 for i in range(1, k + 1):
                     self.global_it = base + i
                     ncols = i if broke == i else i + 1
-                    self._record(rep.res[i], nred[i], gram, ncols)
+                    self._record(rep.res[i], nred[i], gram, ncols, rep, i)
             else:
                 for i in range(1, k + 1):
                     self.global_it += 1
                     led.iteration = self.global_it
                     nr = self._events_direct(i, cfg.method == "cgs2")
                     ncols = i if broke == i else i + 1
-                    self._record(rep.res[i], nr, gram, ncols)
+                    self._record(rep.res[i], nr, gram, ncols, rep, i)
             if stopped:
                 status = CONVERGED if rep.status == _abi.CONVERGED else BREAKDOWN
             else:
@@ -380,19 +386,41 @@ class _DeviceSolve:
         hist.outcome = outcome
         return self._result(eng)
 
-    def _record(self, res, nred, gram, ncols):
+    def _record(self, res, nred, gram, ncols, rep=None, i=0):
+        """gmres.py:280-292: diagnostics from the device Gram rows, the
+        true-residual probe from the device trial of iteration i."""
         s = o = None
         if self.diag_every and self.global_it % self.diag_every == 0:
             Gm = gram[:ncols, :ncols]
             Gm = np.triu(Gm.T, 0) + np.triu(Gm.T, 1).T  # rows hold Q^T q_row: symmetrise
             s, o = gram_paige_metric(Gm), gram_orthogonality_loss(Gm)
+        true_rel = None
+        if self.true_every and self.global_it % self.true_every == 0 and i >= 1:
+            v = float(rep.true_res[i])
+            if np.isnan(v):
+                raise SingularHessenberg("zero diagonal in the trial least-squares solve")
+            true_rel = v / self.history.denom
         self.history.records.append(IterationRecord(
             iteration=self.global_it, implicit_rel_res=float(res) / self.history.denom,
-            s_norm=s, orth_loss=o, reductions=nred))
+            true_rel_res=true_rel, s_norm=s, orth_loss=o, reductions=nred))
 
     def _result(self, eng):
         x = eng.x_view().clone()
-        return D.out_like(x, self.host), self.history
+        out = D.out_like(x, self.host), self.history
+        self._mark("result")
+        if self._trace is not None:
+            import sys
+            t0 = self._trace[0][1]
+            sys.stderr.write("lsb trace: " + ", ".join(
+                f"{k} {1e3 * (t - t0):.1f}ms" for k, t in self._trace[1:]) + "\n")
+        return out
+
+    def _mark(self, label):
+        """LSB_TRACE=1: synchronised phase timestamps of one solve."""
+        if self._trace is not None:
+            import time
+            torch.cuda.synchronize()
+            self._trace.append((label, time.perf_counter()))
 
 
 def _run(method, A, b, x0, config, ledger, diagnostics_every, true_residual_every):

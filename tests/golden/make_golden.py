@@ -175,6 +175,31 @@ def small():
     _save("convdiff27_16.npz", **out)
 
 
+def extras():
+    """true_residual_every probes (gmres.py:273-283)."""
+    out = {}
+    A = ls.gen_simoncini(100)
+    b = ls.gen_rhs("random", A, 42)
+    for meth in ("mgs_l1", "one_sync_mgs"):
+        led = ls.ReductionLedger()
+        cfg = ls.GmresConfig(restart_m=100, max_restarts=1, rel_tol=1e-14, method=meth)
+        _, h = ls.solve(A, b, config=cfg, ledger=led, diagnostics_every=1, true_residual_every=1)
+        out[f"sim_{meth}_true"] = np.array([np.nan if r.true_rel_res is None else r.true_rel_res
+                                            for r in h.records])
+        out[f"sim_{meth}_curve"] = h.implicit_curve()
+    A = ls.gen_laplace2d(64)
+    b = ls.gen_rhs("random", A, 42)
+    for meth, te in (("one_sync_mgs", 5), ("two_sync_cgs2", 3), ("cgs2", 7)):
+        led = ls.ReductionLedger()
+        cfg = ls.GmresConfig(restart_m=30, max_restarts=200, rel_tol=1e-6, method=meth)
+        _, h = ls.solve(A, b, config=cfg, ledger=led, diagnostics_every=0, true_residual_every=te)
+        out[f"c1_{meth}_true"] = np.array([np.nan if r.true_rel_res is None else r.true_rel_res
+                                           for r in h.records])
+        out[f"c1_{meth}_curve"] = h.implicit_curve()
+        out[f"c1_{meth}_every"] = np.array(te)
+    _save("extras.npz", **out)
+
+
 def big_c2(N=256, methods=("one_sync_mgs",)):
     t0 = time.perf_counter()
     A = _ref_csr(orc.laplace3d(N))
@@ -205,6 +230,8 @@ if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what == "small":
         small()
+    elif what == "extras":
+        extras()
     elif what == "c2":
         big_c2(int(sys.argv[2]) if len(sys.argv) > 2 else 256)
     elif what == "c5":

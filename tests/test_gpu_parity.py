@@ -363,6 +363,45 @@ def test_device_inputs_stay_on_device(P):
     assert float(torch.linalg.vector_norm(r)) <= 1.01e-8
 
 
+@pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2", "cgs2"])
+def test_true_residual_probe_c1(P, meth):
+    """true_residual_every (gmres.py:273-283): device trial solution +
+    residual norm at the same iterations as the reference."""
+    E = _load("extras.npz")
+    A = P.gen_laplace2d(64)
+    b = P.gen_rhs("random", A, 42)
+    te = int(E[f"c1_{meth}_every"])
+    cfg = P.GmresConfig(restart_m=30, max_restarts=200, rel_tol=1e-6, method=meth)
+    _, h = P.solve(A, b, config=cfg, diagnostics_every=0, true_residual_every=te)
+    ref = E[f"c1_{meth}_true"]
+    ours = np.array([np.nan if r.true_rel_res is None else r.true_rel_res for r in h.records])
+    assert len(ours) == len(ref)
+    assert np.array_equal(np.isnan(ours), np.isnan(ref))
+    m = ~np.isnan(ref)
+    assert np.max(np.abs(ours[m] - ref[m]) / ref[m]) <= 1e-6
+
+
+def test_true_residual_probe_simoncini(P):
+    E = _load("extras.npz")
+    A = P.gen_simoncini(100)
+    b = P.gen_rhs("random", A, 42)
+    cfg = P.GmresConfig(restart_m=100, max_restarts=1, rel_tol=1e-14)
+    _, h = P.gmres_mgs_l1(A, b, config=cfg, true_residual_every=1)
+    ref = E["sim_mgs_l1_true"]
+    ours = np.array([r.true_rel_res for r in h.records], dtype=float)
+    assert len(ours) == len(ref)
+    sr = _load("simoncini100.npz")["mgs_l1__s_norm"]
+    # basis still independent; ||b - A x_try|| carries kappa = 1e10 cancellation
+    good = sr < 1e-3
+    assert np.max(np.abs(ours[good] - ref[good]) / ref[good]) <= 1e-4
+    ratio = ours / ref              # stall phase: same probe within 2x
+    assert np.all((ratio > 0.5) & (ratio < 2.0))
+    # the reference's own contract (test_gmres.py:193-203)
+    for r in h.records:
+        if r.s_norm is not None and r.s_norm < 0.1 and r.true_rel_res is not None:
+            assert abs(r.implicit_rel_res - r.true_rel_res) <= 1e-2 * max(r.implicit_rel_res, 1e-14)
+
+
 @pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2"])
 def test_fused_spmv_k1_bitwise_equals_unfused(P, meth):
     """The fused K1+SpMV kernel computes the same w bits (reference SpMV
