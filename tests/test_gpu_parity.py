@@ -423,6 +423,20 @@ def test_fused_spmv_k1_bitwise_equals_unfused(P, meth):
     assert np.array_equal(reps[0][2], reps[1][2])
 
 
+# ------------------------------------------------------------------ full-size parity
+def test_c2_256cube_one_sync_full_solve_matches_reference(P):
+    """BASELINE config 2 (256^3, n = 16.7M), one-sync GMRES(50), tol 1e-6,
+    run to convergence: the reference needs 1,749 iterations (35 cycles,
+    65 min on one host core); identical count, curve within 1e-10 relative
+    at every iteration, identical ledger."""
+    G = _load("laplace3d256.npz")
+    A = P.gen_laplace3d(256)
+    b = P.gen_rhs("random", A, 42)
+    x, h, led = _solve(P, A, b, "one_sync_mgs", 50, 100, 1e-6)
+    _check(h, led, G, "one_sync_mgs")
+    assert h.iterations == 1749
+
+
 # ------------------------------------------------------------------ full-size properties
 def test_c2_scale_one_cycle_properties(P):
     """n = 16.7M (256^3), one GMRES(50) cycle: the basis stays orthonormal,
