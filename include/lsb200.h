@@ -44,6 +44,7 @@ extern "C" {
 #define LSB_BREAKDOWN 2          /* HappyBreakdown inside the cycle      */
 #define LSB_STARTUP_BREAKDOWN 3  /* HappyBreakdown outside a solver loop */
 #define LSB_SINGULAR 4           /* SingularHessenberg in back-subst.    */
+#define LSB_GHYSELS_CHECK 5      /* cgs1_ghysels radicand lost its digits */
 
 #define LSB_NO_STOP 0x7fffffff
 
@@ -68,6 +69,7 @@ typedef struct lsb_flags {
 #define LSB_S_AMAX 6      /* norm pass scratch                              */
 #define LSB_S_SSQ 7
 #define LSB_S_TOL 8       /* last breakdown tolerance (for HappyBreakdown)  */
+#define LSB_S_RAD 9       /* cgs1_ghysels radicand ||z||^2 - ||y||^2        */
 #define LSB_S_COUNT 16
 
 /* Reduction workspace: partial >= lsb_partial_len() doubles, counter >= 8
@@ -232,6 +234,10 @@ int lsb_cgs_project(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p,
  * coef[0..p); Hbar column (R[:, col]); Givens fold of column col-1;
  * convergence. */
 int lsb_direct_small(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, void* stream);
+/* cgs1_ghysels small state (gmres.py:325-360): G = [Q^T z (p), max|z|,
+ * sum z^2] -> y, h = sqrt(||z||^2 - y.y), Hbar column, Givens fold; stops the
+ * cycle with LSB_GHYSELS_CHECK when the radicand cancels. */
+int lsb_ghysels_small(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, void* stream);
 /* V[:, col] /= r_diag unless the column broke down. */
 int lsb_direct_normalize(const lsb_arnoldi* S, int32_t it, int32_t col, void* stream);
 

@@ -14,11 +14,11 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LSB200_LIB", os.path.join(_HERE, "liblsb200.so"))
 
 OK, EINVAL, ECUDA, ERANGE = 0, 1, 2, 3
-RUNNING, CONVERGED, BREAKDOWN, STARTUP_BREAKDOWN, SINGULAR = 0, 1, 2, 3, 4
+RUNNING, CONVERGED, BREAKDOWN, STARTUP_BREAKDOWN, SINGULAR, GHYSELS_CHECK = 0, 1, 2, 3, 4, 5
 NO_STOP = 0x7FFFFFFF
 
 # scalar slots (LSB_S_*)
-S_BETA, S_TARGET, S_DENOM, S_RNORM, S_RELTOL, S_BTF, S_AMAX, S_SSQ, S_TOL = range(9)
+S_BETA, S_TARGET, S_DENOM, S_RNORM, S_RELTOL, S_BTF, S_AMAX, S_SSQ, S_TOL, S_RAD = range(10)
 S_COUNT = 16
 MAX_OFF = 27
 
@@ -99,6 +99,7 @@ _SIGS = {
     "lsb_cgs_project": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
     "lsb_direct_small": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_direct_normalize": ([_P, _I32, _I32, _P], C.c_int),
+    "lsb_ghysels_small": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_cycle_begin": ([_P, _P], C.c_int),
     "lsb_cycle_lsq": ([_P, _P], C.c_int),
     "lsb_cycle_extract": ([_P, _P, _P, _P], C.c_int),

@@ -212,6 +212,61 @@ direct_small_kernel(lsb_arnoldi S, int it, int col, int p, int gc) {
   }
 }
 
+// Single-pass classical GS with the Pythagorean norm substitute
+// (cgs1_ghysels, gmres.py:325-360).  G holds [Q^T z (p), max|z|, sum z^2]:
+// y = Q^T z, h = sqrt(||z||^2 - y.y).  If the radicand keeps its digits the
+// column is accepted (H[i, i-1] = h, normal settle); otherwise H[i, i-1] = 0,
+// the rotation is still folded, and the cycle stops with status
+// LSB_GHYSELS_CHECK so the host can run the true-residual arbitration of
+// gmres.py:338-359 before deciding converged / breakdown / cancellation.
+__global__ void __launch_bounds__(kSmall)
+ghysels_small_kernel(lsb_arnoldi S, int it, int col, int p) {
+  if (gated_off(S.flags, it)) return;
+  __shared__ SmallShared sh;
+  const int t = threadIdx.x, cap = S.cap;
+  for (int j = t; j < p; j += blockDim.x) {
+    const double y = gsum(S, j);
+    sh.col[j] = y;
+    S.coef[j] = y;
+    S.coef2[j] = y;
+  }
+  __syncthreads();
+  if (t == 0) {
+    const double ssq = gsum(S, p + 1);
+    const double znorm = sqrt(ssq);
+    double yy = 0.0;
+    for (int j = 0; j < p; ++j) yy = fma(sh.col[j], sh.col[j], yy);
+    const double zz = __dmul_rn(znorm, znorm);
+    const double rad = __dsub_rn(zz, yy);
+    S.scal[LSB_S_RAD] = rad;
+    // rad >= 4.0 * EPS * znorm * znorm, evaluated left to right as in Python
+    const bool ok = rad > 0.0 && rad >= __dmul_rn(__dmul_rn(__dmul_rn(4.0, kEps), znorm), znorm);
+    sh.broke = !ok;
+    if (ok) {
+      const double h = sqrt(rad);
+      S.scal[LSB_S_BETA] = h;
+      sh.col[p] = h;
+    } else {
+      S.flags->broke_iter = it;
+      sh.col[p] = 0.0;
+    }
+  }
+  __syncthreads();
+  for (int j = t; j <= p; j += blockDim.x) S.R[(int64_t)j * cap + col] = sh.col[j];
+  settle_block(S, sh, it, col, false);
+  if (t == 0 && sh.broke) {
+    // converged-or-not is decided on the host from the true residual
+    S.flags->stop_iter = it;
+    S.flags->status = LSB_GHYSELS_CHECK;
+  }
+}
+
+int launch_ghysels_small(const lsb_arnoldi& S, int it, int col, int p, cudaStream_t st) {
+  if (p + 2 > 2 * S.cap || col < 1) return LSB_ERANGE;
+  ghysels_small_kernel<<<1, kSmall, 0, st>>>(S, it, col, p);
+  return check_launch("ghysels_small");
+}
+
 // ------------------------------------------------------------------ cycle control
 __global__ void __launch_bounds__(kSmall)
 cycle_begin_kernel(lsb_arnoldi S) {
@@ -240,7 +295,8 @@ cycle_lsq_kernel(lsb_arnoldi S) {
   __shared__ double sy[kSmall];
   const int lane = threadIdx.x;
   const int stop = S.flags->stop_iter;
-  const int k = stop == LSB_NO_STOP ? S.m : stop;
+  // a cgs1_ghysels cancellation check leaves the extract to the host
+  const int k = S.flags->status == LSB_GHYSELS_CHECK ? 0 : (stop == LSB_NO_STOP ? S.m : stop);
   if (lane == 0) S.flags->k = k;
   const int m = S.m;
   for (int i = k - 1; i >= 0; --i) {

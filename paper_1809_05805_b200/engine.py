@@ -313,6 +313,49 @@ class Engine:
                    D.ptr(self.rtrial), self.n, C.c_void_p(self.true_res.data_ptr() + 8 * i),
                    self.ws.ref(), D.ptr(self.flags), i, st)
 
+    # ---- host-driven pieces of the cgs1_ghysels cancellation arbitration
+    def _ensure_trial_buffers(self):
+        if not hasattr(self, "xt"):
+            f64 = dict(dtype=D.F64, device=self.dev)
+            self.ytrial = torch.zeros(self.cap, **f64)
+            self.xt = self._vec_with_halo()
+            self.rtrial = torch.zeros(self.n, **f64)
+            self.true_res = torch.zeros(self.m + 1, **f64)
+
+    def trial_residual(self, k):
+        """(||b - A (x + Mi V_k y_k)||, singular?) for iteration k, eagerly
+        (gmres.py:338-348); the trial iterate stays in self.xt."""
+        self._ensure_trial_buffers()
+        st = D.stream()
+        self._call("lsb_trial_lsq", self.Sref, k, D.ptr(self.ytrial), st)
+        if bool(torch.isnan(self.ytrial[0])):
+            return float("inf"), True
+        self._trial(k, st)
+        return float(self.true_res[k].item()), False
+
+    def accept_trial(self):
+        self.x_view().copy_(self.xt[self.off:self.off + self.n])
+
+    def extract_k(self, k):
+        """x <- x + Mi V_k y_k with the first k rotated columns (_extract)."""
+        if k < 1:
+            return
+        self._ensure_trial_buffers()
+        st = D.stream()
+        xo = 8 * self.off
+        self._call("lsb_trial_lsq", self.Sref, k, D.ptr(self.ytrial), st)
+        self._call("lsb_trial_combine", self.Sref, k, C.c_void_p(self.x.data_ptr() + xo),
+                   D.ptr(self.ytrial), C.c_void_p(self.xt.data_ptr() + xo),
+                   None if self.inv_diag is None else C.c_void_p(self.inv_diag.data_ptr() + xo),
+                   st)
+        self.accept_trial()
+
+    def refresh_residual(self):
+        """Restart residual + norm for the current x, then a fresh report."""
+        self._residual_and_norm()
+        self._call("lsb_restart_check", self.Sref, 0, D.stream())
+        return self.report()
+
     def _direct_body(self, st):
         S, m = self.Sref, self.m
         if self.diagnostics:
@@ -320,6 +363,22 @@ class Engine:
         for i in range(1, m + 1):
             p = i
             self._op_col(i - 1, i, i)                        # z = A v_{i-1}, in place in V[:, i]
+            if self.method == "cgs1_ghysels":
+                # one fused reduction: [Q^T z, max|z|, sum z^2] (fused_mdot_norm)
+                self._call("lsb_mdot", self.col_ptr(0), self.ld, self.n, p, self.col_ptr(i), None,
+                           D.ptr(self.Gloc), self.ws.ref(), D.ptr(self.flags), i, st)
+                self._call("lsb_norm_partial", self.col_ptr(i), self.n,
+                           C.c_void_p(self.Gloc.data_ptr() + 8 * p), self.ws.ref(),
+                           D.ptr(self.flags), i, st)
+                self._gather(p + 2)
+                self._call("lsb_ghysels_small", S, i, i, p, st)
+                self._call("lsb_cgs_project", S, i, i, p, 0, st)
+                self._call("lsb_direct_normalize", S, i, i, st)
+                if self.diagnostics:
+                    self._call("lsb_gram_row", S, i, i, i + 1, D.ptr(self.gram), self.cap, st)
+                if self.true_residual:
+                    self._trial(i, st)
+                continue
             if self.method == "mgs_l1":
                 for k in range(p + 1):
                     self._call("lsb_mgs1_pass", S, i, i, k, p, st)

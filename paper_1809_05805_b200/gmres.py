@@ -34,7 +34,7 @@ _ALIASES = {
     "two-sync": "two_sync_cgs2", "two_sync": "two_sync_cgs2",
     "one-sync": "one_sync_mgs", "one_sync": "one_sync_mgs",
 }
-DEVICE_METHODS = ("mgs_l1", "cgs2", "two_sync_cgs2", "one_sync_mgs", "pipeline2")
+DEVICE_METHODS = METHODS
 
 
 def canonical_method(name):
@@ -320,6 +320,7 @@ class _DeviceSolve:
             return self._result(eng)
         target = cfg.rel_tol * beta
         outcome = None
+        saw_cancellation = False
         lagged = cfg.method in ("one_sync_mgs", "two_sync_cgs2", "pipeline2")
         for _cycle in range(cfg.max_restarts):
             hist.cycle_starts.append(self.global_it)
@@ -337,6 +338,7 @@ class _DeviceSolve:
             broke = rep.broke_iter if rep.broke_iter >= 1 else None
             gram = eng.gram.cpu().numpy() if self.diag_every else None
             base = self.global_it
+            decided = None
             if lagged:
                 nred = self._events_lagged(base, k, k if stopped else None, broke,
                                            cfg.method == "two_sync_cgs2",
@@ -345,6 +347,36 @@ class _DeviceSolve:
                     self.global_it = base + i
                     ncols = i if broke == i else i + 1
                     self._record(rep.res[i], nred[i], gram, ncols, rep, i)
+            elif cfg.method == "cgs1_ghysels":
+                check = rep.status == _abi.GHYSELS_CHECK
+                last = k - 1 if check else k
+                stop_col = k
+                for i in range(1, last + 1):
+                    self.global_it += 1
+                    led.iteration = self.global_it
+                    led.record(FUSED, i + 1)
+                    self._record(rep.res[i], 1, gram, i + 1, rep, i)
+                if check:
+                    # gmres.py:333-360: the Pythagorean radicand lost its
+                    # digits -- arbitrate with the true residual of the trial
+                    i = k
+                    self.global_it += 1
+                    led.iteration = self.global_it
+                    mark = len(led)
+                    led.record(FUSED, i + 1)
+                    true_abs, singular = eng.trial_residual(i)
+                    if not singular:
+                        led.record(NORM, 1)
+                    rad = float(rep.scal[_abi.S_RAD])
+                    if not singular and (true_abs <= target or rad == 0.0):
+                        self._record(rep.res[i], len(led) - mark, gram, i, rep, i)
+                        eng.accept_trial()
+                        decided = CONVERGED if true_abs <= target else BREAKDOWN
+                    else:
+                        k = i - 1                  # aborted attempt: nothing recorded
+                        eng.extract_k(k)
+                        decided = CANCELLATION_FAILURE
+                    rep = eng.refresh_residual()
             else:
                 for i in range(1, k + 1):
                     self.global_it += 1
@@ -352,12 +384,16 @@ class _DeviceSolve:
                     nr = self._events_direct(i, cfg.method == "cgs2")
                     ncols = i if broke == i else i + 1
                     self._record(rep.res[i], nr, gram, ncols, rep, i)
-            if stopped:
+            if decided is not None:
+                status = decided
+            elif stopped:
                 status = CONVERGED if rep.status == _abi.CONVERGED else BREAKDOWN
             else:
                 status = "full"
             if lagged:
                 ncols_norm = k + (0 if status == BREAKDOWN else 1)
+            elif cfg.method == "cgs1_ghysels":
+                ncols_norm = stop_col if decided is not None else k + 1
             else:
                 ncols_norm = k if broke == k else k + 1
             hist.k = k
@@ -366,6 +402,8 @@ class _DeviceSolve:
             if status in (CONVERGED, BREAKDOWN):
                 outcome = status
                 break
+            if status == CANCELLATION_FAILURE:
+                saw_cancellation = True
             led.iteration = self.global_it
             led.record(NORM, 1)
             beta = float(rep.scal[_abi.S_RNORM])
@@ -376,7 +414,7 @@ class _DeviceSolve:
                 outcome = CONVERGED
                 break
         if outcome is None:
-            outcome = STALLED_MAXITER
+            outcome = CANCELLATION_FAILURE if saw_cancellation else STALLED_MAXITER
         led.iteration = self.global_it
         led.record(NORM, 1)
         final_rel = float(rep.scal[_abi.S_RNORM]) / hist.denom
@@ -425,8 +463,6 @@ class _DeviceSolve:
 
 def _run(method, A, b, x0, config, ledger, diagnostics_every, true_residual_every):
     config = replace(config, method=method) if config is not None else GmresConfig(method=method)
-    if method == "cgs1_ghysels":
-        raise NotImplementedError("cgs1_ghysels is outside the B200 hot path (SURVEY §8f)")
     return _DeviceSolve(A, b, x0, config, ledger, diagnostics_every, true_residual_every).run()
 
 
@@ -444,7 +480,9 @@ def gmres_cgs2(A, b, x0=None, config=None, ledger=None, diagnostics_every=1,
 
 def gmres_cgs1_ghysels(A, b, x0=None, config=None, ledger=None, diagnostics_every=1,
                        true_residual_every=0):
-    """Not on the B200 path: raises NotImplementedError."""
+    """Single-pass classical GS with the Pythagorean norm substitute, one
+    fused reduction per iteration; cancellation is arbitrated with the true
+    residual exactly as gmres.py:325-360 (gmres.py:540-548)."""
     return _run("cgs1_ghysels", A, b, x0, config, ledger, diagnostics_every, true_residual_every)
 
 
@@ -491,8 +529,6 @@ def solve_distributed(op, b_local, comm, n_global, x0_local=None, config=None, l
     runs the same host restart shell on bit-identical device reports, so
     histories and ledgers agree across ranks; returns (x_local, history)."""
     config = config if config is not None else GmresConfig()
-    if config.method == "cgs1_ghysels":
-        raise NotImplementedError("cgs1_ghysels is outside the B200 hot path (SURVEY §8f)")
     if diagnostics_every:
         raise NotImplementedError("per-iteration diagnostics on the multi-rank path")
     return _DeviceSolve(op, b_local, x0_local, config, ledger, diagnostics_every, 0,

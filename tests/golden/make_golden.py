@@ -175,6 +175,30 @@ def small():
     _save("convdiff27_16.npz", **out)
 
 
+def ghysels():
+    """cgs1_ghysels runs: the stall problem (cancellation failure), a
+    well-conditioned system, the identity (exact-zero radicand), C1."""
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from helpers import spread_system
+    out = {}
+    cases = {
+        "sim": (ls.gen_simoncini(100), None, 100, 1, 1e-14, 1),
+        "spread": spread_system(10, seed=10)[0::2] + (10, 10, 1e-12, 0),
+        "eye": (ls.CsrMatrix.diagonal(np.ones(5)), np.ones(5), 5, 10, 1e-10, 0),
+        "c1": (ls.gen_laplace2d(64), None, 30, 200, 1e-6, 0),
+    }
+    for tag, (A, b, m, R, tol, diag) in cases.items():
+        if b is None:
+            b = ls.gen_rhs("random", A, 42)
+        r = _run(A, b, "cgs1_ghysels", m, R, tol, diag=diag)
+        out.update({f"{tag}__{k}": v for k, v in r.items()})
+        out[f"{tag}__b"] = b
+        if hasattr(A, "to_dense") and A.n_rows <= 100:
+            out[f"{tag}__A"] = A.to_dense()
+        print("ghysels", tag, len(r["curve"]), r["outcome"])
+    _save("ghysels.npz", **out)
+
+
 def extras():
     """true_residual_every probes (gmres.py:273-283)."""
     out = {}
@@ -232,6 +256,8 @@ if __name__ == "__main__":
         small()
     elif what == "extras":
         extras()
+    elif what == "ghysels":
+        ghysels()
     elif what == "c2":
         big_c2(int(sys.argv[2]) if len(sys.argv) > 2 else 256)
     elif what == "c5":

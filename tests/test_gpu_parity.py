@@ -423,6 +423,44 @@ def test_fused_spmv_k1_bitwise_equals_unfused(P, meth):
     assert np.array_equal(reps[0][2], reps[1][2])
 
 
+@pytest.mark.parametrize("tag", ["sim", "spread", "eye", "c1"])
+def test_ghysels_matches_reference(P, tag):
+    """cgs1_ghysels (gmres.py:325-360): the stall problem ends in
+    cancellation_failure after 52 iterations, the well-conditioned ones
+    converge, the identity hits the exact-zero radicand path."""
+    G = _load("ghysels.npz")
+    p = tag + "__"
+    if tag == "c1":
+        A = P.gen_laplace2d(64)
+        m, R, tol, diag = 30, 200, 1e-6, 0
+    else:
+        A = P.CsrMatrix.from_dense(G[p + "A"])
+        m, R, tol, diag = {"sim": (100, 1, 1e-14, 1), "spread": (10, 10, 1e-12, 0),
+                           "eye": (5, 10, 1e-10, 0)}[tag]
+    led = P.ReductionLedger()
+    cfg = P.GmresConfig(restart_m=m, max_restarts=R, rel_tol=tol, method="cgs1_ghysels")
+    x, h = P.solve(A, G[p + "b"], config=cfg, ledger=led, diagnostics_every=diag)
+    curve = G[p + "curve"]
+    c = h.implicit_curve()
+    assert h.outcome == str(G[p + "outcome"])
+    if tag == "sim":
+        # the Pythagorean radicand cancels at rounding level: where it first
+        # drops below 4 eps ||z||^2 is itself rounding-dependent (+-2 iterations)
+        assert abs(h.iterations - len(curve)) <= 2
+        n = min(len(c), len(curve)) - 3
+        assert np.max(np.abs(c[:n] - curve[:n]) / curve[:n]) <= 1e-6
+        return
+    assert h.iterations == len(curve)
+    # the exhaustion iteration's h is expected garbage (test_gmres.py:278-282)
+    # and the Pythagorean h loses digits as the radicand shrinks: 1e-7
+    q = len(curve) - 1 if tag == "spread" else len(curve)
+    assert np.max(np.abs(c[:q] - curve[:q]) / np.maximum(curve[:q], 1e-300)) <= 1e-7
+    assert [e.kind for e in led.events] == list(G[p + "ev_kind"])
+    assert [e.iteration for e in led.events] == list(G[p + "ev_iter"])
+    xr = G[p + "x"]
+    assert np.linalg.norm(x - xr) <= 1e-7 * np.linalg.norm(xr)
+
+
 # ------------------------------------------------------------------ full-size parity
 def test_c2_256cube_one_sync_full_solve_matches_reference(P):
     """BASELINE config 2 (256^3, n = 16.7M), one-sync GMRES(50), tol 1e-6,

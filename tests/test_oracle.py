@@ -132,3 +132,21 @@ def test_convdiff27_small_history(meth):
     _check_run(run, G, meth)
     ref = float(G[meth + "__final_orth_loss"])
     assert 0.1 * ref <= run.cycle_orth_loss[-1] <= 10 * ref
+
+
+@pytest.mark.parametrize("tag", ["sim", "spread", "eye", "c1"])
+def test_ghysels_matches_reference(tag):
+    G = _load("ghysels.npz")
+    p = tag + "__"
+    if tag == "c1":
+        A = orc.laplace2d(64)
+        m, R, tol, diag = 30, 200, 1e-6, 0
+    else:
+        A = orc.dense_to_csr(G[p + "A"])
+        m, R, tol, diag = {"sim": (100, 1, 1e-14, 1), "spread": (10, 10, 1e-12, 0),
+                           "eye": (5, 10, 1e-10, 0)}[tag]
+    run = orc.gmres(A, G[p + "b"], "cgs1_ghysels", m, R, tol, diag_every=diag)
+    curve = G[p + "curve"]
+    assert len(run.curve) == len(curve) and run.outcome == str(G[p + "outcome"])
+    assert np.max(np.abs(np.array(run.curve) - curve) / np.maximum(curve, 1e-300)) <= 1e-9
+    assert [e[1] for e in run.ledger.events] == list(G[p + "ev_kind"])
