@@ -297,7 +297,7 @@ def run_gpu(args):
                      "ortho_GBps": ortho_b / (ortho_t / 1e3) / 1e9,
                      "ortho_frac": ortho_b / (ortho_t / 1e3) / 1e9 / peak},
         "kernels": kern,
-        "gpu_launches": sum(v[1] for v in agg.values()),
+        "gpu_launches": eng.launches_per_cycle * args.steps,   # every liblsb200 launch timed
         "clocks": clk.summary(),
     }
     del eng
