@@ -133,6 +133,13 @@ typedef struct lsb_arnoldi {
   lsb_workspace ws;
 } lsb_arnoldi;
 
+/* ---------------------------------------------------------------- tuning */
+#define LSB_TUNE_FUSED_OCC3 1   /* fused K1+SpMV: 3 CTAs/SM, <= 8 items/warp  */
+#define LSB_TUNE_COUNT 8
+/* Set / read a kernel-variant knob (performance only; results unchanged up
+ * to the reduction tree of the affected kernel). Returns the old value. */
+int lsb_set_tuning(int32_t key, int32_t value);
+
 /* ---------------------------------------------------------------- info */
 const char* lsb_version(void);
 const char* lsb_last_error(void);

@@ -76,6 +76,7 @@ _I64 = C.c_int64
 
 _SIGS = {
     "lsb_version": ([], C.c_char_p),
+    "lsb_set_tuning": ([_I32, _I32], C.c_int),
     "lsb_last_error": ([], C.c_char_p),
     "lsb_sm_count": ([], C.c_int),
     "lsb_partial_len": ([_I32], _I64),

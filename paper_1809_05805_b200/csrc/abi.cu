@@ -8,6 +8,9 @@ namespace lsb {
 
 static thread_local char g_err[512] = "";
 static int g_sms = 0;
+static int g_tune[LSB_TUNE_COUNT] = {0};
+
+int tuning(int key) { return (key >= 0 && key < LSB_TUNE_COUNT) ? g_tune[key] : 0; }
 
 int sm_count() {
   if (!g_sms) {
@@ -74,6 +77,13 @@ using namespace lsb;
 extern "C" {
 
 const char* lsb_version(void) { return "lsb200 0.1 sm_100a"; }
+
+int lsb_set_tuning(int32_t key, int32_t value) {
+  if (key < 0 || key >= LSB_TUNE_COUNT) return -1;
+  const int old = g_tune[key];
+  g_tune[key] = value;
+  return old;
+}
 const char* lsb_last_error(void) { return g_err; }
 int lsb_sm_count(void) { return sm_count(); }
 int32_t lsb_max_columns(void) { return 128; }

@@ -37,8 +37,8 @@ __device__ __forceinline__ void stage_rows(double* dst, const double* u, int64_t
   }
 }
 
-template <int R, int SLOTS>
-__global__ void __launch_bounds__(kThreads, 2)
+template <int R, int SLOTS, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
 mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
                   double* __restrict__ wout, const Stencil7 K, double* __restrict__ out,
                   double* __restrict__ partial, unsigned* counter, lsb_flags* flags, int it) {
@@ -85,6 +85,7 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
     const double* zt = smem + buf * stage + span;
     const double* pt = zt + kTile;
     // ---- w = A u for the tile rows (row pairs; nx even keeps pairs in a line)
+#pragma unroll 2
     for (int j = threadIdx.x; j < kTile / 2; j += kThreads) {
       const int lr = 2 * j;
       const int64_t r = r0 + lr;
@@ -202,16 +203,24 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
   if (threadIdx.x == 0) *counter = 0u;
 }
 
+// 3 CTAs/SM (<= 8 items per warp) wins up to p ~ 40 (tools/kbench.py:
+// p=26 627 vs 679 us); above, the 2-CTA 16-item deal balances better.
+// Knob LSB_TUNE_FUSED_OCC3: 0 auto, 1 always, 2 never.
+static bool occ3(int p) {
+  const int k = tuning(LSB_TUNE_FUSED_OCC3);
+  return k == 1 || (k == 0 && p <= 40);
+}
+
 static size_t smem_bytes(int nx) { return sizeof(double) * (2 * (kTile + 2 * nx + 2 * kTile) + kTile); }
 
-template <int R, int SLOTS>
+template <int R, int SLOTS, int MINB>
 static int launch_t(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cudaStream_t st) {
   static int occ_nx = -1, occ = 0;
+  auto kern = mdot_spmv7_kernel<R, SLOTS, MINB>;
   const size_t sm = smem_bytes(K.nx);
   if (occ_nx != K.nx) {
-    cudaFuncSetAttribute(mdot_spmv7_kernel<R, SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mdot_spmv7_kernel<R, SLOTS>, kThreads, sm);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, sm);
     if (occ < 1) occ = 1;
     occ_nx = K.nx;
   }
@@ -220,21 +229,26 @@ static int launch_t(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cuda
   if (S.ws.grid > 0 && S.ws.grid < grid) grid = S.ws.grid;
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
-  mdot_spmv7_kernel<R, SLOTS><<<(unsigned)grid, kThreads, sm, st>>>(
-      S.V, S.ld, S.n, p, S.V + (int64_t)p * S.ld, K, S.Gloc, S.ws.partial, S.ws.counter,
-      S.flags, it);
+  kern<<<(unsigned)grid, kThreads, sm, st>>>(S.V, S.ld, S.n, p, S.V + (int64_t)p * S.ld, K,
+                                            S.Gloc, S.ws.partial, S.ws.counter, S.flags, it);
   return check_launch("mdot_spmv7");
 }
 
 template <int R>
 static int launch_r(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cudaStream_t st) {
   const int s = slots_for(p, R);
-  if (s <= 1) return launch_t<R, 1>(S, K, p, it, st);
-  if (s <= 2) return launch_t<R, 2>(S, K, p, it, st);
-  if (s <= 4) return launch_t<R, 4>(S, K, p, it, st);
-  if (s <= 8) return launch_t<R, 8>(S, K, p, it, st);
-  if (s <= 13) return launch_t<R, 13>(S, K, p, it, st);
-  return launch_t<R, 16>(S, K, p, it, st);
+  if (occ3(p)) {   // 3 CTAs/SM, at most 8 items per warp
+    if (s <= 1) return launch_t<R, 1, 3>(S, K, p, it, st);
+    if (s <= 2) return launch_t<R, 2, 3>(S, K, p, it, st);
+    if (s <= 4) return launch_t<R, 4, 3>(S, K, p, it, st);
+    return launch_t<R, 8, 3>(S, K, p, it, st);
+  }
+  if (s <= 1) return launch_t<R, 1, 2>(S, K, p, it, st);
+  if (s <= 2) return launch_t<R, 2, 2>(S, K, p, it, st);
+  if (s <= 4) return launch_t<R, 4, 2>(S, K, p, it, st);
+  if (s <= 8) return launch_t<R, 8, 2>(S, K, p, it, st);
+  if (s <= 13) return launch_t<R, 13, 2>(S, K, p, it, st);
+  return launch_t<R, 16, 2>(S, K, p, it, st);
 }
 
 int launch_lagged_reduce_spmv7(const lsb_arnoldi& S, const lsb_stencil* A, int it, int p,
@@ -252,7 +266,7 @@ int launch_lagged_reduce_spmv7(const lsb_arnoldi& S, const lsb_stencil* A, int i
   K.fy = FastDiv::make((uint32_t)A->ny);
   K.lo_valid = A->halo_lo ? -(int64_t)K.plane : 0;
   K.hi_valid = S.n + (A->halo_hi ? K.plane : 0);
-  switch (choose_parts(p)) {
+  switch (occ3(p) ? choose_parts(p, 8) : choose_parts(p)) {
     case 8: return launch_r<8>(S, K, p, it, st);
     case 4: return launch_r<4>(S, K, p, it, st);
     case 2: return launch_r<2>(S, K, p, it, st);

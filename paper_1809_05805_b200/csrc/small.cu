@@ -101,7 +101,7 @@ __device__ bool lagged_front(const lsb_arnoldi& S, SmallShared& sh, int it, int 
 
 // ------------------------------------------------------------------ mgs_lvl2
 __global__ void __launch_bounds__(kSmall)
-mgs_lvl2_small_kernel(lsb_arnoldi S, int it, int p, int ks, int gc) {
+mgs_lvl2_small_kernel(lsb_arnoldi S, int it, int p, int ks, int gc, bool use_smem) {
   if (gated_off(S.flags, it)) return;
   __shared__ SmallShared sh;
   const int t = threadIdx.x, cap = S.cap;
@@ -111,21 +111,46 @@ mgs_lvl2_small_kernel(lsb_arnoldi S, int it, int p, int ks, int gc) {
     return;
   }
   const double beta = sh.beta;
+  // T block in shared memory when it fits (p x p, row stride p): the two
+  // triangular mat-vecs then run at smem latency (launch sets the size)
+  extern __shared__ double sT[];
+  const bool st = use_smem;
+  if (st) {
+    for (int e = t; e < (p - 1) * (p - 1); e += blockDim.x) {
+      const int j = e / (p - 1), l = e - j * (p - 1);
+      sT[j * p + l] = S.T[(int64_t)j * cap + l];
+    }
+  }
   // T[:p-1, p-1] = -(T[:p-1, :p-1] @ (G[:p-1, 0] / beta));  T[p-1, p-1] = 1
   for (int e = t; e < p - 1; e += blockDim.x) sh.a[e] = __ddiv_rn(sh.a[e], beta);
   if (t == 0) sh.y[p - 1] = __ddiv_rn(sh.y[p - 1], beta);
   __syncthreads();
   for (int j = t; j < p - 1; j += blockDim.x) {
     double acc = 0.0;
-    for (int l = j; l < p - 1; ++l) acc = fma(S.T[(int64_t)j * cap + l], sh.a[l], acc);
+    if (st) {
+      for (int l = j; l < p - 1; ++l) acc = fma(sT[j * p + l], sh.a[l], acc);
+      sT[j * p + (p - 1)] = -acc;
+    } else {
+      for (int l = j; l < p - 1; ++l) acc = fma(S.T[(int64_t)j * cap + l], sh.a[l], acc);
+    }
     S.T[(int64_t)j * cap + (p - 1)] = -acc;
   }
-  if (t == 0) S.T[(int64_t)(p - 1) * cap + (p - 1)] = 1.0;
+  if (t == 0) {
+    S.T[(int64_t)(p - 1) * cap + (p - 1)] = 1.0;
+    if (st) {
+      sT[(p - 1) * p + (p - 1)] = 1.0;
+      for (int l = 0; l < p - 1; ++l) sT[(p - 1) * p + l] = 0.0;
+    }
+  }
   __syncthreads();
-  // c = T[:p,:p]^T y  (/beta);  R[:p, p] = c  (coalesced column reads)
+  // c = T[:p,:p]^T y  (/beta);  R[:p, p] = c
   for (int j = t; j < p; j += blockDim.x) {
     double acc = 0.0;
-    for (int l = 0; l <= j; ++l) acc = fma(S.T[(int64_t)l * cap + j], sh.y[l], acc);
+    if (st) {
+      for (int l = 0; l <= j; ++l) acc = fma(sT[l * p + j], sh.y[l], acc);
+    } else {
+      for (int l = 0; l <= j; ++l) acc = fma(S.T[(int64_t)l * cap + j], sh.y[l], acc);
+    }
     if (ks) acc = __ddiv_rn(acc, beta);
     S.coef[j] = acc;
     S.R[(int64_t)j * cap + p] = acc;
@@ -356,7 +381,16 @@ __global__ void restart_check_kernel(lsb_arnoldi S, int first) {
 // ------------------------------------------------------------------ launchers
 int launch_mgs_lvl2_small(const lsb_arnoldi& S, int it, int p, int ks, int gc, cudaStream_t st) {
   if (p < 1 || S.cap > kSmall || p >= S.cap) return LSB_ERANGE;
-  mgs_lvl2_small_kernel<<<1, kSmall, 0, st>>>(S, it, p, ks, gc);
+  constexpr size_t kMaxT = 160 * 1024;   // T block staged in smem up to p = 143
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(mgs_lvl2_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kMaxT);
+    attr = true;
+  }
+  const size_t need = sizeof(double) * (size_t)p * p;
+  const bool use = need <= kMaxT;
+  mgs_lvl2_small_kernel<<<1, kSmall, use ? need : 0, st>>>(S, it, p, ks, gc, use);
   return check_launch("mgs_lvl2_small");
 }
 int launch_cgs2_small_a(const lsb_arnoldi& S, int it, int p, int ks, int gc, cudaStream_t st) {

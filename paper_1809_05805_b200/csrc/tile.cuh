@@ -6,6 +6,9 @@ namespace lsb {
 
 constexpr int kTile = 1024;  // rows per K1 tile
 
+// runtime tuning knobs (lsb_set_tuning); defaults are the measured best
+int tuning(int key);
+
 // 128-bit streaming load that does not allocate in L1 (basis columns are
 // read exactly once per pass).
 __device__ __forceinline__ double2 ld_stream(const double* p) {
@@ -77,12 +80,12 @@ inline bool canonical7(const lsb_stencil* S) {
 // Choose R in {1,2,4,8} row parts per tile column so the p*R (column,
 // part) items deal evenly over 8 warps with at most 16 items per warp.
 inline int slots_for(int p, int R) { return (p * R + kWarps - 1) / kWarps; }
-inline int choose_parts(int p) {
+inline int choose_parts(int p, int max_slots = 16) {
   int best = 1;
   double best_eff = 0.0;
   for (int R = 1; R <= 8; R *= 2) {
     const int s = slots_for(p, R);
-    if (s > 16) break;
+    if (s > max_slots) break;
     const double eff = (double)(p * R) / (double)(s * kWarps);
     if (eff > best_eff + 1e-9) { best_eff = eff; best = R; }
   }

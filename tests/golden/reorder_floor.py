@@ -54,10 +54,10 @@ def dot(x, y, led):
     return float(_blocked_T(x[:, None], y)[0])
 
 
-def main():
+def main(N=64):
     orc.mdot_pair, orc.mass_ip, orc.dot = mdot_pair, mass_ip, dot
-    G = np.load(os.path.join(HERE, "convdiff27_64.npz"))
-    A = orc.convdiff27(64)
+    G = np.load(os.path.join(HERE, f"convdiff27_{N}.npz"))
+    A = orc.convdiff27(N)
     b = orc.rhs_random(A.n_rows, 42)
     out = {}
     for meth in ("one_sync_mgs", "two_sync_cgs2", "mgs_l1"):
@@ -66,13 +66,15 @@ def main():
         n = min(len(c), len(cr))
         out[meth] = float(np.max(np.abs(c[:n] - cr[:n]) / cr[:n]))
         print(meth, len(c), len(cr), out[meth], flush=True)
-    with open(os.path.join(HERE, "reorder_floor.json"), "w") as fh:
-        json.dump({"_what": "max relative per-iteration deviation of the reference algorithm's "
-                            "own implicit-residual curve when only the summation order of its "
-                            "reductions changes (148 row blocks), vs the golden run; "
-                            "tests/golden/reorder_floor.py",
-                   "convdiff27_64": out}, fh, indent=1)
+    path = os.path.join(HERE, "reorder_floor.json")
+    data = json.load(open(path)) if os.path.exists(path) else {}
+    data["_what"] = ("max relative per-iteration deviation of the reference algorithm's own "
+                     "implicit-residual curve when only the summation order of its reductions "
+                     "changes (148 row blocks), vs the golden run; tests/golden/reorder_floor.py")
+    data[f"convdiff27_{N}"] = out
+    with open(path, "w") as fh:
+        json.dump(data, fh, indent=1)
 
 
 if __name__ == "__main__":
-    main()
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 64)
