@@ -507,6 +507,29 @@ def test_c5_convdiff27_64_history_and_orthogonality(P, meth, form):
     assert ours <= 10 * ref + 100 * EPS
 
 
+@pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2", "mgs_l1"])
+def test_c5_convdiff27_128_csr(P, meth):
+    """BASELINE config 5 at the survey's parity size N = 128 (n = 2,097,152,
+    nnz = 55,742,968) in CSR form, GMRES(100), tol 1e-10: 409 iterations in
+    the reference; ||I - V^T V|| of the final basis within 10x."""
+    import json
+    G = _load("convdiff27_128.npz")
+    O = orc.convdiff27(128)
+    A = P.CsrMatrix(O.n_rows, O.n_cols, O.row_ptr, O.col_idx, O.values)
+    del O
+    b = P.gen_rhs("random", A, 42)
+    x, h, led = _solve(P, A, b, meth, 100, 30, 1e-10)
+    with open(os.path.join(GOLD, "reorder_floor.json")) as fh:
+        floor = json.load(fh)["convdiff27_128"].get(meth, 0.0)
+    _check(h, led, G, meth, tol=max(1e-10, 4 * floor))
+    eng = h._stash[0]
+    V = eng.Vstore[: h.k + 1, : eng.n]
+    gram = (V @ V.T).cpu().numpy()
+    ours = orc.spectral_norm_small(np.eye(h.k + 1) - gram)
+    ref = float(G[meth + "__final_orth_loss"])
+    assert ours <= 10 * ref + 100 * EPS
+
+
 # ------------------------------------------------------------------ full-size parity
 def test_c2_256cube_one_sync_full_solve_matches_reference(P):
     """BASELINE config 2 (256^3, n = 16.7M), one-sync GMRES(50), tol 1e-6,
