@@ -48,10 +48,10 @@ def _peaks():
         return 6650.0, "fallback"
 
 
-def _dims(n_gpus):
-    """Global grid for N GPUs: 256^3 per GPU, doubling x, y, z in turn
-    (N=8 -> 512^3 = config 4); slabs along z."""
-    nx = ny = nz = N_SLAB
+def _dims(n_gpus, slab=N_SLAB):
+    """Global grid for N GPUs: slab^3 (256^3) per GPU, doubling x, y, z in
+    turn (N=8 -> 512^3 = config 4); slabs along z."""
+    nx = ny = nz = slab
     k = 0
     g = n_gpus
     while g > 1:
@@ -73,12 +73,15 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, enabled=True):
         self.index = index
+        self.enabled = enabled
         self.proc = None
         self.lines = []
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -189,6 +192,32 @@ def _ortho_bytes(n, p, kind):
 
 
 def run_gpu(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if args.emulate_ranks > 1:
+        # P ranks as threads on this one GPU (parallel.ThreadComm): exercises
+        # the multi-rank path end to end; the number is NOT a scaling result
+        from paper_1809_05805_b200.parallel import run_threads
+        out = run_threads(args.emulate_ranks,
+                          lambda c: _bench_core(args, c, args.emulate_ranks, c.rank, local))
+        print(json.dumps(dict(out[0], emulated_ranks_on_one_gpu=args.emulate_ranks)), flush=True)
+        return
+    comm = None
+    if world > 1:
+        from paper_1809_05805_b200.parallel import Comm
+        comm = Comm.init()
+    result = _bench_core(args, comm, world, rank, local)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if comm is not None:
+        comm.close()
+
+
+def _bench_core(args, comm, world, rank, local):
     import numpy as np
     import torch
 
@@ -196,26 +225,18 @@ def run_gpu(args):
     from paper_1809_05805_b200 import _abi
     from paper_1809_05805_b200.engine import Engine
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    comm = None
-    nx, ny, nz = _dims(world)
-    if world > 1:
-        from paper_1809_05805_b200.parallel import Comm, slab_problem
-        comm = Comm.init()
+    slab = args.slab
+    nx, ny, nz = _dims(world, slab)
+    if comm is not None:
+        from paper_1809_05805_b200.parallel import slab_problem
         A_local, n_global = slab_problem((nx, ny, nz), comm)
     else:
-        A_local = P.gen_laplace3d(N_SLAB)
+        A_local = P.gen_laplace3d(slab)
         n_global = A_local.n_rows
     n = A_local.n_rows
-    rng = np.random.default_rng(42)
-    b_full = None
-    if world == 1:
-        b_full = rng.standard_normal(n)
-        b_full /= np.linalg.norm(b_full)
-        b_local = b_full
+    if comm is None:
+        b_local = np.random.default_rng(42).standard_normal(n)
+        b_local /= np.linalg.norm(b_local)
     else:
         from paper_1809_05805_b200.parallel import local_rhs
         b_local = local_rhs((nx, ny, nz), comm, 42)
@@ -240,7 +261,7 @@ def run_gpu(args):
     if comm is not None:
         comm.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, enabled=(rank == 0)) as clk:
         ev0.record()
         for _ in range(args.steps):
             step()
@@ -289,7 +310,7 @@ def run_gpu(args):
                    "step": "one GMRES(50) restart cycle = 50 Arnoldi iterations",
                    "rel_tol": 1e-14, "l2": "inputs larger than L2 (basis 7.0 GB per GPU)",
                    "partition": "z-slabs" if world > 1 else "none",
-                   "value_units": "global Arnoldi iterations/s x N (per-GPU slab 256^3)"},
+                   "value_units": f"global Arnoldi iterations/s x N (per-GPU slab {slab}^3)"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
@@ -302,35 +323,42 @@ def run_gpu(args):
     }
     del eng
     torch.cuda.empty_cache()
-    # e2e through the public API with host buffers (N=1)
-    if world == 1:
-        A = P.gen_laplace3d(N_SLAB)
-        cfg = P.GmresConfig(restart_m=M, max_restarts=1, rel_tol=1e-14, method="one_sync_mgs")
-        for _ in range(1):
-            x, h = P.solve(A, b_full, config=cfg, diagnostics_every=0)
-            h.release()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e2e_steps = max(2, min(args.steps, 5))
-        for _ in range(e2e_steps):
-            x, h = P.solve(A, b_full, config=cfg, diagnostics_every=0)
-            assert h.iterations == M
-            h.release()
-        dt = time.perf_counter() - t0
-        result["e2e"] = {"value": M * e2e_steps / dt, "unit": UNIT,
-                         "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
-                         "steps": e2e_steps,
-                         "what": "solve(A, b_host) -> x_host, GmresConfig(50, 1 cycle)"}
-        if not args.no_cpu:
-            v, dt_cpu, thr = cpu_sample(args.cpu_iters)
-            result["cpu_baseline"] = {
-                "value": v, "unit": UNIT, "cores": thr, "kind": "port",
-                "sample": f"first {args.cpu_iters} Arnoldi iterations of the same 256^3 one-sync "
-                          f"GMRES(50) solve, numpy oracle port ({dt_cpu:.1f} s)"}
-    if rank == 0:
-        print(json.dumps(result), flush=True)
+    # e2e through the public API with host buffers: solve() on one GPU,
+    # solve_distributed() per rank (each rank uploads its b rows, downloads x)
+    cfg = P.GmresConfig(restart_m=M, max_restarts=1, rel_tol=1e-14, method="one_sync_mgs")
+    b_host = np.ascontiguousarray(b_local)
+
+    def e2e_once():
+        if comm is None:
+            x, h = P.solve(A_local, b_host, config=cfg, diagnostics_every=0)
+        else:
+            x, h = P.gmres.solve_distributed(A_local, b_host, comm, n_global, config=cfg)
+        assert h.iterations == M and isinstance(x, np.ndarray)
+        h.release()
+
+    e2e_once()
+    torch.cuda.synchronize()
     if comm is not None:
-        comm.close()
+        comm.barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(2, min(args.steps, 5))
+    for _ in range(e2e_steps):
+        e2e_once()
+    dt = time.perf_counter() - t0
+    if comm is not None:
+        dt = comm.max_scalar(dt)
+    result["e2e"] = {"value": M * e2e_steps / dt * world, "unit": UNIT,
+                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                     "steps": e2e_steps,
+                     "what": "solve(A, b_host) -> x_host (per rank: solve_distributed), "
+                             "GmresConfig(50, 1 cycle); bytes per rank"}
+    if world == 1 and not args.no_cpu and rank == 0:
+        v, dt_cpu, thr = cpu_sample(args.cpu_iters)
+        result["cpu_baseline"] = {
+            "value": v, "unit": UNIT, "cores": thr, "kind": "port",
+            "sample": f"first {args.cpu_iters} Arnoldi iterations of the same 256^3 one-sync "
+                      f"GMRES(50) solve, numpy oracle port ({dt_cpu:.1f} s)"}
+    return result
 
 
 def main():
@@ -341,6 +369,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=8)
+    ap.add_argument("--slab", type=int, default=N_SLAB, help="per-GPU cube edge (256 = config 2)")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="run the multi-rank path as K threads on one GPU (validation only)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -7,6 +7,7 @@ graphs; every arithmetic operation on the hot path is a liblsb200 kernel.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 
 import numpy as np
 import torch
@@ -102,14 +103,14 @@ def out_like(t, like_host):
 # buffer: pageable cudaMemcpy of a 134 MB vector runs at ~2 GB/s on the
 # B200 host, pinned DMA at ~50 GB/s plus a ~40 GB/s host memcpy.
 _STAGE_MIN = 1 << 16
-_stage = None
+_stage = threading.local()   # one staging buffer per host thread (in-process ranks)
 
 
 def _staging(n):
-    global _stage
-    if _stage is None or _stage.numel() < n:
-        _stage = torch.empty(max(n, 1 << 20), dtype=F64).pin_memory()
-    return _stage[:n]
+    buf = getattr(_stage, "buf", None)
+    if buf is None or buf.numel() < n:
+        buf = _stage.buf = torch.empty(max(n, 1 << 20), dtype=F64).pin_memory()
+    return buf[:n]
 
 
 def h2d(a, dev):

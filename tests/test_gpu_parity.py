@@ -561,3 +561,29 @@ def test_c2_scale_one_cycle_properties(P):
     assert np.abs(Gm - np.eye(51)).max() <= 1e-12
     # all variants reach the same residual after one cycle (2.670e-03)
     assert abs(h.implicit_curve()[-1] - 2.670e-3) <= 1e-5
+
+
+def test_c4_512cube_single_gpu_cycle(P):
+    """Config 4's global problem (512^3, n = 134,217,728; basis 56 GB) on ONE
+    B200: maximum-size run of the fused path (nx = 512 halo tiles, 64-bit
+    row offsets).  Size-independent properties: the Arnoldi basis stays
+    orthonormal, every rank of the reduction is finite, and the implicit
+    residual equals ||b - A x|| after the cycle's extract."""
+    A = P.gen_laplace3d(512)
+    n = A.n_rows
+    b = torch.randn(n, dtype=torch.float64, device="cuda",
+                    generator=torch.Generator(device="cuda").manual_seed(42))
+    b /= torch.linalg.vector_norm(b)
+    cfg = P.GmresConfig(restart_m=50, max_restarts=1, rel_tol=1e-14)
+    x, h = P.solve(A, b, config=cfg, diagnostics_every=0)
+    assert h.iterations == 50 and h.outcome == "stalled_maxiter"
+    eng = h._stash[0]
+    assert eng.fused7
+    V = eng.Vstore[:51, :n]
+    gram = torch.empty((51, 51), dtype=torch.float64, device="cuda")
+    for j in range(51):                       # chunked Gram to bound temporaries
+        gram[j] = V @ V[j]
+    assert float((gram - torch.eye(51, device="cuda", dtype=torch.float64)).abs().max()) <= 1e-12
+    # restart residual of the final verification == the implicit one to O(eps kappa)
+    assert abs(h.final_true_rel_res - h.implicit_curve()[-1]) <= 1e-6 * h.implicit_curve()[-1]
+    h.release()
