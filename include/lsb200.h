@@ -205,9 +205,14 @@ int lsb_lagged_reduce_spmv7(const lsb_arnoldi* S, const lsb_stencil* A, int32_t 
 /* Small-state update of the one-reduce MGS-CWY kernel: beta, breakdown test,
  * R/T columns, c = T^T y (/beta).  givens_col > 0 also folds Hessenberg
  * column givens_col-1 = R[0..givens_col, givens_col] into the Givens state
- * and tests convergence (gmres.py:418-435). */
+ * and tests convergence (gmres.py:418-435); givens_col < 0 defers that fold
+ * to lsb_settle (pipeline2 schedule, gmres.py:444-462). */
 int lsb_mgs_lvl2_small(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
                        int32_t givens_col, void* stream);
+/* Deferred Givens fold + convergence test of Hessenberg column col-1
+ * (settle, gmres.py:427-435), for a small-state call made with
+ * givens_col = -col; runs on a side stream in the pipeline2 schedule. */
+int lsb_settle(const lsb_arnoldi* S, int32_t it, int32_t col, void* stream);
 /* cgs2_lvl2 front: beta, breakdown, L row, r = (I - L - L^T) y (/beta). */
 int lsb_cgs2_lvl2_small_a(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
                           int32_t givens_col, void* stream);

@@ -101,6 +101,7 @@ _SIGS = {
     "lsb_direct_small": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_direct_normalize": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_ghysels_small": ([_P, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_settle": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_cycle_begin": ([_P, _P], C.c_int),
     "lsb_cycle_lsq": ([_P, _P], C.c_int),
     "lsb_cycle_extract": ([_P, _P, _P, _P], C.c_int),

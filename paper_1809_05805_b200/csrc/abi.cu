@@ -63,6 +63,7 @@ int launch_givens_update(double*, double*, double*, int, const double*, int, dou
 int launch_lagged_reduce_spmv7(const lsb_arnoldi&, const lsb_stencil*, int, int, cudaStream_t);
 int launch_trial_lsq(const lsb_arnoldi&, int, double*, cudaStream_t);
 int launch_ghysels_small(const lsb_arnoldi&, int, int, int, cudaStream_t);
+int launch_settle(const lsb_arnoldi&, int, int, cudaStream_t);
 int launch_trial_combine(const lsb_arnoldi&, int, const double*, const double*, double*,
                          const double*, cudaStream_t);
 int launch_back_substitute(const double*, const double*, int, int, double*, int*, cudaStream_t);
@@ -217,6 +218,11 @@ int lsb_direct_small(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, v
   if (int rc = check_arnoldi(S)) return rc;
   const int gc = S->m > 0 ? col : 0;
   return launch_direct_small(*S, it, col, p, gc, S_(stream));
+}
+
+int lsb_settle(const lsb_arnoldi* S, int32_t it, int32_t col, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_settle(*S, it, col, S_(stream));
 }
 
 int lsb_ghysels_small(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, void* stream) {

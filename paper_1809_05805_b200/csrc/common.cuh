@@ -23,7 +23,12 @@ constexpr int kNoStop = 0x7fffffff;
 // kernel of an iteration > d returns immediately.  That keeps a whole
 // restart cycle launchable as one CUDA graph with zero host syncs.
 __device__ __forceinline__ bool gated_off(const lsb_flags* f, int it) {
-  return f != nullptr && it >= 0 && *((volatile const int*)&f->stop_iter) < it;
+  if (f == nullptr || it < 0) return false;
+  const int stop = *((volatile const int*)&f->stop_iter);
+  const int broke = *((volatile const int*)&f->broke_iter);
+  // an earlier breakdown also stops later iterations (with a deferred
+  // Givens fold the stop flag itself may land one iteration late)
+  return stop < it || (broke >= 0 && broke < it);
 }
 
 // ---------------------------------------------------------------- warp sums

@@ -158,6 +158,28 @@ mgs_lvl2_small_kernel(lsb_arnoldi S, int it, int p, int ks, int gc, bool use_sme
   if (gc > 0) settle_block(S, sh, it, gc, false);
 }
 
+// Deferred settle (pipeline2, gmres.py:444-462): the Givens fold of
+// Hessenberg column gc-1 = R[0..gc, gc] run apart from the small-state
+// kernel (which was launched with givens_col = -gc), on a side stream, so it
+// overlaps the next iteration's basis passes.
+__global__ void __launch_bounds__(kSmall)
+settle_kernel(lsb_arnoldi S, int it, int gc) {
+  if (gated_off(S.flags, it)) return;
+  __shared__ SmallShared sh;
+  const int cap = S.cap;
+  for (int j = threadIdx.x; j <= gc; j += blockDim.x) sh.col[j] = S.R[(int64_t)j * cap + gc];
+  __syncthreads();
+  const bool broke = S.flags->broke_iter == it;
+  if (broke && threadIdx.x == 0) sh.col[gc] = 0.0;
+  settle_block(S, sh, it, gc, broke);
+}
+
+int launch_settle(const lsb_arnoldi& S, int it, int gc, cudaStream_t st) {
+  if (gc < 1 || gc > S.m) return LSB_ERANGE;
+  settle_kernel<<<1, kSmall, 0, st>>>(S, it, gc);
+  return check_launch("settle");
+}
+
 // ------------------------------------------------------------------ cgs2_lvl2
 __global__ void __launch_bounds__(kSmall)
 cgs2_small_a_kernel(lsb_arnoldi S, int it, int p, int ks, int gc) {

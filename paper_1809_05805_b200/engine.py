@@ -268,8 +268,23 @@ class Engine:
     def _lagged_body(self, st):
         S, m = self.Sref, self.m
         two = self.method == "two_sync_cgs2"
+        # pipeline2 (gmres.py:444-462) as real overlap: the Givens fold of
+        # column i-1 runs on a side stream while iteration i+1's basis passes
+        # proceed; iteration i+2 waits for it (depth-2 schedule).  Arithmetic
+        # identical to one_sync_mgs (tests: bitwise-equal histories).
+        defer = self.method == "pipeline2" and not self.true_residual
+        main = torch.cuda.current_stream()
+        if defer:
+            if not hasattr(self, "_side") or self._side.device != main.device:
+                self._side = torch.cuda.Stream()
+                self._ev_front = [torch.cuda.Event() for _ in range(m + 1)]
+                self._ev_settled = [torch.cuda.Event() for _ in range(m + 1)]
+            side = self._side
+            side_ptr = C.c_void_p(side.cuda_stream)
         for i in range(0, m + 1):
             p = i + 1
+            if defer and i >= 3:
+                main.wait_event(self._ev_settled[i - 2])
             if self.fused7:                                  # w = A u and [Q^T u, Q^T w], one pass
                 if self.comm is not None and self.halo:
                     self.comm.halo(self.Vstore[i], self.off, self.n, self.halo)
@@ -278,7 +293,14 @@ class Engine:
                 self._op_col(i, i + 1, i)                    # V.push(A v_i)
                 self._call("lsb_lagged_reduce", S, i, p, st)  # one pass: [Q^T u, Q^T w]
             self._gather(2 * p)
-            if not two:
+            if not two and defer and i >= 1:
+                self._call("lsb_mgs_lvl2_small", S, i, p, 1, -i, st)
+                self._ev_front[i].record(main)
+                side.wait_event(self._ev_front[i])
+                self._call("lsb_settle", S, i, i, side_ptr)
+                self._ev_settled[i].record(side)
+                self._call("lsb_lagged_update", S, i, p, 1, st)
+            elif not two:
                 self._call("lsb_mgs_lvl2_small", S, i, p, 1, i, st)
                 self._call("lsb_lagged_update", S, i, p, 1, st)
             else:
@@ -293,6 +315,10 @@ class Engine:
                 self._call("lsb_gram_row", S, i, i, i + 1, D.ptr(self.gram), self.cap, st)
             if self.true_residual and i >= 1:
                 self._trial(i, st)
+        if defer:   # join: the least squares needs every fold
+            main.wait_event(self._ev_settled[m])
+            if m >= 2:
+                main.wait_event(self._ev_settled[m - 1])
 
     def _trial(self, i, st):
         """||b - A (x + Mi V_i y_i)|| of iteration i into true_res[i]
