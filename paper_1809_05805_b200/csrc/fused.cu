@@ -22,21 +22,6 @@ struct Stencil7 {
   int64_t lo_valid, hi_valid;  // u rows that exist in memory (ghost planes included)
 };
 
-// stage rows [a, a + len) of u into dst (len even, a even); rows outside
-// [lo, hi) are zero-filled (never consumed: their presence flag is false)
-__device__ __forceinline__ void stage_rows(double* dst, const double* u, int64_t a, int len,
-                                           int64_t lo, int64_t hi) {
-  for (int j = threadIdx.x; j < len / 2; j += kThreads) {
-    const int64_t r = a + 2 * j;
-    if (r >= lo && r + 1 < hi) {
-      cp_async16(dst + 2 * j, u + r);
-    } else {
-      dst[2 * j] = (r >= lo && r < hi) ? u[r] : 0.0;
-      dst[2 * j + 1] = (r + 1 >= lo && r + 1 < hi) ? u[r + 1] : 0.0;
-    }
-  }
-}
-
 template <int R, int SLOTS, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
 mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
@@ -59,27 +44,40 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
   for (int s = 0; s < SLOTS; ++s) acc[s][0] = acc[s][1] = 0.0;
   bool bad = false;
 
+  // u tile + halo + z-neighbour tiles arrive by three TMA bulk copies issued
+  // by one thread, completion on a per-buffer mbarrier (double-buffered)
+  __shared__ __align__(8) uint64_t bars[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
   auto stage_all = [&](int b, int64_t t) {
     double* base = smem + b * stage;
     const int64_t r0 = t * kTile;
-    stage_rows(base, u, r0 - H, span, K.lo_valid, K.hi_valid);
-    stage_rows(base + span, u, r0 - K.plane, kTile, K.lo_valid, K.hi_valid);
-    stage_rows(base + span + kTile, u, r0 + K.plane, kTile, K.lo_valid, K.hi_valid);
+    unsigned tx = 0;
+    const bool leader = threadIdx.x == 0;
+    stage_bulk(base, u, r0 - H, span, K.lo_valid, K.hi_valid, &bars[b], leader, &tx);
+    stage_bulk(base + span, u, r0 - K.plane, kTile, K.lo_valid, K.hi_valid, &bars[b], leader, &tx);
+    stage_bulk(base + span + kTile, u, r0 + K.plane, kTile, K.lo_valid, K.hi_valid, &bars[b],
+               leader, &tx);
+    if (leader) mbar_arrive_tx(&bars[b], tx);
   };
 
   const int64_t ntiles = (n + kTile - 1) / kTile;
   int64_t t = blockIdx.x;
   int buf = 0;
+  unsigned phase = 0;
   if (t < ntiles) stage_all(0, t);
-  cp_async_commit();
   for (; t < ntiles; t += gridDim.x) {
-    // two barriers per tile: (A) tile t staged and every warp done with
+    // two barriers per tile: (A) tile t landed and every warp done with
     // tile t-1 (so buf^1 and sw are free), (B) w of tile t complete
-    cp_async_wait<0>();
+    mbar_wait(&bars[buf], (phase >> buf) & 1u);
+    phase ^= 1u << buf;
     __syncthreads();
     const int64_t tn = t + gridDim.x;
     if (tn < ntiles) stage_all(buf ^ 1, tn);
-    cp_async_commit();
     const int64_t r0 = t * kTile;
     const double* ut = smem + buf * stage + H;   // ut[lr] = u[r0 + lr], lr in [-H, kTile+H)
     const double* zt = smem + buf * stage + span;
@@ -168,7 +166,6 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
     }
     buf ^= 1;
   }
-  cp_async_wait<0>();
   if (bad && flags) flags->nonfinite = 1;
 
 #pragma unroll

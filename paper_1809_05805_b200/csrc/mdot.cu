@@ -40,19 +40,45 @@ mdot_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
 #pragma unroll
     for (int v = 0; v < NV; ++v) acc[s][v] = 0.0;
 
+  // u/w tiles arrive by TMA bulk copy (one elected thread), completion on a
+  // per-buffer mbarrier; double-buffered one tile ahead
+  __shared__ __align__(8) uint64_t bars[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t n_even = n & ~(int64_t)1;
+  auto stage = [&](int b, int64_t tt) {
+    unsigned tx = 0;
+    const bool leader = threadIdx.x == 0;
+    const int64_t a = tt * kTile;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double* dst = reinterpret_cast<double*>(sy[b][v]);
+      const double* src = v == 0 ? y0 : y1;
+      stage_bulk(dst, src, a, kTile, 0, n_even, &bars[b], leader, &tx);
+      if (n & 1 && n - 1 >= a && n - 1 < a + kTile && threadIdx.x == 0) {
+        dst[n - 1 - a] = src[n - 1];   // odd last row: plain store
+        fence_proxy_async();
+      }
+    }
+    if (leader) mbar_arrive_tx(&bars[b], tx);
+  };
   const int64_t ntiles = (n + kTile - 1) / kTile;
   int64_t t = blockIdx.x;
   int buf = 0;
-  if (t < ntiles) stage_tile<NV>(sy[0], y0, y1, n, t);
-  cp_async_commit();
+  unsigned phase = 0;   // bit b: parity of buffer b's next completion
+  if (t < ntiles) stage(0, t);
   for (; t < ntiles; t += gridDim.x) {
-    // one barrier per tile: tile t staged and every warp done with tile
+    // one barrier per tile: tile t landed and every warp is done with tile
     // t-1, so buf^1 can be refilled while tile t is swept
-    cp_async_wait<0>();
+    mbar_wait(&bars[buf], (phase >> buf) & 1u);
+    phase ^= 1u << buf;
     __syncthreads();
     const int64_t tn = t + gridDim.x;
-    if (tn < ntiles) stage_tile<NV>(sy[buf ^ 1], y0, y1, n, tn);
-    cp_async_commit();
+    if (tn < ntiles) stage(buf ^ 1, tn);
     const int64_t r0 = t * kTile;
     const bool full = r0 + kTile <= n;
     const int jbase = part * (kRows / 2);
@@ -96,7 +122,6 @@ mdot_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
     }
     buf ^= 1;
   }
-  cp_async_wait<0>();
 
   // CTA totals: butterfly per item, then the R parts of a column in order
 #pragma unroll

@@ -48,6 +48,69 @@ __device__ __forceinline__ void stage_tile(double2 (*buf)[kTile / 2], const doub
   }
 }
 
+// ---------------------------------------------------------------- TMA bulk copies
+// 1-D cp.async.bulk (UBLKCP) global -> shared, completion counted in bytes on
+// an mbarrier: one elected thread moves a whole tile, no per-thread copies.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Stage rows [a, a+len) of src into dst: the part inside [lo, hi) by one
+// bulk copy (issued by the calling elected thread, bytes added to *tx), the
+// rest zero-filled by all threads of the CTA (call with every thread; only
+// `leader` issues the copy).  a, len, lo, hi even (16-byte granules).
+__device__ __forceinline__ void stage_bulk(double* dst, const double* src, int64_t a, int len,
+                                          int64_t lo, int64_t hi, uint64_t* bar, bool leader,
+                                          unsigned* tx) {
+  const int64_t v0 = a > lo ? a : lo;
+  const int64_t v1 = (a + len) < hi ? (a + len) : hi;
+  if (v1 > v0) {
+    if (leader) {
+      bulk_g2s(dst + (v0 - a), src + v0, (unsigned)(8 * (v1 - v0)), bar);
+      *tx += (unsigned)(8 * (v1 - v0));
+    }
+  }
+  const int z0 = v1 > v0 ? (int)(v0 - a) : len;   // zero-fill [0, z0) and [z1, len)
+  const int z1 = v1 > v0 ? (int)(v1 - a) : len;
+  if (z0 > 0 || z1 < len) {
+    for (int j = threadIdx.x; j < z0; j += blockDim.x) dst[j] = 0.0;
+    for (int j = z1 + threadIdx.x; j < len; j += blockDim.x) dst[j] = 0.0;
+    fence_proxy_async();
+  }
+}
+
 // Unsigned 32-bit division by an invariant d (valid for n < 2^31).
 struct FastDiv {
   uint32_t d, m, s;
