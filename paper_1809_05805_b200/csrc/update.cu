@@ -9,6 +9,11 @@ namespace lsb {
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
 
+// Dynamic shared memory for a k-entry coefficient vector, padded: the
+// unrolled coefficient loops are vectorised into 128-bit LDS that may touch
+// sc[k] (unused) -- keep that inside the allocation (compute-sanitizer).
+static inline size_t coef_smem(int k) { return sizeof(double) * ((k > 0 ? k : 1) + 16); }
+
 static int row_grid(int64_t n, int per_sm = 8) {
   const int64_t pairs = (n + 1) / 2;
   int64_t g = (pairs + kThreads - 1) / kThreads;
@@ -54,7 +59,7 @@ int launch_maxpy(const double* y, const double* X, int64_t ld, int64_t n, int p,
                  const double* alpha, int sign, double* out, const lsb_flags* gate, int it,
                  cudaStream_t st) {
   if (n <= 0) return LSB_OK;
-  maxpy_kernel<<<row_grid(n), kThreads, sizeof(double) * (p > 0 ? p : 1), st>>>(
+  maxpy_kernel<<<row_grid(n), kThreads, coef_smem(p), st>>>(
       y, X, ld, n, p, alpha, sign < 0 ? -1.0 : 1.0, out, gate, it);
   return check_launch("maxpy");
 }
@@ -111,7 +116,7 @@ lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks) {
 
 int launch_lagged_update(const lsb_arnoldi& S, int it, int p, int ks, cudaStream_t st) {
   if (p < 1) return LSB_OK;
-  lagged_update_kernel<<<row_grid(S.n), kThreads, sizeof(double) * p, st>>>(S, it, p, ks);
+  lagged_update_kernel<<<row_grid(S.n), kThreads, coef_smem(p), st>>>(S, it, p, ks);
   return check_launch("lagged_update");
 }
 
@@ -149,7 +154,7 @@ lagged_correct_kernel(lsb_arnoldi S, int it, int p) {
 
 int launch_lagged_correct(const lsb_arnoldi& S, int it, int p, cudaStream_t st) {
   if (p < 1) return LSB_OK;
-  lagged_correct_kernel<<<row_grid(S.n), kThreads, sizeof(double) * p, st>>>(S, it, p);
+  lagged_correct_kernel<<<row_grid(S.n), kThreads, coef_smem(p), st>>>(S, it, p);
   return check_launch("lagged_correct");
 }
 
@@ -250,7 +255,7 @@ cgs_project_kernel(lsb_arnoldi S, int it, int col, int p, int want_norm) {
 
 int launch_cgs_project(const lsb_arnoldi& S, int it, int col, int p, int want_norm,
                        cudaStream_t st) {
-  cgs_project_kernel<<<row_grid(S.n), kThreads, sizeof(double) * (p > 0 ? p : 1), st>>>(
+  cgs_project_kernel<<<row_grid(S.n), kThreads, coef_smem(p), st>>>(
       S, it, col, p, want_norm);
   return check_launch("cgs_project");
 }
@@ -367,7 +372,7 @@ extract_kernel(lsb_arnoldi S, double* __restrict__ x, const double* __restrict__
 }
 
 int launch_extract(const lsb_arnoldi& S, double* x, const double* d, cudaStream_t st) {
-  extract_kernel<<<row_grid(2 * S.n), kThreads, sizeof(double) * S.cap, st>>>(S, x, d);
+  extract_kernel<<<row_grid(2 * S.n), kThreads, coef_smem(S.cap), st>>>(S, x, d);
   return check_launch("extract");
 }
 
@@ -396,7 +401,7 @@ trial_combine_kernel(lsb_arnoldi S, int it, const double* __restrict__ x,
 int launch_trial_combine(const lsb_arnoldi& S, int it, const double* x, const double* y,
                          double* xt, const double* d, cudaStream_t st) {
   if (it < 1 || it >= S.cap) return LSB_ERANGE;
-  trial_combine_kernel<<<row_grid(2 * S.n), kThreads, sizeof(double) * S.cap, st>>>(S, it, x, y,
+  trial_combine_kernel<<<row_grid(2 * S.n), kThreads, coef_smem(S.cap), st>>>(S, it, x, y,
                                                                                   xt, d);
   return check_launch("trial_combine");
 }
