@@ -82,6 +82,21 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
     const double* ut = smem + buf * stage + H;   // ut[lr] = u[r0 + lr], lr in [-H, kTile+H)
     const double* zt = smem + buf * stage + span;
     const double* pt = zt + kTile;
+    const bool full = r0 + kTile <= n;
+    const int rbase = part * kRows;
+    // the first item's basis loads do not depend on w: issue them now so
+    // they are in flight while the stencil phase below runs (only when few
+    // items per warp leave registers to spare: it spills at 8+ items)
+    constexpr bool kPrefetch = SLOTS <= 4 && kLd <= 8 && MINB == 2;
+    double2 pre[kLd];
+    if (kPrefetch) {
+      const int k0 = warp / R;
+      if (full && k0 < p) {
+        const double* col = X + (int64_t)k0 * ld + r0 + rbase;
+#pragma unroll
+        for (int q = 0; q < kLd; ++q) pre[q] = ld_stream(col + 2 * (lane + 32 * q));
+      }
+    }
     // ---- w = A u for the tile rows (row pairs; nx even keeps pairs in a line)
 #pragma unroll 2
     for (int j = threadIdx.x; j < kTile / 2; j += kThreads) {
@@ -125,8 +140,6 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
     }
     __syncthreads();
     // ---- column sweep: [Q^T u, Q^T w] partials (same item deal as mdot_kernel)
-    const bool full = r0 + kTile <= n;
-    const int rbase = part * kRows;
 #pragma unroll
     for (int s = 0; s < SLOTS; ++s) {
       const int k = (warp + kWarps * s) / R;
@@ -136,7 +149,8 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
         if (full) {
           double2 xv[kLd];
 #pragma unroll
-          for (int q = 0; q < kLd; ++q) xv[q] = ld_stream(col + 2 * (lane + 32 * q));
+          for (int q = 0; q < kLd; ++q)
+            xv[q] = (kPrefetch && s == 0) ? pre[q] : ld_stream(col + 2 * (lane + 32 * q));
 #pragma unroll
           for (int q = 0; q < kLd; ++q) {
             const int lr = rbase + 2 * (lane + 32 * q);
