@@ -134,7 +134,9 @@ typedef struct lsb_arnoldi {
 } lsb_arnoldi;
 
 /* ---------------------------------------------------------------- tuning */
-#define LSB_TUNE_FUSED_OCC3 1   /* fused K1+SpMV: 3 CTAs/SM, <= 8 items/warp  */
+#define LSB_TUNE_FUSED_OCC3 1   /* fused K1+SpMV: 0 auto (p<=40), 1 on, 2 off */
+#define LSB_TUNE_FORCE_PARTS 2  /* K1 row parts per tile column (1/2/4/8), 0 auto */
+#define LSB_TUNE_ROW_CTAS_PER_SM 3 /* row-parallel kernels: persistent CTAs/SM, 0 auto */
 #define LSB_TUNE_COUNT 8
 /* Set / read a kernel-variant knob (performance only; results unchanged up
  * to the reduction tree of the affected kernel). Returns the old value. */

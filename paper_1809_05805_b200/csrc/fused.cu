@@ -214,12 +214,12 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
   if (threadIdx.x == 0) *counter = 0u;
 }
 
-// 3 CTAs/SM (<= 8 items per warp) wins up to p ~ 40 (tools/kbench.py:
-// p=26 627 vs 679 us); above, the 2-CTA 16-item deal balances better.
-// Knob LSB_TUNE_FUSED_OCC3: 0 auto, 1 always, 2 never.
+// 3 CTAs/SM (<= 8 items per warp, register-capped) loses to the 2-CTA
+// variant with whole-tile items at every p >= 8 (tools/kfused.py: p = 26
+// 644 vs 568 us) and ties below; kept as an opt-in (knob value 1).
 static bool occ3(int p) {
-  const int k = tuning(LSB_TUNE_FUSED_OCC3);
-  return k == 1 || (k == 0 && p <= 40);
+  (void)p;
+  return tuning(LSB_TUNE_FUSED_OCC3) == 1;
 }
 
 static size_t smem_bytes(int nx) { return sizeof(double) * (2 * (kTile + 2 * nx + 2 * kTile) + kTile); }

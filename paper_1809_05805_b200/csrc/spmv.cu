@@ -191,8 +191,9 @@ int launch_stencil(const lsb_stencil* S, const double* x, const double* b, doubl
                      ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
                      (!b || (uintptr_t)b % 16 == 0);
   if (seven) {
+    static const int occ7 = wave(stencil7_pair_kernel, 0);
     int64_t g = (n64 / 2 + 255) / 256;
-    if (g > cap) g = cap;
+    if (g > (int64_t)sm_count() * occ7) g = (int64_t)sm_count() * occ7;
     if (g < 1) g = 1;
     stencil7_pair_kernel<<<(unsigned)g, 256, 0, st>>>(K, x, b, y, flags, it);
     return check_launch("stencil7");

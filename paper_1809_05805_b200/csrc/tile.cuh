@@ -9,6 +9,17 @@ constexpr int kTile = 1024;  // rows per K1 tile
 // runtime tuning knobs (lsb_set_tuning); defaults are the measured best
 int tuning(int key);
 
+// Resident CTAs per SM of kernel k (256 threads): persistent grid-stride
+// kernels launch exactly one full wave, SMs x this.  A partial second wave
+// costs up to 25% on the streaming kernels (tools/krow.py: K2 6.75 TB/s at
+// one wave vs 6.45 at a fixed 8 CTAs/SM and 5.47 at 6).
+template <class Kern>
+inline int wave(Kern k, size_t smem) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem);
+  return occ > 0 ? occ : 1;
+}
+
 // 128-bit streaming load that does not allocate in L1 (basis columns are
 // read exactly once per pass).
 __device__ __forceinline__ double2 ld_stream(const double* p) {
@@ -144,15 +155,16 @@ inline bool canonical7(const lsb_stencil* S) {
 // part) items deal evenly over 8 warps with at most 16 items per warp.
 inline int slots_for(int p, int R) { return (p * R + kWarps - 1) / kWarps; }
 inline int choose_parts(int p, int max_slots = 16) {
-  int best = 1;
-  double best_eff = 0.0;
-  for (int R = 1; R <= 8; R *= 2) {
-    const int s = slots_for(p, R);
-    if (s > max_slots) break;
-    const double eff = (double)(p * R) / (double)(s * kWarps);
-    if (eff > best_eff + 1e-9) { best_eff = eff; best = R; }
-  }
-  return best;
+  const int forced = tuning(LSB_TUNE_FORCE_PARTS);   // experiments: 1, 2, 4 or 8
+  if (forced == 1 || forced == 2 || forced == 4 || forced == 8)
+    if (slots_for(p, forced) <= max_slots) return forced;
+  // Measured (tools/kparts.py, tools/kfused.py at 256^3): whole-tile items
+  // (R = 1, 16 independent 128-bit loads per lane) beat a perfectly even
+  // deal of shorter items at every p >= 6 -- K1 reaches 7.0-7.1 TB/s with
+  // R = 1 vs 5.9 with R = 4 at p = 26.  Below that, halves keep more warps busy.
+  int R = p >= 6 ? 1 : 2;
+  while (slots_for(p, R) > max_slots && R < 8) R *= 2;
+  return R;
 }
 
 }  // namespace lsb

@@ -2,7 +2,7 @@
 // level-1 MGS axpy+dot pass (K8), norms and scalings.  All are HBM-bound
 // streaming kernels: 128-bit loads of row pairs, coefficients broadcast
 // from shared memory, grid-stride persistent CTAs.
-#include "reduce.cuh"
+#include "tile.cuh"
 
 namespace lsb {
 
@@ -17,6 +17,8 @@ static inline size_t coef_smem(int k) { return sizeof(double) * ((k > 0 ? k : 1)
 static int row_grid(int64_t n, int per_sm = 8) {
   const int64_t pairs = (n + 1) / 2;
   int64_t g = (pairs + kThreads - 1) / kThreads;
+  const int knob = tuning(LSB_TUNE_ROW_CTAS_PER_SM);
+  if (knob > 0) per_sm = knob;
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
@@ -59,7 +61,8 @@ int launch_maxpy(const double* y, const double* X, int64_t ld, int64_t n, int p,
                  const double* alpha, int sign, double* out, const lsb_flags* gate, int it,
                  cudaStream_t st) {
   if (n <= 0) return LSB_OK;
-  maxpy_kernel<<<row_grid(n), kThreads, coef_smem(p), st>>>(
+  static const int occ_ = wave(maxpy_kernel, 2048);
+  maxpy_kernel<<<row_grid(n, occ_), kThreads, coef_smem(p), st>>>(
       y, X, ld, n, p, alpha, sign < 0 ? -1.0 : 1.0, out, gate, it);
   return check_launch("maxpy");
 }
@@ -116,7 +119,8 @@ lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks) {
 
 int launch_lagged_update(const lsb_arnoldi& S, int it, int p, int ks, cudaStream_t st) {
   if (p < 1) return LSB_OK;
-  lagged_update_kernel<<<row_grid(S.n), kThreads, coef_smem(p), st>>>(S, it, p, ks);
+  static const int occ_ = wave(lagged_update_kernel, 2048);
+  lagged_update_kernel<<<row_grid(S.n, occ_), kThreads, coef_smem(p), st>>>(S, it, p, ks);
   return check_launch("lagged_update");
 }
 
@@ -154,7 +158,8 @@ lagged_correct_kernel(lsb_arnoldi S, int it, int p) {
 
 int launch_lagged_correct(const lsb_arnoldi& S, int it, int p, cudaStream_t st) {
   if (p < 1) return LSB_OK;
-  lagged_correct_kernel<<<row_grid(S.n), kThreads, coef_smem(p), st>>>(S, it, p);
+  static const int occ_ = wave(lagged_correct_kernel, 2048);
+  lagged_correct_kernel<<<row_grid(S.n, occ_), kThreads, coef_smem(p), st>>>(S, it, p);
   return check_launch("lagged_correct");
 }
 
@@ -255,7 +260,8 @@ cgs_project_kernel(lsb_arnoldi S, int it, int col, int p, int want_norm) {
 
 int launch_cgs_project(const lsb_arnoldi& S, int it, int col, int p, int want_norm,
                        cudaStream_t st) {
-  cgs_project_kernel<<<row_grid(S.n), kThreads, coef_smem(p), st>>>(
+  static const int occ_ = wave(cgs_project_kernel, 2048);
+  cgs_project_kernel<<<row_grid(S.n, occ_), kThreads, coef_smem(p), st>>>(
       S, it, col, p, want_norm);
   return check_launch("cgs_project");
 }
@@ -346,7 +352,8 @@ scale_div_kernel(const double* __restrict__ x, int64_t n, const double* s, doubl
 int launch_scale_div(const double* x, int64_t n, const double* s, double* out,
                      const lsb_flags* gate, int it, int skip_if_broke, cudaStream_t st) {
   if (n <= 0) return LSB_OK;
-  scale_div_kernel<<<row_grid(2 * n), kThreads, 0, st>>>(x, n, s, out, gate, it, skip_if_broke);
+  static const int occ_ = wave(scale_div_kernel, 2048);
+  scale_div_kernel<<<row_grid(2 * n, occ_), kThreads, 0, st>>>(x, n, s, out, gate, it, skip_if_broke);
   return check_launch("scale_div");
 }
 
@@ -372,7 +379,8 @@ extract_kernel(lsb_arnoldi S, double* __restrict__ x, const double* __restrict__
 }
 
 int launch_extract(const lsb_arnoldi& S, double* x, const double* d, cudaStream_t st) {
-  extract_kernel<<<row_grid(2 * S.n), kThreads, coef_smem(S.cap), st>>>(S, x, d);
+  static const int occ_ = wave(extract_kernel, 2048);
+  extract_kernel<<<row_grid(2 * S.n, occ_), kThreads, coef_smem(S.cap), st>>>(S, x, d);
   return check_launch("extract");
 }
 
@@ -401,7 +409,8 @@ trial_combine_kernel(lsb_arnoldi S, int it, const double* __restrict__ x,
 int launch_trial_combine(const lsb_arnoldi& S, int it, const double* x, const double* y,
                          double* xt, const double* d, cudaStream_t st) {
   if (it < 1 || it >= S.cap) return LSB_ERANGE;
-  trial_combine_kernel<<<row_grid(2 * S.n), kThreads, coef_smem(S.cap), st>>>(S, it, x, y,
+  static const int occ_ = wave(trial_combine_kernel, 2048);
+  trial_combine_kernel<<<row_grid(2 * S.n, occ_), kThreads, coef_smem(S.cap), st>>>(S, it, x, y,
                                                                                   xt, d);
   return check_launch("trial_combine");
 }
