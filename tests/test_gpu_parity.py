@@ -119,6 +119,18 @@ def test_mdot_on_device_views_large(P):
     assert torch.equal(G, G2)
 
 
+@pytest.mark.parametrize("n", [70_001, (1 << 22), 3 * (1 << 22) + 5])
+def test_chunked_staging_round_trip(P, n):
+    """numpy -> device -> numpy through the two-buffer pinned pipeline is exact
+    for one partial chunk, exactly one chunk and a ragged multi-chunk vector."""
+    from paper_1809_05805_b200 import _dev
+    a = np.random.default_rng(n).standard_normal(n)
+    t = _dev.to_device_vector(a, n)
+    assert torch.equal(t.cpu(), torch.from_numpy(a))
+    back = _dev.out_like(t * 2.0, True)
+    assert isinstance(back, np.ndarray) and np.array_equal(back, 2.0 * a)
+
+
 def test_norm_overflow_safe(P):
     led = P.ReductionLedger()
     val = P.norm2([1e200, 1e200], led)
