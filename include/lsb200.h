@@ -137,6 +137,8 @@ typedef struct lsb_arnoldi {
 #define LSB_TUNE_FUSED_OCC3 1   /* fused K1+SpMV: 0 auto (p<=40), 1 on, 2 off */
 #define LSB_TUNE_FORCE_PARTS 2  /* K1 row parts per tile column (1/2/4/8), 0 auto */
 #define LSB_TUNE_ROW_CTAS_PER_SM 3 /* row-parallel kernels: persistent CTAs/SM, 0 auto */
+#define LSB_TUNE_K3_ROWS 4      /* lagged_update_reduce tile rows 64/128/256, 0 auto */
+#define LSB_TUNE_K3_STAGES 5    /* lagged_update_reduce ring stages cap (>= 2), 0 auto */
 #define LSB_TUNE_COUNT 8
 /* Set / read a kernel-variant knob (performance only; results unchanged up
  * to the reduction tree of the affected kernel). Returns the old value. */
@@ -224,6 +226,13 @@ int lsb_cgs2_lvl2_small_b(const lsb_arnoldi* S, int32_t it, int32_t p, void* str
 /* u <- u/beta; w <- (krylov_scale ? w/beta : w) - Q coef  (one pass). */
 int lsb_lagged_update(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
                       void* stream);
+/* Two-sync first projection fused with the second reduction
+ * (gram_schmidt.py:273-276: w -= Q r; s = mass_inner_product(Q, w)):
+ * lsb_lagged_update, then Gloc[0..p) = Q^T w with Q = V[:, :p], reading Q
+ * once.  u and w are bitwise those of lsb_lagged_update.  LSB_ERANGE when
+ * p + 1 > 110 (use lsb_lagged_update + lsb_mdot). */
+int lsb_lagged_update_reduce(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
+                             void* stream);
 /* w <- w - Q coef2 (cgs2_lvl2 second projection, gram_schmidt.py:277). */
 int lsb_lagged_correct(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream);
 

@@ -94,6 +94,7 @@ _SIGS = {
     "lsb_cgs2_lvl2_small_a": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
     "lsb_cgs2_lvl2_small_b": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_lagged_update": ([_P, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_lagged_update_reduce": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_lagged_correct": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_mgs1_pass": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
     "lsb_collect_coef": ([_P, _I32, _I32, _I32, _P], C.c_int),

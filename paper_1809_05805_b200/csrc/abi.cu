@@ -38,6 +38,8 @@ int launch_maxpy(const double*, const double*, int64_t, int64_t, int, const doub
                  const lsb_flags*, int, cudaStream_t);
 int launch_lagged_update(const lsb_arnoldi&, int, int, int, cudaStream_t);
 int launch_lagged_correct(const lsb_arnoldi&, int, int, cudaStream_t);
+int launch_lagged_update_reduce(const lsb_arnoldi&, int, int, int, cudaStream_t);
+int k3_tile_rows(int);
 int launch_mgs1_pass(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int launch_cgs_project(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int launch_norm_partial(const double*, int64_t, double*, const lsb_workspace*, const lsb_flags*,
@@ -186,6 +188,14 @@ int lsb_lagged_update(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylo
   if (int rc = check_arnoldi(S)) return rc;
   if (p < 1 || p + 1 > S->cap) return LSB_ERANGE;
   return launch_lagged_update(*S, it, p, krylov_scale, S_(stream));
+}
+
+int lsb_lagged_update_reduce(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
+                             void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (p < 1 || p + 1 > S->cap || !k3_tile_rows(p)) return LSB_ERANGE;
+  if (!S->Gloc) return LSB_EINVAL;
+  return launch_lagged_update_reduce(*S, it, p, krylov_scale, S_(stream));
 }
 
 int lsb_lagged_correct(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream) {

@@ -4,7 +4,7 @@ One restart cycle of the reference driver (gmres.py:309-466) is enqueued as
 a fixed sequence of liblsb200 launches per Arnoldi iteration:
 
   one_sync_mgs / pipeline2   SpMV -> K1 lagged_reduce -> [allgather] -> K5 -> K2
-  two_sync_cgs2              SpMV -> K1 -> [ag] -> K5a -> K2 -> K1' -> [ag] -> K5b -> K4
+  two_sync_cgs2              SpMV -> K1 -> [ag] -> K5a -> K3 (= K2 + K1') -> [ag] -> K5b -> K4
   mgs_l1                     SpMV -> (p+1) x K8 pass -> [ag each] -> norm -> K5d -> scale
   cgs2                       SpMV -> K1' -> coef -> project -> K1' -> coef -> project+norm -> K5d -> scale
 
@@ -28,6 +28,7 @@ from . import _dev as D
 from .operators import device_operator
 
 LAGGED = ("one_sync_mgs", "two_sync_cgs2", "pipeline2")
+K3_MAX_COLS = 110   # lsb_lagged_update_reduce stages p + 1 <= 110 columns
 DIRECT = ("mgs_l1", "cgs2")
 
 
@@ -55,6 +56,13 @@ def _canonical7(op):
     if not isinstance(c, _abi.Stencil) or c.noff != 7 or c.col_scale or c.nx % 2 or c.nx < 4:
         return False
     return [(c.dx[k], c.dy[k], c.dz[k]) for k in range(7)] == _CANON7
+
+
+def _timing_event():
+    """Timing event that also works inside the captured cycle graph: an
+    external record becomes an event-record node, re-recorded on every
+    replay (a plain record under capture is only a dependency marker)."""
+    return torch.cuda.Event(enable_timing=True, external=True)
 
 
 _REPORT = {}
@@ -155,6 +163,8 @@ class Engine:
         # fuse the 7-point SpMV into K1 when the operator allows it
         self.fused7 = bool(fuse) and self.lagged and _canonical7(self.op) and self.n % 2 == 0 \
             and self.cap - 1 <= 128
+        # two-sync: fuse the first projection with the second reduction (K3)
+        self.fuse_k3 = bool(fuse)
 
     # ---------------------------------------------------------------- helpers
     def _vec_with_halo(self):
@@ -175,14 +185,14 @@ class Engine:
     # kernel -> (bench label, index of p in the argument list)
     _TIMED = {"lsb_lagged_reduce": ("lagged_reduce", 2),
               "lsb_lagged_reduce_spmv7": ("lagged_reduce_spmv", 3),
-              "lsb_lagged_update": ("lagged_update", 2)}
+              "lsb_lagged_update": ("lagged_update", 2),
+              "lsb_lagged_update_reduce": ("lagged_update_reduce", 2)}
 
     def _call(self, name, *args):
         self._count += 1
         tm = self.timer is not None and name in self._TIMED
         if tm:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
+            e0, e1 = _timing_event(), _timing_event()
             e0.record()
         rc = getattr(self.lib, name)(*args)
         if rc:
@@ -203,8 +213,7 @@ class Engine:
         self._count += 1
         tm = self.timer is not None and b_ptr is None
         if tm:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
+            e0, e1 = _timing_event(), _timing_event()
             e0.record()
         self.op.apply_ptr(src_ptr, dst_ptr, b_ptr, C.c_void_p(self.flags.data_ptr()), it,
                           D.stream())
@@ -305,9 +314,12 @@ class Engine:
                 self._call("lsb_lagged_update", S, i, p, 1, st)
             else:
                 self._call("lsb_cgs2_lvl2_small_a", S, i, p, 1, i, st)
-                self._call("lsb_lagged_update", S, i, p, 1, st)
-                self._call("lsb_mdot", self.col_ptr(0), self.ld, self.n, p, self.col_ptr(p), None,
-                           D.ptr(self.Gloc), self.ws.ref(), D.ptr(self.flags), i, st)
+                if self.fuse_k3 and p + 1 <= K3_MAX_COLS:   # K2 + 2nd mdot, Q read once
+                    self._call("lsb_lagged_update_reduce", S, i, p, 1, st)
+                else:
+                    self._call("lsb_lagged_update", S, i, p, 1, st)
+                    self._call("lsb_mdot", self.col_ptr(0), self.ld, self.n, p, self.col_ptr(p),
+                               None, D.ptr(self.Gloc), self.ws.ref(), D.ptr(self.flags), i, st)
                 self._gather(p)
                 self._call("lsb_cgs2_lvl2_small_b", S, i, p, st)
                 self._call("lsb_lagged_correct", S, i, p, st)

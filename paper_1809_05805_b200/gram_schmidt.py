@@ -106,10 +106,13 @@ def _lagged(V, state, j, ledger, krylov_scale, btf, eligible, two):
                              r_col=state.R[: p - 1, p - 1].cpu().numpy().copy())
     if two:
         from .kernels import MDOT
-        _abi.call("lsb_lagged_update", ref, 0, p, int(bool(krylov_scale)), st)
         ledger.record(MDOT, p, False)
-        _abi.call("lsb_mdot", C.c_void_p(V.ptr(0)), V.ld, V.n, p, C.c_void_p(V.ptr(p)), None,
-                  D.ptr(sc.G), sc.ws.ref(), None, 0, st)
+        if p + 1 <= 110:   # K3: w -= Q r and s = Q^T w in one pass over Q
+            _abi.call("lsb_lagged_update_reduce", ref, 0, p, int(bool(krylov_scale)), st)
+        else:
+            _abi.call("lsb_lagged_update", ref, 0, p, int(bool(krylov_scale)), st)
+            _abi.call("lsb_mdot", C.c_void_p(V.ptr(0)), V.ld, V.n, p, C.c_void_p(V.ptr(p)), None,
+                      D.ptr(sc.G), sc.ws.ref(), None, 0, st)
         _abi.call("lsb_cgs2_lvl2_small_b", ref, 0, p, st)
         _abi.call("lsb_lagged_correct", ref, 0, p, st)
     state.active = p

@@ -439,6 +439,59 @@ def test_fused_spmv_k1_matches_unfused(P, p):
     assert torch.allclose(G_fused, G, rtol=1e-12, atol=1e-9)
 
 
+@pytest.mark.parametrize("p,n", [(1, 4096), (2, 70_001), (7, 65_536), (26, 300_001),
+                                 (51, 1 << 20), (60, 99_999), (101, 200_000), (109, 5_000)])
+def test_fused_update_reduce_matches_unfused(P, p, n):
+    """K3 (two-sync first projection + second reduction in one pass): u and w
+    bit for bit lagged_update's, Q^T w equal to K1's up to the reduction
+    tree -- every tile width (1024..128 rows), ragged and odd n."""
+    import ctypes as C
+    from paper_1809_05805_b200 import _abi
+    from paper_1809_05805_b200 import _dev as D
+    lib, st = _abi.load(), D.stream()
+    cap = p + 2
+    ld = D.round_up(n, 32)
+    g = torch.Generator(device="cuda").manual_seed(p)
+    V = torch.randn((cap, ld), generator=g, device="cuda", dtype=torch.float64)
+    coef = torch.randn(cap, generator=g, device="cuda", dtype=torch.float64)
+    scal = torch.zeros(_abi.S_COUNT, dtype=torch.float64, device="cuda")
+    scal[_abi.S_BETA] = 1.7
+    flags = torch.tensor([_abi.NO_STOP, 0, -1, 0, 0, 0, 0, 0], dtype=torch.int32, device="cuda")
+    outs = []
+    for fused in (True, False):
+        Vc = V.clone()
+        Gloc = torch.full((2 * cap,), float("nan"), dtype=torch.float64, device="cuda")
+        ws = D.Workspace(cap)
+        z = torch.zeros(cap * cap, dtype=torch.float64, device="cuda")
+        S = _abi.Arnoldi(V=Vc.data_ptr(), ld=ld, n=n, n_global=n, cap=cap, m=cap - 2,
+                         R=z.data_ptr(), T=z.data_ptr(), L=z.data_ptr(), rot=z.data_ptr(),
+                         g=z.data_ptr(), tri=z.data_ptr(), coef=coef.data_ptr(),
+                         coef2=z.data_ptr(), G=Gloc.data_ptr(), g_parts=1, g_stride=2 * cap,
+                         Gloc=Gloc.data_ptr(), scal=scal.data_ptr(), res=z.data_ptr(),
+                         flags=flags.data_ptr(), ws=ws.c)
+        if fused:
+            _abi.check(lib.lsb_lagged_update_reduce(C.byref(S), 0, p, 1, st), "k3")
+        else:
+            _abi.check(lib.lsb_lagged_update(C.byref(S), 0, p, 1, st), "k2")
+            _abi.check(lib.lsb_mdot(C.c_void_p(Vc.data_ptr()), ld, n, p,
+                                    C.c_void_p(Vc.data_ptr() + 8 * p * ld), None,
+                                    C.c_void_p(Gloc.data_ptr()), ws.ref(), None, -1, st), "k1")
+        torch.cuda.synchronize()
+        outs.append((Vc[p - 1, :n].clone(), Vc[p, :n].clone(), Gloc[:p].clone()))
+    (u3, w3, s3), (u2, w2, s2) = outs
+    assert torch.equal(u3, u2) and torch.equal(w3, w2)
+    scale = torch.linalg.norm(V[:p, :n], dim=1) * torch.linalg.norm(w2)
+    assert torch.all((s3 - s2).abs() <= 64 * EPS * math.sqrt(n) * scale)
+
+
+def test_fused_update_reduce_rejects_wide(P):
+    from paper_1809_05805_b200 import _abi
+    from paper_1809_05805_b200.engine import Engine
+    eng = Engine(P.gen_laplace3d(8), 130, "two_sync_cgs2", 1e-12, use_graph=False)
+    rc = _abi.load().lsb_lagged_update_reduce(eng.Sref, 0, 128, 1, None)
+    assert rc == 3  # LSB_ERANGE: the engine takes the unfused pair instead
+
+
 @pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2"])
 def test_fused_and_unfused_histories_agree(P, meth):
     from paper_1809_05805_b200.engine import Engine
