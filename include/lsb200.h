@@ -253,6 +253,12 @@ int lsb_collect_coef(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t accumu
 /* z <- z + Q (-coef2) and, when want_norm, Gloc[0..1] = (max|z|, sum z^2). */
 int lsb_cgs_project(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p,
                     int32_t want_norm, void* stream);
+/* cgs_iterated's first projection fused with the second pass's reduction
+ * (gram_schmidt.py:136-138 then 131-133): z <- z - Q coef2 (bitwise equal to
+ * lsb_cgs_project), then Gloc[0..p) = Q^T z, reading Q once.  z must be
+ * column p (col == p); LSB_ERANGE when p + 1 > 110. */
+int lsb_cgs_project_reduce(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p,
+                           void* stream);
 /* r_diag from the (amax, ssq) rank partials in G; breakdown test against
  * coef[0..p); Hbar column (R[:, col]); Givens fold of column col-1;
  * convergence. */

@@ -99,6 +99,7 @@ _SIGS = {
     "lsb_mgs1_pass": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
     "lsb_collect_coef": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_cgs_project": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_cgs_project_reduce": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_direct_small": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_direct_normalize": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_ghysels_small": ([_P, _I32, _I32, _I32, _P], C.c_int),

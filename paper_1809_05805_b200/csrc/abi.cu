@@ -38,7 +38,7 @@ int launch_maxpy(const double*, const double*, int64_t, int64_t, int, const doub
                  const lsb_flags*, int, cudaStream_t);
 int launch_lagged_update(const lsb_arnoldi&, int, int, int, cudaStream_t);
 int launch_lagged_correct(const lsb_arnoldi&, int, int, cudaStream_t);
-int launch_lagged_update_reduce(const lsb_arnoldi&, int, int, int, cudaStream_t);
+int launch_lagged_update_reduce(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int k3_tile_rows(int);
 int launch_mgs1_pass(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int launch_cgs_project(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
@@ -195,7 +195,7 @@ int lsb_lagged_update_reduce(const lsb_arnoldi* S, int32_t it, int32_t p, int32_
   if (int rc = check_arnoldi(S)) return rc;
   if (p < 1 || p + 1 > S->cap || !k3_tile_rows(p)) return LSB_ERANGE;
   if (!S->Gloc) return LSB_EINVAL;
-  return launch_lagged_update_reduce(*S, it, p, krylov_scale, S_(stream));
+  return launch_lagged_update_reduce(*S, it, p, krylov_scale, 0, S_(stream));
 }
 
 int lsb_lagged_correct(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream) {
@@ -222,6 +222,14 @@ int lsb_cgs_project(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, in
   if (int rc = check_arnoldi(S)) return rc;
   if (col < p || col >= S->cap) return LSB_ERANGE;
   return launch_cgs_project(*S, it, col, p, want_norm, S_(stream));
+}
+
+int lsb_cgs_project_reduce(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p,
+                           void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (col != p || col >= S->cap || !k3_tile_rows(p)) return LSB_ERANGE;
+  if (!S->Gloc) return LSB_EINVAL;
+  return launch_lagged_update_reduce(*S, it, p, 0, 1, S_(stream));
 }
 
 int lsb_direct_small(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, void* stream) {

@@ -38,10 +38,11 @@ inline size_t k3_smem(int p, int T, int ns) {
 // half the time (the in-flight bytes drain to zero before the next issue).
 template <int SLOTS, int T>
 __global__ void __launch_bounds__(kThreads, 2)
-lagged_update_reduce_kernel(lsb_arnoldi S, int it, int p, int ks, int ns, double* __restrict__ out,
-                            double* __restrict__ partial, unsigned* counter) {
+lagged_update_reduce_kernel(lsb_arnoldi S, int it, int p, int ks, int ns, int direct,
+                            double* __restrict__ out, double* __restrict__ partial,
+                            unsigned* counter) {
   if (gated_off(S.flags, it)) return;
-  if (S.flags && S.flags->broke_iter == it) return;
+  if (!direct && S.flags && S.flags->broke_iter == it) return;
   static_assert(T % 64 == 0 && (T <= kThreads || T % kThreads == 0), "tile rows");
   constexpr int kRpt = T > kThreads ? T / kThreads : 1;   // rows per thread, phase A
   constexpr int kPairs = T / 64;            // double2 per lane per item
@@ -52,7 +53,7 @@ lagged_update_reduce_kernel(lsb_arnoldi S, int it, int p, int ks, int ns, double
   __shared__ double red[kWarps * SLOTS];
   __shared__ bool is_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int k = threadIdx.x; k < p; k += kThreads) sc[k] = S.coef[k];
+  for (int k = threadIdx.x; k < p; k += kThreads) sc[k] = direct ? S.coef2[k] : S.coef[k];
   if (threadIdx.x == 0) {
     for (int b = 0; b < ns; ++b) mbar_init(&bars[b], kWarps);
     mbar_fence_init();
@@ -115,8 +116,9 @@ lagged_update_reduce_kernel(lsb_arnoldi S, int it, int p, int ks, int ns, double
       double accr[kRpt];
 #pragma unroll
       for (int i = 0; i < kRpt; ++i) accr[i] = 0.0;
+      const int kend = direct ? p : p - 1;
 #pragma unroll 4
-      for (int k = 0; k < p - 1; ++k) {
+      for (int k = 0; k < kend; ++k) {
         const double c = sc[k];
         const double* q = col_of(buf, k) + threadIdx.x;
 #pragma unroll
@@ -125,6 +127,12 @@ lagged_update_reduce_kernel(lsb_arnoldi S, int it, int p, int ks, int ns, double
 #pragma unroll
       for (int i = 0; i < kRpt; ++i) {
         const int r = threadIdx.x + i * kThreads;
+        if (direct) {   // cgs_project's z - Q s (its fma(-s, q, .) chain is this one negated)
+          const double zz = col_of(buf, p)[r] - accr[i];
+          if (a + r < n) w[a + r] = zz;
+          col_of(buf, p)[r] = a + r < n ? zz : 0.0;
+          continue;
+        }
         const double uu = __ddiv_rn(col_of(buf, p - 1)[r], beta);
         const double acc1 = fma(cu, uu, accr[i]);
         double ww = col_of(buf, p)[r];
@@ -204,7 +212,7 @@ inline int k3_stages(int p, int T) {
 }
 
 template <int SLOTS, int T>
-int launch_k3_t(const lsb_arnoldi& S, int it, int p, int ks, cudaStream_t st) {
+int launch_k3_t(const lsb_arnoldi& S, int it, int p, int ks, int direct, cudaStream_t st) {
   auto kern = lagged_update_reduce_kernel<SLOTS, T>;
   const int ns = k3_stages(p, T);
   const size_t sm = k3_smem(p, T, ns);
@@ -226,24 +234,24 @@ int launch_k3_t(const lsb_arnoldi& S, int it, int p, int ks, cudaStream_t st) {
   if (S.ws.grid > 0 && S.ws.grid < grid) grid = S.ws.grid;
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, kThreads, sm, st>>>(S, it, p, ks, ns, S.Gloc, S.ws.partial,
+  kern<<<(unsigned)grid, kThreads, sm, st>>>(S, it, p, ks, ns, direct, S.Gloc, S.ws.partial,
                                              S.ws.counter);
   return check_launch("lagged_update_reduce");
 }
 
 template <int T>
-int launch_k3_rows(const lsb_arnoldi& S, int it, int p, int ks, cudaStream_t st) {
+int launch_k3_rows(const lsb_arnoldi& S, int it, int p, int ks, int direct, cudaStream_t st) {
   const int s = (p + kWarps - 1) / kWarps;
-  if (s <= 1) return launch_k3_t<1, T>(S, it, p, ks, st);
-  if (s <= 2) return launch_k3_t<2, T>(S, it, p, ks, st);
-  if (s <= 4) return launch_k3_t<4, T>(S, it, p, ks, st);
+  if (s <= 1) return launch_k3_t<1, T>(S, it, p, ks, direct, st);
+  if (s <= 2) return launch_k3_t<2, T>(S, it, p, ks, direct, st);
+  if (s <= 4) return launch_k3_t<4, T>(S, it, p, ks, direct, st);
   if constexpr (T > 256) {
     return LSB_ERANGE;   // wide tiles only for p <= 32
   } else {
-    if (s <= 7) return launch_k3_t<7, T>(S, it, p, ks, st);
-    if (s <= 10) return launch_k3_t<10, T>(S, it, p, ks, st);
-    if (s <= 13) return launch_k3_t<13, T>(S, it, p, ks, st);
-    return launch_k3_t<16, T>(S, it, p, ks, st);
+    if (s <= 7) return launch_k3_t<7, T>(S, it, p, ks, direct, st);
+    if (s <= 10) return launch_k3_t<10, T>(S, it, p, ks, direct, st);
+    if (s <= 13) return launch_k3_t<13, T>(S, it, p, ks, direct, st);
+    return launch_k3_t<16, T>(S, it, p, ks, direct, st);
   }
 }
 
@@ -264,17 +272,17 @@ int k3_tile_rows(int p) {
   return k3_stages(p, 64) >= 2 ? 64 : 0;
 }
 
-int launch_lagged_update_reduce(const lsb_arnoldi& S, int it, int p, int ks, cudaStream_t st) {
+int launch_lagged_update_reduce(const lsb_arnoldi& S, int it, int p, int ks, int direct, cudaStream_t st) {
   if (S.n <= 0) {
     cudaMemsetAsync(S.Gloc, 0, sizeof(double) * p, st);
     return check_launch("lagged_update_reduce-empty");
   }
   switch (k3_tile_rows(p)) {
-    case 1024: return launch_k3_rows<1024>(S, it, p, ks, st);
-    case 512: return launch_k3_rows<512>(S, it, p, ks, st);
-    case 256: return launch_k3_rows<256>(S, it, p, ks, st);
-    case 128: return launch_k3_rows<128>(S, it, p, ks, st);
-    case 64: return launch_k3_rows<64>(S, it, p, ks, st);
+    case 1024: return launch_k3_rows<1024>(S, it, p, ks, direct, st);
+    case 512: return launch_k3_rows<512>(S, it, p, ks, direct, st);
+    case 256: return launch_k3_rows<256>(S, it, p, ks, direct, st);
+    case 128: return launch_k3_rows<128>(S, it, p, ks, direct, st);
+    case 64: return launch_k3_rows<64>(S, it, p, ks, direct, st);
     default: return LSB_ERANGE;
   }
 }

@@ -188,12 +188,41 @@ mgs1_pass_kernel(lsb_arnoldi S, int it, int col, int k, int p) {
   }
   const double* qk = k < p ? S.V + (int64_t)k * ld : nullptr;
   double a0 = 0.0, a1 = 0.0;  // dot  or  (amax, ssq)
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    double zz = z[r];
-    if (qm) { zz = __dsub_rn(zz, __dmul_rn(h, qm[r])); z[r] = zz; }
-    if (qk) a0 = fma(qk[r], zz, a0);
+  auto row = [&](double zz, double qmv, double qkv) -> double {
+    if (qm) zz = __dsub_rn(zz, __dmul_rn(h, qmv));
+    if (qk) a0 = fma(qkv, zz, a0);
     else { a0 = fmax(a0, fabs(zz)); a1 = fma(zz, zz, a1); }
+    return zz;
+  };
+  // row pairs, two pairs per thread per step: six independent 128-bit loads
+  // in flight (a scalar row loop leaves the pass latency-bound)
+  const int64_t npair = n / 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double2 zero2 = make_double2(0.0, 0.0);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair; j += 2 * stride) {
+    const int64_t j2 = j + stride;
+    const bool two = j2 < npair;
+    const double2 z0 = ld2(z + 2 * j);
+    const double2 z1 = two ? ld2(z + 2 * j2) : zero2;
+    const double2 m0 = qm ? ld2(qm + 2 * j) : zero2;
+    const double2 m1 = qm && two ? ld2(qm + 2 * j2) : zero2;
+    const double2 k0 = qk ? ld2(qk + 2 * j) : zero2;
+    const double2 k1 = qk && two ? ld2(qk + 2 * j2) : zero2;
+    double2 o0;
+    o0.x = row(z0.x, m0.x, k0.x);
+    o0.y = row(z0.y, m0.y, k0.y);
+    if (qm) st2(z + 2 * j, o0);
+    if (two) {
+      double2 o1;
+      o1.x = row(z1.x, m1.x, k1.x);
+      o1.y = row(z1.y, m1.y, k1.y);
+      if (qm) st2(z + 2 * j2, o1);
+    }
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t r = n - 1;
+    const double zz = row(z[r], qm ? qm[r] : 0.0, qk ? qk[r] : 0.0);
+    if (qm) z[r] = zz;
   }
   if (qk) {
     const double v[1] = {a0};
@@ -207,8 +236,8 @@ mgs1_pass_kernel(lsb_arnoldi S, int it, int col, int k, int p) {
 }
 
 int launch_mgs1_pass(const lsb_arnoldi& S, int it, int col, int k, int p, cudaStream_t st) {
-  int g = row_grid(2 * S.n, 4);
-  mgs1_pass_kernel<<<g, kThreads, 0, st>>>(S, it, col, k, p);
+  static const int occ_ = wave(mgs1_pass_kernel, 0);
+  mgs1_pass_kernel<<<row_grid(S.n / 2 + 1, occ_), kThreads, 0, st>>>(S, it, col, k, p);
   return check_launch("mgs1_pass");
 }
 

@@ -422,12 +422,18 @@ class Engine:
                     self._call("lsb_mgs1_pass", S, i, i, k, p, st)
                     self._gather(2)
             else:
+                fused = self.fuse_k3 and p + 1 <= K3_MAX_COLS
                 for accumulate in (0, 1):
-                    self._call("lsb_mdot", self.col_ptr(0), self.ld, self.n, p, self.col_ptr(i),
-                               None, D.ptr(self.Gloc), self.ws.ref(), D.ptr(self.flags), i, st)
+                    if not (fused and accumulate):
+                        self._call("lsb_mdot", self.col_ptr(0), self.ld, self.n, p,
+                                   self.col_ptr(i), None, D.ptr(self.Gloc), self.ws.ref(),
+                                   D.ptr(self.flags), i, st)
                     self._gather(p)
                     self._call("lsb_collect_coef", S, i, p, accumulate, st)
-                    self._call("lsb_cgs_project", S, i, i, p, accumulate, st)
+                    if fused and not accumulate:   # z -= Q s and the 2nd pass's Q^T z, one read of Q
+                        self._call("lsb_cgs_project_reduce", S, i, i, p, st)
+                    else:
+                        self._call("lsb_cgs_project", S, i, i, p, accumulate, st)
                 self._gather(2)
             self._call("lsb_norm_finish", D.ptr(self.G), self.S.g_parts, self.S.g_stride, self.col_ptr(i), self.n,
                        C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_BETA), self.ws.ref(),

@@ -180,12 +180,18 @@ def _direct(Q, a, ledger, btf, passes):
                 ledger.record(DOT, 1)
             _abi.call("lsb_mgs1_pass", ref, 0, p, k, p, st)
     else:
+        fused_next = False   # Q^T z of this pass already produced by the previous projection
         for ps in range(passes if p else 0):
             ledger.record(MDOT, p)
-            _abi.call("lsb_mdot", C.c_void_p(store.data_ptr()), ld, n, p, zp, None, D.ptr(sc.G),
-                      sc.ws.ref(), None, 0, st)
+            if not fused_next:
+                _abi.call("lsb_mdot", C.c_void_p(store.data_ptr()), ld, n, p, zp, None,
+                          D.ptr(sc.G), sc.ws.ref(), None, 0, st)
             _abi.call("lsb_collect_coef", ref, 0, p, int(ps > 0), st)
-            _abi.call("lsb_cgs_project", ref, 0, p, p, int(ps == passes - 1), st)
+            fused_next = ps < passes - 1 and p + 1 <= 110
+            if fused_next:   # z -= Q s and the next pass's Q^T z in one read of Q
+                _abi.call("lsb_cgs_project_reduce", ref, 0, p, p, st)
+            else:
+                _abi.call("lsb_cgs_project", ref, 0, p, p, int(ps == passes - 1), st)
         if not p:
             _abi.call("lsb_norm_partial", zp, n, D.ptr(sc.G), sc.ws.ref(), None, 0, st)
     ledger.record(NORM, 1)

@@ -492,7 +492,48 @@ def test_fused_update_reduce_rejects_wide(P):
     assert rc == 3  # LSB_ERANGE: the engine takes the unfused pair instead
 
 
-@pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2"])
+@pytest.mark.parametrize("p,n", [(1, 4096), (7, 70_001), (30, 1 << 20), (60, 99_999)])
+def test_fused_project_reduce_matches_unfused(P, p, n):
+    """Direct-mode K3 (cgs_iterated: z -= Q s, then the next pass's Q^T z):
+    z bit for bit cgs_project's, Q^T z equal to K1's up to the tree."""
+    import ctypes as C
+    from paper_1809_05805_b200 import _abi
+    from paper_1809_05805_b200 import _dev as D
+    lib, st = _abi.load(), D.stream()
+    cap = p + 1
+    ld = D.round_up(n, 32)
+    g = torch.Generator(device="cuda").manual_seed(100 + p)
+    V = torch.randn((cap, ld), generator=g, device="cuda", dtype=torch.float64)
+    coef2 = torch.randn(cap, generator=g, device="cuda", dtype=torch.float64)
+    flags = torch.tensor([_abi.NO_STOP, 0, -1, 0, 0, 0, 0, 0], dtype=torch.int32, device="cuda")
+    outs = []
+    for fused in (True, False):
+        Vc = V.clone()
+        Gloc = torch.full((2 * cap,), float("nan"), dtype=torch.float64, device="cuda")
+        ws = D.Workspace(cap)
+        z = torch.zeros(cap * cap + _abi.S_COUNT, dtype=torch.float64, device="cuda")
+        S = _abi.Arnoldi(V=Vc.data_ptr(), ld=ld, n=n, n_global=n, cap=cap, m=cap - 1,
+                         R=z.data_ptr(), T=z.data_ptr(), L=z.data_ptr(), rot=z.data_ptr(),
+                         g=z.data_ptr(), tri=z.data_ptr(), coef=z.data_ptr(),
+                         coef2=coef2.data_ptr(), G=Gloc.data_ptr(), g_parts=1, g_stride=2 * cap,
+                         Gloc=Gloc.data_ptr(), scal=z.data_ptr(), res=z.data_ptr(),
+                         flags=flags.data_ptr(), ws=ws.c)
+        if fused:
+            _abi.check(lib.lsb_cgs_project_reduce(C.byref(S), 1, p, p, st), "k3d")
+        else:
+            _abi.check(lib.lsb_cgs_project(C.byref(S), 1, p, p, 0, st), "project")
+            _abi.check(lib.lsb_mdot(C.c_void_p(Vc.data_ptr()), ld, n, p,
+                                    C.c_void_p(Vc.data_ptr() + 8 * p * ld), None,
+                                    C.c_void_p(Gloc.data_ptr()), ws.ref(), None, -1, st), "k1")
+        torch.cuda.synchronize()
+        outs.append((Vc[p, :n].clone(), Gloc[:p].clone()))
+    (z3, s3), (z2, s2) = outs
+    assert torch.equal(z3, z2)
+    scale = torch.linalg.norm(V[:p, :n], dim=1) * torch.linalg.norm(z2)
+    assert torch.all((s3 - s2).abs() <= 64 * EPS * math.sqrt(n) * scale)
+
+
+@pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2", "cgs2"])
 def test_fused_and_unfused_histories_agree(P, meth):
     from paper_1809_05805_b200.engine import Engine
     A = P.gen_laplace3d(40)
@@ -500,7 +541,7 @@ def test_fused_and_unfused_histories_agree(P, meth):
     curves = []
     for fuse in (True, False):
         eng = Engine(A, 30, meth, 1e-12, fuse=fuse, use_graph=False)
-        assert eng.fused7 == fuse
+        assert eng.fused7 == (fuse and meth != "cgs2") and eng.fuse_k3 == fuse
         eng.load(b)
         eng.prologue()
         curves.append(np.concatenate([eng.cycle().res[1:] for _ in range(2)]))
