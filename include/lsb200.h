@@ -139,6 +139,7 @@ typedef struct lsb_arnoldi {
 #define LSB_TUNE_ROW_CTAS_PER_SM 3 /* row-parallel kernels: persistent CTAs/SM, 0 auto */
 #define LSB_TUNE_K3_ROWS 4      /* lagged_update_reduce tile rows 64/128/256, 0 auto */
 #define LSB_TUNE_K3_STAGES 5    /* lagged_update_reduce ring stages cap (>= 2), 0 auto */
+#define LSB_TUNE_CSR_THREAD_ROW 6 /* CSR SpMV: 0 warp-staged (default), 1 thread per row, 2 warp-staged 8 loads/lane at 3 CTAs/SM */
 #define LSB_TUNE_COUNT 8
 /* Set / read a kernel-variant knob (performance only; results unchanged up
  * to the reduction tree of the affected kernel). Returns the old value. */

@@ -21,6 +21,9 @@ NO_STOP = 0x7FFFFFFF
 S_BETA, S_TARGET, S_DENOM, S_RNORM, S_RELTOL, S_BTF, S_AMAX, S_SSQ, S_TOL, S_RAD = range(10)
 S_COUNT = 16
 MAX_OFF = 27
+# lsb_set_tuning keys (include/lsb200.h LSB_TUNE_*)
+TUNE_FUSED_OCC3, TUNE_FORCE_PARTS, TUNE_ROW_CTAS_PER_SM = 1, 2, 3
+TUNE_K3_ROWS, TUNE_K3_STAGES, TUNE_CSR_THREAD_ROW = 4, 5, 6
 
 
 class LsbUnavailable(RuntimeError):

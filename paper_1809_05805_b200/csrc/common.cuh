@@ -105,6 +105,98 @@ __device__ __forceinline__ double np_row_sum(const Acc& a, int64_t cnt) {
   return __dadd_rn(first, np_pairwise(a, 1, cnt - 1));
 }
 
+// Same order for a row whose length C is a compile-time constant and whose
+// products sit in a register array: every index is folded after unrolling,
+// so nothing spills to local memory (the runtime-length np_row_sum on a
+// register array forces the array into local memory).
+template <int S, int N, int M>
+__device__ __forceinline__ double np_pw_fixed(const double (&a)[M]) {
+  if constexpr (N < 8) {
+    double res = -0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) res = __dadd_rn(res, a[S + i]);
+    return res;
+  } else if constexpr (N <= 128) {
+    double r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = a[S + k];
+#pragma unroll
+    for (int i = 8; i < N - (N % 8); i += 8)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], a[S + i + k]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+    for (int i = N - (N % 8); i < N; ++i) res = __dadd_rn(res, a[S + i]);
+    return res;
+  } else {
+    constexpr int n2 = N / 2 - (N / 2) % 8;
+    return __dadd_rn(np_pw_fixed<S, n2>(a), np_pw_fixed<S + n2, N - n2>(a));
+  }
+}
+
+template <int C, int M>
+__device__ __forceinline__ double np_row_sum_fixed(const double (&a)[M]) {
+  if constexpr (C <= 0) return 0.0;
+  else if constexpr (C == 1) return a[0];
+  else return __dadd_rn(a[0], np_pw_fixed<1, C - 1>(a));
+}
+
+// ---------------------------------------------------------------- 27-point box rows
+// The 27-point box stencil (offsets (dx,dy,dz) in {-1,0,1}^3, CSR column
+// order o = (dz+1)*9 + (dy+1)*3 + (dx+1)).  With Dirichlet boundaries the
+// present neighbours of a row are a sub-box fixed by one state per axis:
+// bit 0 = the -1 neighbour exists, bit 1 = the +1 neighbour exists.  For
+// each of the 4^3 state triples the compacted product list (and hence
+// numpy's pairwise order over it) is a compile-time fact: box27_row<SX,SY,SZ>
+// sums it fully unrolled in registers.
+struct Box27Plan {
+  int cnt;
+  int idx[27];
+};
+__host__ __device__ constexpr Box27Plan box27_plan(int sx, int sy, int sz) {
+  Box27Plan P{0, {}};
+  for (int o = 0; o < 27; ++o) {
+    const int d[3] = {o % 3 - 1, (o / 3) % 3 - 1, o / 9 - 1};
+    const int s[3] = {sx, sy, sz};
+    bool ok = true;
+    for (int a = 0; a < 3; ++a) {
+      if (d[a] < 0 && !(s[a] & 1)) ok = false;
+      if (d[a] > 0 && !(s[a] & 2)) ok = false;
+    }
+    if (ok) P.idx[P.cnt++] = o;
+  }
+  return P;
+}
+
+// g(o): (already scaled) x at the neighbour of offset o; c(o): its
+// coefficient (offsets in column order).
+template <int SX, int SY, int SZ, class Gx, class Cf>
+__device__ __forceinline__ double box27_row(const Gx& g, const Cf& c) {
+  constexpr Box27Plan P = box27_plan(SX, SY, SZ);
+  double q[P.cnt > 0 ? P.cnt : 1];
+#pragma unroll
+  for (int j = 0; j < P.cnt; ++j) q[j] = __dmul_rn(c(P.idx[j]), g(P.idx[j]));
+  return np_row_sum_fixed<P.cnt>(q);
+}
+
+// state = sx + 4*sy + 16*sz -> box27_row<sx, sy, sz>
+template <class Gx, class Cf>
+__device__ __forceinline__ double box27_dispatch(int state, const Gx& g, const Cf& c) {
+  if (state == 63) return box27_row<3, 3, 3>(g, c);   // interior: the hot case
+  switch (state) {
+#define LSB_B27(k) case k: return box27_row<((k) & 3), (((k) >> 2) & 3), ((k) >> 4)>(g, c);
+#define LSB_B27x4(k) LSB_B27(k) LSB_B27(k + 1) LSB_B27(k + 2) LSB_B27(k + 3)
+#define LSB_B27x16(k) LSB_B27x4(k) LSB_B27x4(k + 4) LSB_B27x4(k + 8) LSB_B27x4(k + 12)
+    LSB_B27x16(0) LSB_B27x16(16) LSB_B27x16(32)
+    LSB_B27x4(48) LSB_B27x4(52) LSB_B27x4(56) LSB_B27(60) LSB_B27(61) LSB_B27(62)
+    default: return 0.0;
+#undef LSB_B27x16
+#undef LSB_B27x4
+#undef LSB_B27
+  }
+}
+
 // ---------------------------------------------------------------- CPython hypot
 // math.hypot(a, b) of CPython 3.12 (Modules/mathmodule.c vector_norm):
 // lossless scaling to [0.5, 1), double-length squares and sums, one

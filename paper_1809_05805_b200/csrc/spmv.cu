@@ -9,10 +9,13 @@
 // K6 is matrix-free: a constant-coefficient box stencil (5-point 2D,
 // 7-point and 27-point 3D) whose offsets are given in CSR column order; it
 // moves 16 B/row of compulsory HBM traffic instead of CSR's ~12*nnz/n + 20.
-// Interior rows (all neighbours present) take a register-only path; the
-// 7-point operator additionally works on row pairs with 128-bit loads.
-// Boundary rows fall back to a packed generic path.  K7 is a general CSR
-// kernel with 32-bit indices.
+// The 7-point and 27-point operators work on row pairs with 128-bit loads;
+// the 27-point rows pick their present-neighbour sub-box at compile time
+// (common.cuh box27_row) so products and pairwise sums stay in registers.
+// Other layouts take the generic per-row path.  K7 is a general CSR kernel
+// with 32-bit indices: a warp stages the products of 32 consecutive rows in
+// shared memory from coalesced col/value streams, then every lane sums its
+// own row in numpy's order.
 #include "tile.cuh"
 
 namespace lsb {
@@ -88,6 +91,135 @@ stencil_kernel(const StencilK K, const double* __restrict__ x, const double* __r
     y[r] = b ? __dsub_rn(b[r], s) : s;
   }
   if (bad && flags) flags->nonfinite = 1;
+}
+
+// 27-point box operator (offsets {-1,0,1}^3 in column order): one row per
+// thread, the row's present-neighbour sub-box picked by box27_dispatch so the
+// 27 products and numpy's pairwise sum stay in registers (the generic
+// stencil_kernel<27> kept them in local memory: 204 GB/s at 256^3).
+__global__ void __launch_bounds__(256)
+stencil27_kernel(const StencilK K, const double* __restrict__ x, const double* __restrict__ b,
+                 double* __restrict__ y, lsb_flags* flags, int it) {
+  if (gated_off(flags, it)) return;
+  const uint32_t n = (uint32_t)K.nx * K.ny * K.nz;
+  bool bad = false;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const uint32_t line = K.fx.div(r);
+    const int ix = (int)(r - line * (uint32_t)K.nx);
+    const uint32_t iz = K.fy.div(line);
+    const int iy = (int)(line - iz * (uint32_t)K.ny);
+    const int state = (ix >= 1) | ((ix + 1 < K.nx) << 1) | ((iy >= 1) << 2) |
+                      ((iy + 1 < K.ny) << 3) | (((int)iz - 1 >= K.zlo) << 4) |
+                      (((int)iz + 1 <= K.zhi) << 5);
+    const double s = box27_dispatch(
+        state, [&](int o) { return ldx(K, x, (int64_t)r + K.lin[o]); },
+        [&](int o) { return K.val[o]; });
+    if (!isfinite(s)) bad = true;
+    y[r] = b ? __dsub_rn(b[r], s) : s;
+  }
+  if (bad && flags) flags->nonfinite = 1;
+}
+
+// Same operator on row pairs (nx even, x 16-byte aligned, no column scale):
+// each of the 9 (dz, dy) lines is loaded once for both rows as one LDG.128
+// plus two LDG.64 from a line base pointer (immediate offsets), 27 loads per
+// two rows instead of 54 loads with a 64-bit address each.  Absent lines
+// (Dirichlet planes / edges) are not loaded; the row's plan never reads them.
+// Work items are split so warps do not diverge on the x edges: first the
+// interior pairs of every x-line (ix = 2 .. nx-4, both rows have both x
+// neighbours: one shared plan), then the two edge pairs of every line.
+__device__ __forceinline__ void load27_pair(const double* __restrict__ x, int64_t r,
+                                            int64_t nx, int64_t plane, int sy, int sz,
+                                            bool xm, bool xp, double (&v)[9][4]) {
+#pragma unroll
+  for (int l = 0; l < 9; ++l) {
+    const int dz = l / 3 - 1, dy = l % 3 - 1;
+    const bool pres = (dy < 0 ? (sy & 1) : dy > 0 ? (sy & 2) : 1) &&
+                      (dz < 0 ? (sz & 1) : dz > 0 ? (sz & 2) : 1);
+    const double* base = x + r + dz * plane + dy * nx;
+    double2 c2 = make_double2(0.0, 0.0);
+    v[l][0] = v[l][3] = 0.0;
+    if (pres) {
+      c2 = __ldg(reinterpret_cast<const double2*>(base));
+      if (xm) v[l][0] = __ldg(base - 1);
+      if (xp) v[l][3] = __ldg(base + 2);
+    }
+    v[l][1] = c2.x;
+    v[l][2] = c2.y;
+  }
+}
+
+template <int SY, int SZ, class Cf>
+__device__ __forceinline__ void box27_pair_row(const double (&v)[9][4], const Cf& cf, double& y0,
+                                               double& y1) {
+  y0 = box27_row<3, SY, SZ>([&](int o) { return v[o / 3][o % 3]; }, cf);
+  y1 = box27_row<3, SY, SZ>([&](int o) { return v[o / 3][o % 3 + 1]; }, cf);
+}
+
+__global__ void __launch_bounds__(256)
+stencil27_pair_kernel(const StencilK K, FastDiv fint, const double* __restrict__ x,
+                      const double* __restrict__ b, double* __restrict__ y, lsb_flags* flags,
+                      int it) {
+  if (gated_off(flags, it)) return;
+  const uint32_t lines = (uint32_t)K.ny * K.nz;
+  const uint32_t nint = K.nx >= 6 ? (uint32_t)(K.nx / 2 - 2) : 0u;  // interior pairs per line
+  const uint32_t items_int = lines * nint, items = items_int + 2u * lines;
+  const int64_t nx = K.nx, plane = (int64_t)K.nx * K.ny;
+  auto cf = [&](int o) { return K.val[o]; };
+  bool bad = false;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < items; i += gridDim.x * blockDim.x) {
+    uint32_t line;
+    int ix;
+    if (i < items_int) {
+      line = fint.div(i);
+      ix = 2 + 2 * (int)(i - line * nint);
+    } else {
+      const uint32_t e = i - items_int;
+      line = e >> 1;
+      ix = (e & 1) ? K.nx - 2 : 0;
+    }
+    const uint32_t iz = K.fy.div(line);
+    const int iy = (int)(line - iz * (uint32_t)K.ny);
+    const int64_t r = (int64_t)line * nx + ix;
+    const int sy = (iy >= 1) | ((iy + 1 < K.ny) << 1);
+    const int sz = ((int)iz - 1 >= K.zlo) | (((int)iz + 1 <= K.zhi) << 1);
+    const bool xm = ix >= 1, xp = ix + 2 < K.nx;
+    double v[9][4];
+    load27_pair(x, r, nx, plane, sy, sz, xm, xp, v);
+    double y0, y1;
+    if (xm && xp) {     // both rows interior in x: one plan for the pair
+      switch (sy | (sz << 2)) {
+#define LSB_P27(k) case k: box27_pair_row<((k) & 3), ((k) >> 2)>(v, cf, y0, y1); break;
+        LSB_P27(0) LSB_P27(1) LSB_P27(2) LSB_P27(3) LSB_P27(4) LSB_P27(5) LSB_P27(6)
+        LSB_P27(7) LSB_P27(8) LSB_P27(9) LSB_P27(10) LSB_P27(11) LSB_P27(12) LSB_P27(13)
+        LSB_P27(14)
+#undef LSB_P27
+        default: box27_pair_row<3, 3>(v, cf, y0, y1); break;
+      }
+    } else {
+      const int s0 = (xm ? 1 : 0) | 2 | (sy << 2) | (sz << 4);
+      const int s1 = 1 | (xp ? 2 : 0) | (sy << 2) | (sz << 4);
+      y0 = box27_dispatch(s0, [&](int o) { return v[o / 3][o % 3]; }, cf);
+      y1 = box27_dispatch(s1, [&](int o) { return v[o / 3][o % 3 + 1]; }, cf);
+    }
+    if (!isfinite(y0) || !isfinite(y1)) bad = true;
+    double2 out;
+    if (b) {
+      const double2 bb = *reinterpret_cast<const double2*>(b + r);
+      out = make_double2(__dsub_rn(bb.x, y0), __dsub_rn(bb.y, y1));
+    } else {
+      out = make_double2(y0, y1);
+    }
+    *reinterpret_cast<double2*>(y + r) = out;
+  }
+  if (bad && flags) flags->nonfinite = 1;
+}
+
+static bool canonical27(const lsb_stencil* S) {
+  if (S->noff != 27) return false;
+  for (int o = 0; o < 27; ++o)
+    if (S->dx[o] != o % 3 - 1 || S->dy[o] != (o / 3) % 3 - 1 || S->dz[o] != o / 9 - 1) return false;
+  return true;
 }
 
 // 7-point operator on row pairs (nx even): 5 x LDG.128 + 2 x LDG.64 per
@@ -201,6 +333,22 @@ int launch_stencil(const lsb_stencil* S, const double* x, const double* b, doubl
   int64_t g = (n64 + 255) / 256;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
+  if (canonical27(S) && S->nx % 2 == 0 && S->nx >= 4 && !S->col_scale &&
+      (uintptr_t)x % 16 == 0 && (uintptr_t)y % 16 == 0 && (!b || (uintptr_t)b % 16 == 0)) {
+    static const int occ27p = wave(stencil27_pair_kernel, 0);
+    int64_t gp = (n64 / 2 + 255) / 256;
+    if (gp > (int64_t)sm_count() * occ27p) gp = (int64_t)sm_count() * occ27p;
+    if (gp < 1) gp = 1;
+    const FastDiv fint = FastDiv::make(S->nx >= 6 ? (uint32_t)(S->nx / 2 - 2) : 1u);
+    stencil27_pair_kernel<<<(unsigned)gp, 256, 0, st>>>(K, fint, x, b, y, flags, it);
+    return check_launch("stencil27_pair");
+  }
+  if (canonical27(S)) {
+    static const int occ27 = wave(stencil27_kernel, 0);
+    if (g > (int64_t)sm_count() * occ27) g = (int64_t)sm_count() * occ27;
+    stencil27_kernel<<<(unsigned)g, 256, 0, st>>>(K, x, b, y, flags, it);
+    return check_launch("stencil27");
+  }
   if (!unit) {
     stencil_kernel<0><<<(unsigned)g, 256, 0, st>>>(K, x, b, y, flags, it);
     return check_launch("stencil");
@@ -245,9 +393,138 @@ csr_kernel(const lsb_csr A, const double* __restrict__ x, const double* __restri
   if (bad && flags) flags->nonfinite = 1;
 }
 
+// Warp-staged CSR: a warp owns 32 consecutive rows.  Their nonzeros form one
+// contiguous segment [row_ptr[r0], row_ptr[r0+32]); the warp streams it with
+// coalesced col/value loads (kCsrUnroll independent loads in flight per lane),
+// forms each product val*x[col] exactly once, and parks it in a per-warp
+// shared-memory slab.  Each lane then sums its own row from shared memory in
+// numpy's reduceat order (np_row_sum), so y is bitwise the thread-per-row
+// result.  A thread-per-row CSR warp touches 32 rows 12*nnz/n bytes apart per
+// load instruction and depends on L1 to catch the rest of each sector;
+// staging makes every col/value sector a single full-line request.
+// Segments longer than the slab fall back to thread-per-row for that group.
+constexpr int kCsrSlab = 1024;   // products per warp (8 KB)
+constexpr int kCsrWarps = 8;
+
+// col/value streams are read exactly once: keep them out of L1 so it holds x
+__device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p) {
+  int32_t r;
+  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double ld_stream_f64(const double* p) {
+  double r;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+
+struct SmemAcc {
+  const double* a;
+  __device__ double operator()(int64_t j) const { return a[j]; }
+};
+
+template <int kCsrUnroll, int MINB = 1>
+__global__ void __launch_bounds__(kCsrWarps * 32, MINB)
+csr_warp_kernel(const lsb_csr A, const double* __restrict__ x, const double* __restrict__ b,
+                double* __restrict__ y, lsb_flags* flags, int it) {
+  if (gated_off(flags, it)) return;
+  extern __shared__ double csr_slab[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* slab = csr_slab + wid * kCsrSlab;
+  const int32_t* __restrict__ colv = A.col_idx;
+  const double* __restrict__ valv = A.values;
+  const double* __restrict__ d = A.col_scale;
+  const int64_t n = A.n_rows, ngroups = (n + 31) >> 5;
+  const int64_t wstride = (int64_t)gridDim.x * kCsrWarps;
+  bool bad = false;
+  for (int64_t g = (int64_t)blockIdx.x * kCsrWarps + wid; g < ngroups; g += wstride) {
+    const int64_t r0 = g << 5, r = r0 + lane;
+    const int64_t rlast = min(r0 + 32, n);
+    const int64_t lo = __ldg(A.row_ptr + r0), hi = __ldg(A.row_ptr + rlast);
+    int64_t rs = 0, re = 0;
+    if (r < n) { rs = __ldg(A.row_ptr + r); re = __ldg(A.row_ptr + r + 1); }
+    const int64_t seg = hi - lo;
+    double s;
+    if (seg <= kCsrSlab) {
+      // three explicit phases per batch so every load of a phase is in flight
+      // at once: col/value stream, then the x gathers, then products -> slab
+      const int32_t* __restrict__ cg = colv + lo;
+      const double* __restrict__ vg = valv + lo;
+      const int segi = (int)seg;
+      const int32_t c_pad = (int32_t)A.x_lo;
+      for (int j0 = 0; j0 < segi; j0 += 32 * kCsrUnroll) {
+        int32_t c[kCsrUnroll];
+        double v[kCsrUnroll], xv[kCsrUnroll];
+#pragma unroll
+        for (int u = 0; u < kCsrUnroll; ++u) {
+          const int j = j0 + u * 32 + lane;
+          c[u] = j < segi ? ld_stream_i32(cg + j) : c_pad;
+          v[u] = j < segi ? ld_stream_f64(vg + j) : 0.0;
+        }
+        if (d) {
+          double dv[kCsrUnroll];
+#pragma unroll
+          for (int u = 0; u < kCsrUnroll; ++u) {
+            const int64_t cc = (int64_t)c[u] - A.x_lo;
+            xv[u] = __ldg(x + cc);
+            dv[u] = __ldg(d + cc);
+          }
+#pragma unroll
+          for (int u = 0; u < kCsrUnroll; ++u) xv[u] = __dmul_rn(xv[u], dv[u]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < kCsrUnroll; ++u) xv[u] = __ldg(x + ((int64_t)c[u] - A.x_lo));
+        }
+#pragma unroll
+        for (int u = 0; u < kCsrUnroll; ++u) {
+          const int j = j0 + u * 32 + lane;
+          if (j < segi) slab[j] = __dmul_rn(v[u], xv[u]);
+        }
+      }
+      __syncwarp();
+      s = np_row_sum(SmemAcc{slab + (rs - lo)}, re - rs);
+      __syncwarp();
+    } else {
+      s = np_row_sum(CsrRowAcc{colv + rs, valv + rs, x, d, A.x_lo}, re - rs);
+    }
+    if (r < n) {
+      if (!isfinite(s)) bad = true;
+      y[r] = b ? __dsub_rn(b[r], s) : s;
+    }
+  }
+  if (bad && flags) flags->nonfinite = 1;
+}
+
+template <int U, int MINB = 1>
+static int launch_csr_warp(const lsb_csr* A, const double* x, const double* b, double* y,
+                           lsb_flags* flags, int it, cudaStream_t st) {
+  constexpr size_t smem = sizeof(double) * kCsrSlab * kCsrWarps;
+  static const int occ = [] {
+    cudaFuncSetAttribute(csr_warp_kernel<U, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, csr_warp_kernel<U, MINB>, kCsrWarps * 32,
+                                                  smem);
+    return o > 0 ? o : 1;
+  }();
+  const int64_t groups = (A->n_rows + 31) / 32;
+  int64_t g = (groups + kCsrWarps - 1) / kCsrWarps;
+  if (g > (int64_t)sm_count() * occ) g = (int64_t)sm_count() * occ;
+  csr_warp_kernel<U, MINB><<<(unsigned)g, kCsrWarps * 32, smem, st>>>(*A, x, b, y, flags, it);
+  return check_launch("csr_warp");
+}
+
 int launch_csr(const lsb_csr* A, const double* x, const double* b, double* y, lsb_flags* flags,
                int it, cudaStream_t st) {
   if (A->n_rows <= 0) return LSB_OK;
+  const int knob = tuning(LSB_TUNE_CSR_THREAD_ROW);
+  if (knob != 1) {
+    // 16 independent col/value loads per lane at 2 CTAs/SM (116 registers)
+    // measured best on the 27-point CSR at 256^3: 5.02 TB/s vs 4.81 for 8
+    // loads at 3 CTAs/SM (knob 2), 4.72 for 12 at 3 and 3.79 thread-per-row
+    if (knob == 2) return launch_csr_warp<8, 3>(A, x, b, y, flags, it, st);
+    return launch_csr_warp<16, 2>(A, x, b, y, flags, it, st);
+  }
   int64_t g = (A->n_rows + 255) / 256;
   const int64_t cap = (int64_t)sm_count() * 8;
   if (g > cap) g = cap;

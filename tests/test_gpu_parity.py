@@ -82,6 +82,74 @@ def test_spmv_empty_rows(P):
     assert np.array_equal(P.spmv(A, [1.0, 1.0, 1.0]), [4.0, 0.0, 5.0])
 
 
+@pytest.mark.parametrize("knob", [0, 1, 2])   # K7 variants: warp-staged (0, 2), thread per row (1)
+def test_spmv_csr_kernels_mixed_segments(P, knob):
+    """Row groups whose 32-row segment fits the warp slab and groups that
+    overflow it (rows of 40..300 entries), empty rows, ragged tail; y = Ax and
+    the residual form y = b - Ax, with and without a column scale."""
+    from paper_1809_05805_b200 import _abi
+    from paper_1809_05805_b200.operators import CsrOperator
+    rng = np.random.default_rng(11)
+    n = 32 * 9 + 13
+    lens = rng.integers(0, 30, n)
+    lens[64:96] = rng.integers(40, 300, 32)       # one overflowing group
+    lens[200] = 1000                              # one very long row
+    lens[7:11] = 0
+    cols = [np.sort(rng.choice(n, size=min(int(k), n), replace=False)) for k in lens]
+    ptr = np.concatenate([[0], np.cumsum([len(c) for c in cols])]).astype(np.int64)
+    ci = np.concatenate(cols).astype(np.int64)
+    vals = rng.standard_normal(ci.size) * np.exp(rng.standard_normal(ci.size) * 3)
+    O = orc.Csr(n, n, ptr, ci, vals)
+    A = P.CsrMatrix(n, n, O.row_ptr, O.col_idx, O.values)
+    x = rng.standard_normal(n)
+    b = rng.standard_normal(n)
+    d = rng.uniform(0.5, 2.0, n)
+    lib = _abi.load()
+    lib.lsb_set_tuning(_abi.TUNE_CSR_THREAD_ROW, knob)
+    try:
+        op = CsrOperator(A)
+        xd, bd, dd = (torch.as_tensor(v).cuda() for v in (x, b, d))
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        op.apply(xd, y)
+        assert np.array_equal(_np(y), orc.spmv(O, x))
+        op.apply(xd, y, b=bd)
+        assert np.array_equal(_np(y), b - orc.spmv(O, x))
+        op.with_scale(dd).apply(xd, y)
+        assert np.array_equal(_np(y), orc.spmv(O, x * d))
+    finally:
+        lib.lsb_set_tuning(_abi.TUNE_CSR_THREAD_ROW, 0)
+
+
+@pytest.mark.parametrize("dims", [(4, 3, 7), (6, 5, 4), (8, 8, 8), (12, 7, 5), (9, 4, 4), (10, 3, 3)])
+def test_spmv_box27_bitwise_shapes(P, dims):
+    """27-point operator on boxes that exercise every edge class of the
+    row-pair kernel (nx = 4 has no interior pairs) and the odd-nx fallback;
+    y = Ax and y = b - Ax, bitwise against the reference SpMV order."""
+    from paper_1809_05805_b200.operators import convdiff27
+    S, O = convdiff27(0, dims=dims), orc.convdiff27(0, dims=dims)
+    n = O.n_rows
+    rng = np.random.default_rng(sum(dims))
+    x = rng.standard_normal(n) * np.exp(rng.standard_normal(n) * 4)
+    b = rng.standard_normal(n)
+    ref = orc.spmv(O, x)
+    op = S.device_op()
+    xd, bd = torch.as_tensor(x).cuda(), torch.as_tensor(b).cuda()
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    op.apply(xd, y)
+    assert np.array_equal(_np(y), ref)
+    op.apply(xd, y, b=bd)
+    assert np.array_equal(_np(y), b - ref)
+
+
+def test_stencil_device_csr_matches_host(P):
+    S = P.gen_convdiff27(9)
+    O = orc.convdiff27(9)
+    C = S.device_csr()
+    assert np.array_equal(_np(C.row_ptr), O.row_ptr)
+    assert np.array_equal(_np(C.col_idx), O.col_idx)
+    assert np.array_equal(_np(C.values), O.values)
+
+
 # ------------------------------------------------------------------ reductions
 @pytest.mark.parametrize("tag", ["a", "b", "c"])
 def test_mdot_pair_mass_maxpy_norm_dot(P, K, tag):
