@@ -140,7 +140,9 @@ typedef struct lsb_arnoldi {
 #define LSB_TUNE_K3_ROWS 4      /* lagged_update_reduce tile rows 64/128/256, 0 auto */
 #define LSB_TUNE_K3_STAGES 5    /* lagged_update_reduce ring stages cap (>= 2), 0 auto */
 #define LSB_TUNE_CSR_THREAD_ROW 6 /* CSR SpMV: 0 warp-staged (default), 1 thread per row, 2 warp-staged 8 loads/lane at 3 CTAs/SM */
-#define LSB_TUNE_COUNT 8
+#define LSB_TUNE_PERSIST_TRACE 7  /* 1: lsb_cycle_persistent records phase timestamps */
+#define LSB_TUNE_PERSIST_CTAS 8   /* lsb_cycle_persistent cluster size 1..16, 0 auto */
+#define LSB_TUNE_COUNT 16
 /* Set / read a kernel-variant knob (performance only; results unchanged up
  * to the reduction tree of the affected kernel). Returns the old value. */
 int lsb_set_tuning(int32_t key, int32_t value);
@@ -218,6 +220,24 @@ int lsb_mgs_lvl2_small(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t kryl
  * (settle, gmres.py:427-435), for a small-state call made with
  * givens_col = -col; runs on a side stream in the pipeline2 schedule. */
 int lsb_settle(const lsb_arnoldi* S, int32_t it, int32_t col, void* stream);
+
+/* One whole lagged one-sync restart cycle (iterations 0..m of
+ * gmres.py:389-466 with mgs_lvl2, gram_schmidt.py:206-245: SpMV, fused
+ * reduction, K5 small state, K2 update) in ONE launch of one thread-block
+ * cluster (<= 16 CTAs, distributed-shared-memory reduction, cluster
+ * barriers) for launch-bound sizes.  A is the operator as CSR (a stencil's
+ * CSR gives the same bits).  Call between lsb_cycle_begin and
+ * lsb_cycle_lsq in place of the per-iteration kernels.  Every CTA keeps its
+ * rows of all cap basis columns in shared memory: LSB_ERANGE when they do
+ * not fit (lsb_cycle_persistent_fits) or the state is multi-rank. */
+int lsb_cycle_persistent(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_scale,
+                         void* stream);
+/* 1 if an n-row, cap-column cycle fits one cluster's shared memory
+ * (n * cap <= ~450K doubles, cap <= 128), else 0.  No device needed. */
+int lsb_cycle_persistent_fits(int64_t n, int32_t cap);
+/* Diagnostics: the last traced persistent cycle's phase timestamps (6 per
+ * iteration, globaltimer ns; LSB_TUNE_PERSIST_TRACE = 1 to record). */
+int lsb_persist_trace(int64_t* out, int32_t count);
 /* cgs2_lvl2 front: beta, breakdown, L row, r = (I - L - L^T) y (/beta). */
 int lsb_cgs2_lvl2_small_a(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
                           int32_t givens_col, void* stream);

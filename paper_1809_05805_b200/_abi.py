@@ -24,6 +24,7 @@ MAX_OFF = 27
 # lsb_set_tuning keys (include/lsb200.h LSB_TUNE_*)
 TUNE_FUSED_OCC3, TUNE_FORCE_PARTS, TUNE_ROW_CTAS_PER_SM = 1, 2, 3
 TUNE_K3_ROWS, TUNE_K3_STAGES, TUNE_CSR_THREAD_ROW = 4, 5, 6
+TUNE_PERSIST_TRACE, TUNE_PERSIST_CTAS = 7, 8
 
 
 class LsbUnavailable(RuntimeError):
@@ -107,6 +108,9 @@ _SIGS = {
     "lsb_direct_normalize": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_ghysels_small": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_settle": ([_P, _I32, _I32, _P], C.c_int),
+    "lsb_cycle_persistent": ([_P, _P, _I32, _P], C.c_int),
+    "lsb_cycle_persistent_fits": ([C.c_int64, _I32], C.c_int),
+    "lsb_persist_trace": ([_P, _I32], C.c_int),
     "lsb_cycle_begin": ([_P, _P], C.c_int),
     "lsb_cycle_lsq": ([_P, _P], C.c_int),
     "lsb_cycle_extract": ([_P, _P, _P, _P], C.c_int),

@@ -54,6 +54,9 @@ int launch_stencil(const lsb_stencil*, const double*, const double*, double*, ls
 int launch_csr(const lsb_csr*, const double*, const double*, double*, lsb_flags*, int,
                cudaStream_t);
 int launch_mgs_lvl2_small(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
+int launch_cycle_persistent(const lsb_arnoldi&, const lsb_csr*, int, cudaStream_t);
+int persist_fits(int64_t, int);
+int persist_trace(long long*, int);
 int launch_cgs2_small_a(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int launch_cgs2_small_b(const lsb_arnoldi&, int, int, cudaStream_t);
 int launch_collect_coef(const lsb_arnoldi&, int, int, int, cudaStream_t);
@@ -169,6 +172,20 @@ int lsb_mgs_lvl2_small(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t kryl
                        int32_t givens_col, void* stream) {
   if (int rc = check_arnoldi(S)) return rc;
   return launch_mgs_lvl2_small(*S, it, p, krylov_scale, givens_col, S_(stream));
+}
+
+int lsb_cycle_persistent(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_scale,
+                         void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (!A) return LSB_EINVAL;
+  return launch_cycle_persistent(*S, A, krylov_scale, S_(stream));
+}
+
+int lsb_cycle_persistent_fits(int64_t n, int32_t cap) { return persist_fits(n, cap); }
+
+int lsb_persist_trace(int64_t* out, int32_t count) {
+  if (!out || count < 0) return LSB_EINVAL;
+  return persist_trace((long long*)out, count);
 }
 
 int lsb_cgs2_lvl2_small_a(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,

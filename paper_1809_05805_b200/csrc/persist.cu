@@ -1,0 +1,340 @@
+// Persistent cluster cycle: a whole lagged one-sync GMRES(m) restart cycle
+// (Arnoldi iterations 0..m of gmres.py:389-466 with mgs_lvl2,
+// gram_schmidt.py:206-245) in ONE launch of ONE thread-block cluster.
+//
+// At launch-bound sizes (C1: n = 4,096) the per-iteration kernels spend
+// their time in launch and grid-reduction latency, not in HBM traffic.  Here
+// up to 16 CTAs of one cluster each hold a contiguous row block of EVERY
+// basis column in shared memory (V never leaves the SMs during the cycle;
+// columns are mirrored to HBM for the cycle epilogue) and run the
+// iterations back to back:
+//   SpMV of the own rows: CSR, u of every row read from its owner CTA
+//     through distributed shared memory, numpy row order (the K7 bits)
+//   -> per-CTA [Q^T u, Q^T w] partials (shared memory only)
+//   -> cluster barrier; CTA 0 sums the partials of all CTAs in rank order
+//      over DSMEM and runs the K5 small state (mgs_small_body: beta,
+//      breakdown test, T column, c = T^T y, Hessenberg column, Givens)
+//   -> cluster barrier; every CTA applies the K2 row update to its rows
+//   -> cluster barrier (the next SpMV reads the updated column).
+// Three cluster barriers per iteration replace four kernel launches and
+// three grid-wide last-CTA reductions.  Barriers are release/acquire at
+// cluster scope; the flags and coefficients CTA 0 writes are read with
+// ld.global.cg.
+//
+// Results: SpMV, beta, T, c, Givens and the K2 row expression are the
+// per-iteration kernels' own code; only the order of the mdot sum differs
+// (per-CTA warp trees + rank-ordered cluster sum instead of the K1 tree),
+// so histories agree with the multi-kernel path to rounding
+// (tests/test_gpu_parity.py).
+#include <cooperative_groups.h>
+
+#include "small_body.cuh"
+#include "tile.cuh"
+
+namespace lsb {
+
+namespace cgx = cooperative_groups;
+
+constexpr int kPT = 512;            // threads per CTA
+constexpr int kPWarps = kPT / 32;
+constexpr int kPMaxCap = 128;       // basis columns (p + 1 <= cap)
+constexpr int kPMaxCluster = 16;
+constexpr size_t kPMaxSmem = 200 * 1024;   // + ~10 KB static <= 227 KB
+
+// Phase timestamps of CTA 0 (tuning knob LSB_TUNE_PERSIST_TRACE, read back
+// with lsb_persist_trace): 6 per iteration, globaltimer ns.
+constexpr int kTraceSlots = 10;
+__device__ long long g_ptrace[kTraceSlots * kPMaxCap];
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define LSB_TRACE(slot, cta) \
+  if (trace && crank == (cta) && tid == 0) g_ptrace[kTraceSlots * i + (slot)] = gtimer();
+
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile(
+      "barrier.cluster.arrive.release.aligned;\n\t"
+      "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Row sum in numpy's order with every product load issued before the first
+// add: rows of <= 8 / <= 32 entries go through a compile-time plan
+// (np_row_sum_fixed) selected by a switch, longer rows through np_row_sum.
+template <int C, class Acc>
+__device__ __forceinline__ double row_sum_c(const Acc& a) {
+  double q[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) q[k] = a(k);
+  return np_row_sum_fixed<C>(q);
+}
+template <class Acc>
+__device__ __forceinline__ double row_sum_fast(const Acc& a, int cnt) {
+  switch (cnt) {
+    case 0: return 0.0;
+#define LSB_RS(c) case c: return row_sum_c<c>(a);
+    LSB_RS(1) LSB_RS(2) LSB_RS(3) LSB_RS(4) LSB_RS(5) LSB_RS(6) LSB_RS(7) LSB_RS(8)
+    LSB_RS(9) LSB_RS(10) LSB_RS(11) LSB_RS(12) LSB_RS(13) LSB_RS(14) LSB_RS(15) LSB_RS(16)
+    LSB_RS(17) LSB_RS(18) LSB_RS(19) LSB_RS(20) LSB_RS(21) LSB_RS(22) LSB_RS(23) LSB_RS(24)
+    LSB_RS(25) LSB_RS(26) LSB_RS(27) LSB_RS(28) LSB_RS(29) LSB_RS(30) LSB_RS(31) LSB_RS(32)
+#undef LSB_RS
+    default: return np_row_sum(a, cnt);
+  }
+}
+
+// CSR row products with x = a basis column held, row block by row block, in
+// the shared memory of the cluster's CTAs (read through DSMEM).
+struct CsrRowAccCluster {
+  const int32_t* col;
+  const double* val;
+  const double* d;
+  double* const* peer;   // peer[c] = CTA c's V block (shared memory, DSMEM address)
+  size_t coloff;         // column offset inside a block
+  FastDiv rdiv;          // division by rows per CTA
+  int rows;
+  __device__ double operator()(int64_t j) const {
+    const uint32_t c = (uint32_t)__ldg(col + j);
+    const uint32_t blk = rdiv.div(c);            // row block; owned by CTA blk + 1
+    double xv = peer[blk + 1][coloff + (c - blk * (uint32_t)rows)];
+    if (d) xv = __dmul_rn(xv, __ldg(d + c));
+    return __dmul_rn(__ldg(val + j), xv);
+  }
+};
+
+__global__ void __launch_bounds__(kPT, 1)
+persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, int t_cap,
+                     bool trace) {
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int crank = (int)cl.block_rank(), csize = (int)cl.num_blocks();
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int cap = S.cap;
+  extern __shared__ __align__(16) double dyn[];
+  double* Vs = dyn;                          // cap columns x rows: own rows of V
+  double* allp = Vs + (size_t)cap * rows;    // [16][2*cap]: every CTA's [Q^T u, Q^T w]
+                                             // (pushed into CTA 0's copy over DSMEM)
+  double* sG = allp + kPMaxCluster * 2 * cap;  // 2*cap: their rank-ordered sum (CTA 0)
+  double* sc = sG + 2 * cap;                 // cap: projection coefficients
+  double* sg = sc + cap;                     // cap: rotated rhs g (CTA 0)
+  double* sT = sg + cap;                     // t_cap^2: T block of the small state
+  __shared__ SmallShared sh;
+  __shared__ double* s_peer[kPMaxCluster];
+  // published by CTA 0: [0] beta, [1] K2 skipped (breakdown at this
+  // iteration) -- before barrier (2); [2] next iteration runs (gated_off
+  // semantics, after the Givens fold) -- before barrier (3)
+  __shared__ double s_pub[3];
+  __shared__ int s_go;
+  const int64_t ld = S.ld;
+  // CTA 0 is the control CTA (reductions, small state, Givens fold) and
+  // owns no rows; row block b lives in CTA b + 1
+  const int64_t r0 = crank == 0 ? S.n : (int64_t)(crank - 1) * rows;
+  const int64_t r1 = min(r0 + (int64_t)rows, S.n);
+  const int nr = r1 > r0 ? (int)(r1 - r0) : 0;
+  // own rows of V[:, 0] (= r / beta from lsb_scale_div) into shared memory
+  for (int j = tid; j < nr; j += kPT) Vs[j] = S.V[r0 + j];
+  if (tid < csize) s_peer[tid] = tid == crank ? Vs : cl.map_shared_rank(Vs, tid);
+  if (crank == 0)
+    for (int e = tid; e <= S.m; e += kPT) sg[e] = S.g[e];
+  if (tid == 0) {
+    const int stop = __ldcg(&S.flags->stop_iter), broke = __ldcg(&S.flags->broke_iter);
+    s_go = !(stop < 0 || (broke >= 0 && broke < 0));   // gated_off(flags, 0)
+  }
+  const double* pub0 = cl.map_shared_rank(s_pub, 0);
+  const double* sc0 = cl.map_shared_rank(sc, 0);
+  double* allp0 = cl.map_shared_rank(allp, 0) + crank * 2 * cap;   // this CTA's slot at CTA 0
+  SmallResident res;
+  res.ldT = t_cap;
+  res.resident = true;
+  res.coef = sc;
+  res.G = sG;
+  res.g = sg;
+  res.scal_cached = true;
+  res.btf = S.scal[LSB_S_BTF];
+  res.target = S.scal[LSB_S_TARGET];
+  bool bad = false;
+  cluster_barrier();
+
+  for (int i = 0; i <= S.m; ++i) {
+    const int p = i + 1;
+    __syncthreads();
+    if (!s_go) break;    // same decision in every CTA (CTA 0's published flag)
+    double* su = Vs + (size_t)(p - 1) * rows;   // u = V[:, p-1], own rows
+    double* sw = Vs + (size_t)p * rows;         // w = V[:, p]
+    double* gu = S.V + (int64_t)(p - 1) * ld;
+    double* gw = S.V + (int64_t)p * ld;
+    LSB_TRACE(0, 1)
+
+    // ---- w = A u on the own rows (V.push(A v_i), gmres.py:411); u of
+    // every row from its owner's shared memory
+    for (int j = tid; j < nr; j += kPT) {
+      const int64_t r = r0 + j;
+      const int lo = __ldg(A.row_ptr + r), hi = __ldg(A.row_ptr + r + 1);
+      const double s = row_sum_fast(CsrRowAccCluster{A.col_idx + lo, A.values + lo, A.col_scale,
+                                                     s_peer, (size_t)(p - 1) * rows, rdiv, rows},
+                                    hi - lo);
+      if (!isfinite(s)) bad = true;
+      sw[j] = s;
+      gw[r] = s;
+    }
+    __syncthreads();
+
+    // ---- partial [Q^T u, Q^T w] of the own rows: warp wid takes columns
+    // wid, wid + 16, ...; lanes stride the rows
+    for (int k = wid; k < p; k += kPWarps) {
+      const double* q = Vs + (size_t)k * rows;
+      double a = 0.0, b = 0.0;
+#pragma unroll 4
+      for (int j = lane; j < nr; j += 32) {
+        const double qv = q[j];
+        a = fma(qv, su[j], a);
+        b = fma(qv, sw[j], b);
+      }
+      a = warp_sum(a);
+      b = warp_sum(b);
+      if (lane == 0) {   // straight into CTA 0's shared memory (DSMEM store)
+        allp0[2 * k] = a;
+        allp0[2 * k + 1] = b;
+      }
+    }
+    LSB_TRACE(1, 1)
+    cluster_barrier();   // (1) every CTA's partials are complete
+    LSB_TRACE(2, 0)
+
+    // ---- CTA 0: cluster sum in rank order (the partials already sit in
+    // its shared memory), then the K5 small state, resident in this CTA
+    // for the whole cycle
+    if (crank == 0) {
+      for (int e = tid; e < 2 * p; e += kPT) {
+        double acc = 0.0;
+        for (int c = 1; c < csize; ++c) acc += allp[c * 2 * cap + e];
+        sG[e] = acc;
+        S.G[e] = acc;
+      }
+      __syncthreads();
+      LSB_TRACE(3, 0)
+      res.trace = trace ? g_ptrace + kTraceSlots * i + 6 : nullptr;
+      // Givens fold deferred (givens_col = -i, the pipeline2 schedule of
+      // gmres.py:444-462): it runs below, while the other CTAs apply K2
+      mgs_small_body(S, sh, sT, i, p, ks, -i, p <= t_cap, res);
+      if (tid == 0) {
+        s_pub[0] = sh.beta;
+        s_pub[1] = sh.broke ? 1.0 : 0.0;
+      }
+    }
+    LSB_TRACE(4, 0)
+    cluster_barrier();   // (2) coef and beta are published
+
+    if (crank == 0) {    // fold Hessenberg column i-1 (sh.col) into the Givens state
+      if (i > 0) settle_block(S, sh, i, i, sh.broke, &res);
+      __syncthreads();
+      if (tid == 0) {
+        const int stop = S.flags->stop_iter, broke = S.flags->broke_iter;
+        s_pub[2] = (stop < i + 1 || (broke >= 0 && broke < i + 1)) ? 0.0 : 1.0;
+      }
+    }
+
+    // ---- K2 on the own rows (gram_schmidt.py:230-242; lagged_update_kernel's
+    // row expression), skipped on breakdown
+    const double beta = pub0[0];
+    const bool skip = pub0[1] != 0.0;
+    if (crank != 0)
+      for (int k = tid; k < p; k += kPT) sc[k] = sc0[k];
+    __syncthreads();
+    if (!skip) {
+      const double cu = sc[p - 1];
+      for (int j = tid; j < nr; j += kPT) {
+        const int64_t r = r0 + j;
+        double acc = 0.0;
+        for (int k = 0; k < p - 1; ++k) acc = fma(sc[k], Vs[(size_t)k * rows + j], acc);
+        const double uu = __ddiv_rn(su[j], beta);
+        su[j] = uu;
+        gu[r] = uu;
+        acc = fma(cu, uu, acc);
+        double ww = sw[j];
+        if (ks) ww = __ddiv_rn(ww, beta);
+        ww = ww - acc;
+        sw[j] = ww;
+        gw[r] = ww;
+      }
+    }
+    LSB_TRACE(5, 1)
+    cluster_barrier();   // (3) the next SpMV reads the updated column; the
+                         // fold's stop decision is published
+    if (tid == 0) s_go = pub0[2] != 0.0;
+  }
+  if (bad && S.flags) S.flags->nonfinite = 1;
+  // no CTA may exit while a peer can still read its shared memory (s_pub)
+  cluster_barrier();
+}
+
+// Cluster shape for (n, cap): 16 CTAs at most, ~256 rows each, V's own
+// rows + the T block in shared memory.  Returns the CTA count, 0 if no fit.
+static int persist_plan(int64_t n, int cap, int* rows_out, int* tcap_out, size_t* smem_out) {
+  if (n < 1 || cap < 2 || cap > kPMaxCap || cap > kSmall) return 0;
+  // one control CTA + row CTAs of ~256 rows
+  int csize = 1 + (int)((n + 255) / 256);
+  const int forced = tuning(LSB_TUNE_PERSIST_CTAS);
+  if (forced >= 2 && forced <= kPMaxCluster) csize = forced;
+  if (csize < 2) csize = 2;
+  if (csize > kPMaxCluster) csize = kPMaxCluster;
+  const int64_t rows = (n + csize - 2) / (csize - 1);
+  const size_t base = sizeof(double) * ((size_t)cap * rows + (2 * kPMaxCluster + 4) * cap);
+  if (base > kPMaxSmem) return 0;
+  int t_cap = 0;             // T block staged while p*p doubles fit
+  while (t_cap < cap - 1 &&
+         base + sizeof(double) * (size_t)(t_cap + 1) * (t_cap + 1) <= kPMaxSmem)
+    ++t_cap;
+  *rows_out = (int)rows;
+  *tcap_out = t_cap;
+  *smem_out = base + sizeof(double) * (size_t)t_cap * t_cap;
+  return csize;
+}
+
+int persist_trace(long long* out, int count) {
+  if (count > kTraceSlots * kPMaxCap) count = kTraceSlots * kPMaxCap;
+  if (cudaMemcpyFromSymbol(out, g_ptrace, sizeof(long long) * count) != cudaSuccess)
+    return check_launch("persist_trace");
+  return LSB_OK;
+}
+
+int persist_fits(int64_t n, int cap) {
+  int rows, tc;
+  size_t sm;
+  return persist_plan(n, cap, &rows, &tc, &sm) > 0;
+}
+
+int launch_cycle_persistent(const lsb_arnoldi& S, const lsb_csr* A, int ks, cudaStream_t st) {
+  if (!A || S.g_parts != 1 || S.m + 2 > S.cap || A->n_rows != S.n || A->n_cols != S.n ||
+      A->x_lo != 0 || A->nnz >= (1LL << 31))
+    return LSB_ERANGE;
+  int rows = 0, t_cap = 0;
+  size_t smem = 0;
+  const int csize = persist_plan(S.n, S.cap, &rows, &t_cap, &smem);
+  if (!csize) return LSB_ERANGE;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(persist_cycle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kPMaxSmem);
+    cudaFuncSetAttribute(persist_cycle_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)csize, 1, 1);
+  cfg.blockDim = dim3(kPT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)csize;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const lsb_csr Av = *A;
+  const bool trace = tuning(LSB_TUNE_PERSIST_TRACE) == 1;
+  cudaLaunchKernelEx(&cfg, persist_cycle_kernel, S, Av, rows, FastDiv::make((uint32_t)rows), ks,
+                     t_cap, trace);
+  return check_launch("cycle_persistent");
+}
+
+}  // namespace lsb

@@ -11,151 +11,17 @@
 // Reference: gram_schmidt.py:96-106 (breakdown), 206-245 (mgs_lvl2),
 // 248-280 (cgs2_lvl2), gmres.py:153-192 (Givens / least squares),
 // gmres.py:407-435 (Hessenberg column assembly and settle).
-#include "reduce.cuh"
+#include "small_body.cuh"
 
 namespace lsb {
-
-constexpr int kSmall = 256;  // threads; cap <= kSmall
-
-__device__ __forceinline__ double gsum(const lsb_arnoldi& S, int e) {
-  double v = S.G[e];
-  for (int q = 1; q < S.g_parts; ++q) v += S.G[(int64_t)q * S.g_stride + e];
-  return v;
-}
-
-struct SmallShared {
-  double a[kSmall];     // G[:,0] / scaled
-  double y[kSmall];     // G[:,1] / y
-  double col[kSmall + 2];  // R column (r_col, then the Hessenberg column)
-  double rot[2 * kSmall];
-  double beta, tol;
-  int broke;
-};
-
-// tol = btf * eps * sqrt(n) * hypot(r_diag, ||r_col||)   (gram_schmidt.py:96-100)
-__device__ double breakdown_tol(const lsb_arnoldi& S, double r_diag, const double* rcol, int len) {
-  double pre = r_diag;
-  if (len > 0) {
-    double ss = 0.0;
-    for (int j = 0; j < len; ++j) ss = fma(rcol[j], rcol[j], ss);
-    pre = py_hypot(r_diag, sqrt(ss));
-  }
-  const double btf = S.scal[LSB_S_BTF];
-  return __dmul_rn(__dmul_rn(__dmul_rn(btf, kEps), sqrt((double)S.n_global)), pre);
-}
-
-// Block-cooperative settle (gmres.py:427-435): Hessenberg column gc-1 is
-// sh.col[0..gc] (= R[0..gc, gc], with R[gc,gc] = 0 after a breakdown);
-// fold it into the Givens state, record |g[gc]|, stop on convergence or
-// breakdown.  All threads must call it.
-__device__ void settle_block(const lsb_arnoldi& S, SmallShared& sh, int it, int gc, bool broke) {
-  const int t = threadIdx.x;
-  for (int e = t; e < 2 * (gc - 1); e += blockDim.x) sh.rot[e] = S.rot[e];
-  __syncthreads();
-  if (t == 0) {
-    const double res = givens_fold(sh.col, sh.rot, S.g, gc);
-    S.rot[2 * (gc - 1)] = sh.rot[2 * (gc - 1)];
-    S.rot[2 * (gc - 1) + 1] = sh.rot[2 * (gc - 1) + 1];
-    S.res[gc] = res;
-    const double target = S.scal[LSB_S_TARGET];
-    if (res <= target || broke) {
-      S.flags->stop_iter = it;
-      S.flags->status = res <= target ? LSB_CONVERGED : LSB_BREAKDOWN;
-    }
-  }
-  __syncthreads();
-  for (int j = t; j <= gc; j += blockDim.x) S.tri[(int64_t)j * S.m + (gc - 1)] = sh.col[j];
-}
-
-// Shared front of both lagged kernels: gathered G, deferred norm beta,
-// breakdown test against R[:p-1, p-1] (gram_schmidt.py:227-229 / 261-263).
-__device__ bool lagged_front(const lsb_arnoldi& S, SmallShared& sh, int it, int p, int gc) {
-  const int t = threadIdx.x, cap = S.cap;
-  for (int e = t; e < p; e += blockDim.x) {
-    sh.a[e] = gsum(S, 2 * e);
-    sh.y[e] = gsum(S, 2 * e + 1);
-    if (e < p - 1) sh.col[e] = S.R[(int64_t)e * cap + (p - 1)];
-  }
-  __syncthreads();
-  if (t == 0) {
-    const double bsq = sh.a[p - 1];
-    const double beta = bsq > 0.0 ? sqrt(bsq) : 0.0;
-    const double tol = breakdown_tol(S, beta, sh.col, p - 1);
-    sh.beta = beta;
-    sh.tol = tol;
-    sh.broke = beta <= tol;
-    S.scal[LSB_S_BETA] = beta;
-    S.scal[LSB_S_TOL] = tol;
-    if (sh.broke) {
-      S.flags->broke_iter = it;
-      if (gc == 0) { S.flags->stop_iter = it; S.flags->status = LSB_STARTUP_BREAKDOWN; }
-      sh.col[p - 1] = 0.0;   // H[i, i-1] = 0 (gmres.py:416)
-    } else {
-      sh.col[p - 1] = beta;  // H[i, i-1] = R[i, i] = beta (gmres.py:418)
-      S.R[(int64_t)(p - 1) * cap + (p - 1)] = beta;
-    }
-  }
-  __syncthreads();
-  return sh.broke;
-}
 
 // ------------------------------------------------------------------ mgs_lvl2
 __global__ void __launch_bounds__(kSmall)
 mgs_lvl2_small_kernel(lsb_arnoldi S, int it, int p, int ks, int gc, bool use_smem) {
   if (gated_off(S.flags, it)) return;
   __shared__ SmallShared sh;
-  const int t = threadIdx.x, cap = S.cap;
-  const bool broke = lagged_front(S, sh, it, p, gc);
-  if (broke) {
-    if (gc > 0) settle_block(S, sh, it, gc, true);
-    return;
-  }
-  const double beta = sh.beta;
-  // T block in shared memory when it fits (p x p, row stride p): the two
-  // triangular mat-vecs then run at smem latency (launch sets the size)
   extern __shared__ double sT[];
-  const bool st = use_smem;
-  if (st) {
-    for (int e = t; e < (p - 1) * (p - 1); e += blockDim.x) {
-      const int j = e / (p - 1), l = e - j * (p - 1);
-      sT[j * p + l] = S.T[(int64_t)j * cap + l];
-    }
-  }
-  // T[:p-1, p-1] = -(T[:p-1, :p-1] @ (G[:p-1, 0] / beta));  T[p-1, p-1] = 1
-  for (int e = t; e < p - 1; e += blockDim.x) sh.a[e] = __ddiv_rn(sh.a[e], beta);
-  if (t == 0) sh.y[p - 1] = __ddiv_rn(sh.y[p - 1], beta);
-  __syncthreads();
-  for (int j = t; j < p - 1; j += blockDim.x) {
-    double acc = 0.0;
-    if (st) {
-      for (int l = j; l < p - 1; ++l) acc = fma(sT[j * p + l], sh.a[l], acc);
-      sT[j * p + (p - 1)] = -acc;
-    } else {
-      for (int l = j; l < p - 1; ++l) acc = fma(S.T[(int64_t)j * cap + l], sh.a[l], acc);
-    }
-    S.T[(int64_t)j * cap + (p - 1)] = -acc;
-  }
-  if (t == 0) {
-    S.T[(int64_t)(p - 1) * cap + (p - 1)] = 1.0;
-    if (st) {
-      sT[(p - 1) * p + (p - 1)] = 1.0;
-      for (int l = 0; l < p - 1; ++l) sT[(p - 1) * p + l] = 0.0;
-    }
-  }
-  __syncthreads();
-  // c = T[:p,:p]^T y  (/beta);  R[:p, p] = c
-  for (int j = t; j < p; j += blockDim.x) {
-    double acc = 0.0;
-    if (st) {
-      for (int l = 0; l <= j; ++l) acc = fma(sT[l * p + j], sh.y[l], acc);
-    } else {
-      for (int l = 0; l <= j; ++l) acc = fma(S.T[(int64_t)l * cap + j], sh.y[l], acc);
-    }
-    if (ks) acc = __ddiv_rn(acc, beta);
-    S.coef[j] = acc;
-    S.R[(int64_t)j * cap + p] = acc;
-  }
-  if (gc > 0) settle_block(S, sh, it, gc, false);
+  mgs_small_body(S, sh, sT, it, p, ks, gc, use_smem);
 }
 
 // Deferred settle (pipeline2, gmres.py:444-462): the Givens fold of

@@ -19,6 +19,7 @@ reads one small report (flags, residuals, scalars) per cycle.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -29,6 +30,9 @@ from .operators import device_operator
 
 LAGGED = ("one_sync_mgs", "two_sync_cgs2", "pipeline2")
 K3_MAX_COLS = 110   # lsb_lagged_update_reduce stages p + 1 <= 110 columns
+# one-cluster persistent cycle (lsb_cycle_persistent): launch-bound sizes
+# whose basis fits the cluster's shared memory (lsb_cycle_persistent_fits)
+PERSIST_METHODS = ("one_sync_mgs", "pipeline2")
 DIRECT = ("mgs_l1", "cgs2")
 
 
@@ -81,7 +85,7 @@ def _report_buffers(m):
 class Engine:
     def __init__(self, A, m, method, rel_tol, btf=1.0, inv_diag=None, comm=None,
                  diagnostics=False, use_graph=True, n_global=None, op=None, fuse=True,
-                 true_residual=False):
+                 true_residual=False, persistent=None):
         self.dev = D.require_cuda()
         self.lib = _abi.load()
         base_op = op if op is not None else device_operator(A)
@@ -165,6 +169,29 @@ class Engine:
             and self.cap - 1 <= 128
         # two-sync: fuse the first projection with the second reduction (K3)
         self.fuse_k3 = bool(fuse)
+        # launch-bound sizes: the whole lagged cycle as one cluster launch
+        self.pcsr = None
+        env = os.environ.get("LSB_PERSISTENT")
+        want = persistent if persistent is not None else (None if env is None else env != "0")
+        if want is not False and method in PERSIST_METHODS and comm is None \
+                and not diagnostics and not self.true_residual \
+                and self.lib.lsb_cycle_persistent_fits(self.n, self.cap):
+            self.pcsr = self._persist_csr(base_op)
+        self.persistent = self.pcsr is not None
+
+    def _persist_csr(self, base_op):
+        """The operator as device CSR (bitwise the same SpMV), column-scaled
+        like self.op under the Jacobi preconditioner; None if unavailable."""
+        from .operators import CsrOperator, StencilOperator
+        if isinstance(base_op, StencilOperator) and not base_op.halo:
+            csr = base_op.stencil.device_csr()
+        elif isinstance(base_op, CsrOperator) and base_op.c.x_lo == 0:
+            csr = base_op
+        else:
+            return None
+        if self.inv_diag is not None:
+            csr = csr.with_scale(self.inv_diag[self.off:])
+        return csr
 
     # ---------------------------------------------------------------- helpers
     def _vec_with_halo(self):
@@ -261,7 +288,9 @@ class Engine:
         self._call("lsb_scale_div", D.ptr(self.rbuf), self.n,
                    C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_RNORM), self.col_ptr(0), None, -1, st)
         self._call("lsb_cycle_begin", S, st)
-        if self.lagged:
+        if self.persistent:       # iterations 0..m in one cluster launch
+            self._call("lsb_cycle_persistent", S, C.byref(self.pcsr.c), 1, st)
+        elif self.lagged:
             self._lagged_body(st)
         else:
             self._direct_body(st)

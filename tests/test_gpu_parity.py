@@ -761,3 +761,60 @@ def test_c4_512cube_single_gpu_cycle(P):
     # restart residual of the final verification == the implicit one to O(eps kappa)
     assert abs(h.final_true_rel_res - h.implicit_curve()[-1]) <= 1e-6 * h.implicit_curve()[-1]
     h.release()
+
+
+# ------------------------------------------------------------------ persistent cluster cycle
+def _persist_problem(P, kind):
+    if kind == "c1":
+        A = P.gen_laplace2d(64)
+        return A, P.gen_rhs("random", A, 42), 30, 1e-6, {}
+    if kind == "c1_jacobi":
+        A = P.gen_laplace2d(48)
+        return A, P.gen_rhs("random", A, 7), 30, 1e-6, {"precond": "jacobi"}
+    if kind == "conv27_csr":
+        O = orc.convdiff27(14)
+        A = P.CsrMatrix(O.n_rows, O.n_cols, O.row_ptr, O.col_idx, O.values)
+        return A, P.gen_rhs("random", A, 3), 40, 1e-8, {}
+    if kind == "lap3d_18":           # n = 5,832, GMRES(50): 16 CTAs x 365 rows x 52 columns
+        A = P.gen_laplace3d(18)
+        return A, P.gen_rhs("random", A, 5), 50, 1e-6, {}
+    A = P.CsrMatrix.diagonal([2.0, 3.0, 4.0, 5.0])   # happy breakdown inside the cycle
+    return A, np.ones(4), 10, 1e-14, {}
+
+
+@pytest.mark.parametrize("kind", ["c1", "c1_jacobi", "conv27_csr", "lap3d_18", "breakdown"])
+@pytest.mark.parametrize("meth", ["one_sync_mgs", "pipeline2"])
+def test_persistent_cycle_matches_per_iteration_kernels(P, monkeypatch, kind, meth):
+    """lsb_cycle_persistent (one cluster launch per restart cycle) against the
+    per-iteration kernels: same iteration count, outcome, cycle starts and
+    ledger; implicit curve within 1e-10 (only the mdot summation order
+    differs); solutions agree."""
+    from paper_1809_05805_b200.engine import Engine
+    A, b, m, tol, kw = _persist_problem(P, kind)
+    assert Engine(A, m, meth, tol).persistent
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("LSB_PERSISTENT", mode)
+        cfg = P.GmresConfig(restart_m=m, max_restarts=200, rel_tol=tol, method=meth, **kw)
+        led = P.ReductionLedger()
+        x, h = P.solve(A, b, config=cfg, ledger=led, diagnostics_every=0)
+        out[mode] = (x, h, led)
+    (x0, h0, l0), (x1, h1, l1) = out["0"], out["1"]
+    c0, c1 = h0.implicit_curve(), h1.implicit_curve()
+    assert len(c0) == len(c1) and h0.outcome == h1.outcome
+    assert h0.cycle_starts == h1.cycle_starts
+    assert [(e.kind, e.scalar_count, e.iteration) for e in l0.events] == \
+        [(e.kind, e.scalar_count, e.iteration) for e in l1.events]
+    big = c0 > 1e-12 * c0[0]            # below that the curve is rounding noise
+    assert np.max(np.abs(c0 - c1)[big] / c0[big]) <= 1e-10
+    assert np.max(np.abs(c0 - c1)[~big], initial=0.0) <= 1e-14 * c0[0]
+    assert np.linalg.norm(x1 - x0) <= 1e-8 * max(np.linalg.norm(x0), 1e-300)
+
+
+def test_persistent_cycle_is_used_at_launch_bound_sizes(P):
+    from paper_1809_05805_b200.engine import Engine
+    A = P.gen_laplace2d(64)
+    eng = Engine(A, 30, "one_sync_mgs", 1e-6)
+    assert eng.persistent
+    assert not Engine(P.gen_laplace3d(48), 30, "one_sync_mgs", 1e-6).persistent   # n > 2^16
+    assert not Engine(A, 30, "two_sync_cgs2", 1e-6).persistent
