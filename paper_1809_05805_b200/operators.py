@@ -117,6 +117,7 @@ class StencilMatrix:
         self.n_rows = self.n_cols = nx * ny * nz
         self._csr = None
         self._dev = None
+        self._dev_csr = None
 
     # -- CsrMatrix duck typing (materialised lazily, host only)
     def _materialise(self):
@@ -184,7 +185,10 @@ class StencilMatrix:
     def device_csr(self):
         """The same CSR as _materialise(), built directly in device memory
         (int32 indices) and wrapped as a K7 CsrOperator: the CSR form of
-        configs 2/5 at N=256 (450M nonzeros for the 27-point operator)."""
+        configs 2/5 at N=256 (450M nonzeros for the 27-point operator).
+        Built once per matrix and cached."""
+        if self._dev_csr is not None:
+            return self._dev_csr
         dev = D.require_cuda()
         nx, ny, nz = self.dims
         n = self.n_rows
@@ -218,7 +222,8 @@ class StencilMatrix:
             values[pos] = v
             fill[m] += 1
             del r, pos
-        return CsrOperator.from_device(n, n, row_ptr, col_idx, values)
+        self._dev_csr = CsrOperator.from_device(n, n, row_ptr, col_idx, values)
+        return self._dev_csr
 
     def device_op(self):
         if self._dev is None:
