@@ -41,17 +41,13 @@ constexpr int kPMaxCap = 128;       // basis columns (p + 1 <= cap)
 constexpr int kPMaxCluster = 16;
 constexpr size_t kPMaxSmem = 200 * 1024;   // + ~10 KB static <= 227 KB
 
-// Phase timestamps of CTA 0 (tuning knob LSB_TUNE_PERSIST_TRACE, read back
-// with lsb_persist_trace): 6 per iteration, globaltimer ns.
-constexpr int kTraceSlots = 10;
-__device__ long long g_ptrace[kTraceSlots * kPMaxCap];
-__device__ __forceinline__ long long gtimer() {
-  long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define LSB_TRACE(slot, cta) \
-  if (trace && crank == (cta) && tid == 0) g_ptrace[kTraceSlots * i + (slot)] = gtimer();
+// Phase anatomy (tuning knob LSB_TUNE_PERSIST_TRACE, read back with
+// lsb_persist_trace): SM-cycle sums over iterations >= 1 -- [0..4] CTA 1:
+// SpMV+dots, wait at barrier 1, wait at barrier 2 (= CTA 0's gather + small
+// state), K2, wait at barrier 3 (= the fold beyond K2); [5..7] CTA 0:
+// small-state front, T column, c; [8] iterations summed.
+constexpr int kTraceSlots = 16;
+__device__ long long g_ptrace[kTraceSlots];
 
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile(
@@ -102,21 +98,47 @@ struct CsrRowAccCluster {
   }
 };
 
+// The cycle's small state in CTA 0's shared memory: the lsb_arnoldi arrays
+// the K5 code touches, copied in at launch and out at the end, so no global
+// store is outstanding at a cluster barrier (each barrier.cluster.arrive
+// .release would otherwise wait for them to reach L2).
+struct StateLayout {
+  int R, T, tri, rot, g, res, coef, G, scal, flags, total;   // offsets (doubles)
+  __host__ __device__ static StateLayout make(int cap, int m) {
+    StateLayout L{};
+    int o = 0;
+    L.R = o; o += cap * cap;
+    L.T = o; o += cap * cap;
+    L.tri = o; o += (m + 1) * m;
+    L.rot = o; o += 2 * m;
+    L.g = o; o += m + 1;
+    L.res = o; o += m + 1;
+    L.coef = o; o += cap;
+    L.G = o; o += 2 * cap;
+    L.scal = o; o += LSB_S_COUNT;
+    L.flags = o; o += (int)(sizeof(lsb_flags) / sizeof(double));
+    L.total = o;
+    return L;
+  }
+};
+
+__device__ __forceinline__ void copy_d(double* dst, const double* src, int n) {
+  for (int e = threadIdx.x; e < n; e += blockDim.x) dst[e] = src[e];
+}
+
 __global__ void __launch_bounds__(kPT, 1)
-persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, int t_cap,
-                     bool trace) {
+persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, bool trace) {
   cgx::cluster_group cl = cgx::this_cluster();
   const int crank = (int)cl.block_rank(), csize = (int)cl.num_blocks();
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int cap = S.cap;
+  const int cap = S.cap, m = S.m;
+  const StateLayout SL = StateLayout::make(cap, m);
   extern __shared__ __align__(16) double dyn[];
   double* Vs = dyn;                          // cap columns x rows: own rows of V
   double* allp = Vs + (size_t)cap * rows;    // [16][2*cap]: every CTA's [Q^T u, Q^T w]
                                              // (pushed into CTA 0's copy over DSMEM)
-  double* sG = allp + kPMaxCluster * 2 * cap;  // 2*cap: their rank-ordered sum (CTA 0)
-  double* sc = sG + 2 * cap;                 // cap: projection coefficients
-  double* sg = sc + cap;                     // cap: rotated rhs g (CTA 0)
-  double* sT = sg + cap;                     // t_cap^2: T block of the small state
+  double* sc = allp + kPMaxCluster * 2 * cap;  // cap: coefficients (row CTAs' copy)
+  double* st = sc + cap;                     // SL.total: the small state (CTA 0)
   __shared__ SmallShared sh;
   __shared__ double* s_peer[kPMaxCluster];
   // published by CTA 0: [0] beta, [1] K2 skipped (breakdown at this
@@ -124,45 +146,61 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
   // semantics, after the Givens fold) -- before barrier (3)
   __shared__ double s_pub[3];
   __shared__ int s_go;
-  const int64_t ld = S.ld;
   // CTA 0 is the control CTA (reductions, small state, Givens fold) and
   // owns no rows; row block b lives in CTA b + 1
   const int64_t r0 = crank == 0 ? S.n : (int64_t)(crank - 1) * rows;
   const int64_t r1 = min(r0 + (int64_t)rows, S.n);
   const int nr = r1 > r0 ? (int)(r1 - r0) : 0;
-  // own rows of V[:, 0] (= r / beta from lsb_scale_div) into shared memory
-  for (int j = tid; j < nr; j += kPT) Vs[j] = S.V[r0 + j];
+  for (int j = tid; j < nr; j += kPT) Vs[j] = S.V[r0 + j];   // V[:, 0] = r / beta
   if (tid < csize) s_peer[tid] = tid == crank ? Vs : cl.map_shared_rank(Vs, tid);
-  if (crank == 0)
-    for (int e = tid; e <= S.m; e += kPT) sg[e] = S.g[e];
+  lsb_arnoldi L = S;   // CTA 0: the same state, shared-memory resident
+  L.R = st + SL.R;
+  L.T = st + SL.T;
+  L.tri = st + SL.tri;
+  L.rot = st + SL.rot;
+  L.g = st + SL.g;
+  L.res = st + SL.res;
+  L.coef = st + SL.coef;
+  L.G = st + SL.G;
+  L.scal = st + SL.scal;
+  L.flags = reinterpret_cast<lsb_flags*>(st + SL.flags);
+  L.g_parts = 1;
+  if (crank == 0) {
+    copy_d(L.R, S.R, cap * cap);
+    copy_d(L.T, S.T, cap * cap);
+    copy_d(L.tri, S.tri, (m + 1) * m);
+    copy_d(L.rot, S.rot, 2 * m);
+    copy_d(L.g, S.g, m + 1);
+    copy_d(L.res, S.res, m + 1);
+    copy_d(L.coef, S.coef, cap);
+    copy_d(L.scal, S.scal, LSB_S_COUNT);
+    if (tid < (int)(sizeof(lsb_flags) / sizeof(int)))
+      reinterpret_cast<int*>(L.flags)[tid] = reinterpret_cast<const int*>(S.flags)[tid];
+  }
   if (tid == 0) {
-    const int stop = __ldcg(&S.flags->stop_iter), broke = __ldcg(&S.flags->broke_iter);
+    const int stop = S.flags->stop_iter, broke = S.flags->broke_iter;
     s_go = !(stop < 0 || (broke >= 0 && broke < 0));   // gated_off(flags, 0)
   }
   const double* pub0 = cl.map_shared_rank(s_pub, 0);
-  const double* sc0 = cl.map_shared_rank(sc, 0);
+  const double* coef0 = cl.map_shared_rank(st + SL.coef, 0);
   double* allp0 = cl.map_shared_rank(allp, 0) + crank * 2 * cap;   // this CTA's slot at CTA 0
   SmallResident res;
-  res.ldT = t_cap;
   res.resident = true;
-  res.coef = sc;
-  res.G = sG;
-  res.g = sg;
-  res.scal_cached = true;
-  res.btf = S.scal[LSB_S_BTF];
-  res.target = S.scal[LSB_S_TARGET];
+  res.warp_dots = true;
+  long long tr[kTraceSlots] = {0};
+  long long tc = 0;
   bool bad = false;
+  int produced = 1;   // basis columns holding data
   cluster_barrier();
 
-  for (int i = 0; i <= S.m; ++i) {
+  for (int i = 0; i <= m; ++i) {
     const int p = i + 1;
     __syncthreads();
     if (!s_go) break;    // same decision in every CTA (CTA 0's published flag)
+    const bool tw = trace && crank == 1 && tid == 0 && i > 0;
+    if (tw) tc = clock64();
     double* su = Vs + (size_t)(p - 1) * rows;   // u = V[:, p-1], own rows
     double* sw = Vs + (size_t)p * rows;         // w = V[:, p]
-    double* gu = S.V + (int64_t)(p - 1) * ld;
-    double* gw = S.V + (int64_t)p * ld;
-    LSB_TRACE(0, 1)
 
     // ---- w = A u on the own rows (V.push(A v_i), gmres.py:411); u of
     // every row from its owner's shared memory
@@ -174,8 +212,8 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
                                     hi - lo);
       if (!isfinite(s)) bad = true;
       sw[j] = s;
-      gw[r] = s;
     }
+    produced = p + 1;
     __syncthreads();
 
     // ---- partial [Q^T u, Q^T w] of the own rows: warp wid takes columns
@@ -196,39 +234,44 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
         allp0[2 * k + 1] = b;
       }
     }
-    LSB_TRACE(1, 1)
+    if (tw) { const long long t = clock64(); tr[0] += t - tc; tc = t; }
     cluster_barrier();   // (1) every CTA's partials are complete
-    LSB_TRACE(2, 0)
+    if (tw) { const long long t = clock64(); tr[1] += t - tc; tc = t; }
 
     // ---- CTA 0: cluster sum in rank order (the partials already sit in
-    // its shared memory), then the K5 small state, resident in this CTA
-    // for the whole cycle
+    // its shared memory), then the K5 small state -- all of it resident in
+    // this CTA's shared memory for the whole cycle
     if (crank == 0) {
       for (int e = tid; e < 2 * p; e += kPT) {
         double acc = 0.0;
         for (int c = 1; c < csize; ++c) acc += allp[c * 2 * cap + e];
-        sG[e] = acc;
-        S.G[e] = acc;
+        L.G[e] = acc;
       }
       __syncthreads();
-      LSB_TRACE(3, 0)
-      res.trace = trace ? g_ptrace + kTraceSlots * i + 6 : nullptr;
+      long long sm[4];
+      res.trace = (trace && i > 0) ? sm + 1 : nullptr;
+      if (res.trace && tid == 0) sm[0] = clock64();
       // Givens fold deferred (givens_col = -i, the pipeline2 schedule of
       // gmres.py:444-462): it runs below, while the other CTAs apply K2
-      mgs_small_body(S, sh, sT, i, p, ks, -i, p <= t_cap, res);
+      mgs_small_body(L, sh, nullptr, i, p, ks, -i, false, res);
+      if (res.trace && tid == 0 && !sh.broke) {
+        tr[5] += sm[1] - sm[0];
+        tr[6] += sm[2] - sm[1];
+        tr[7] += sm[3] - sm[2];
+      }
       if (tid == 0) {
         s_pub[0] = sh.beta;
         s_pub[1] = sh.broke ? 1.0 : 0.0;
       }
     }
-    LSB_TRACE(4, 0)
     cluster_barrier();   // (2) coef and beta are published
+    if (tw) { const long long t = clock64(); tr[2] += t - tc; tc = t; }
 
     if (crank == 0) {    // fold Hessenberg column i-1 (sh.col) into the Givens state
-      if (i > 0) settle_block(S, sh, i, i, sh.broke, &res);
+      if (i > 0) settle_block(L, sh, i, i, sh.broke, &res);
       __syncthreads();
       if (tid == 0) {
-        const int stop = S.flags->stop_iter, broke = S.flags->broke_iter;
+        const int stop = L.flags->stop_iter, broke = L.flags->broke_iter;
         s_pub[2] = (stop < i + 1 || (broke >= 0 && broke < i + 1)) ? 0.0 : 1.0;
       }
     }
@@ -238,78 +281,94 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
     const double beta = pub0[0];
     const bool skip = pub0[1] != 0.0;
     if (crank != 0)
-      for (int k = tid; k < p; k += kPT) sc[k] = sc0[k];
+      for (int k = tid; k < p; k += kPT) sc[k] = coef0[k];
     __syncthreads();
     if (!skip) {
       const double cu = sc[p - 1];
       for (int j = tid; j < nr; j += kPT) {
-        const int64_t r = r0 + j;
         double acc = 0.0;
         for (int k = 0; k < p - 1; ++k) acc = fma(sc[k], Vs[(size_t)k * rows + j], acc);
         const double uu = __ddiv_rn(su[j], beta);
         su[j] = uu;
-        gu[r] = uu;
         acc = fma(cu, uu, acc);
         double ww = sw[j];
         if (ks) ww = __ddiv_rn(ww, beta);
-        ww = ww - acc;
-        sw[j] = ww;
-        gw[r] = ww;
+        sw[j] = ww - acc;
       }
     }
-    LSB_TRACE(5, 1)
+    if (tw) { const long long t = clock64(); tr[3] += t - tc; tc = t; }
     cluster_barrier();   // (3) the next SpMV reads the updated column; the
                          // fold's stop decision is published
+    if (tw) { const long long t = clock64(); tr[4] += t - tc; tr[8] += 1; }
     if (tid == 0) s_go = pub0[2] != 0.0;
   }
-  if (bad && S.flags) S.flags->nonfinite = 1;
-  // no CTA may exit while a peer can still read its shared memory (s_pub)
+  if (bad) atomicOr(reinterpret_cast<int*>(cl.map_shared_rank(L.flags, 0)) + 4, 1);  // nonfinite
+  // the basis columns this cycle produced, own rows, back to HBM
+  for (int k = 0; k < produced; ++k)
+    for (int j = tid; j < nr; j += kPT) S.V[(int64_t)k * S.ld + r0 + j] = Vs[(size_t)k * rows + j];
+  // no CTA may exit while a peer can still touch its shared memory
   cluster_barrier();
+  if (crank == 0) {    // the small state back to HBM for the cycle epilogue
+    copy_d(S.R, L.R, cap * cap);
+    copy_d(S.T, L.T, cap * cap);
+    copy_d(S.tri, L.tri, (m + 1) * m);
+    copy_d(S.rot, L.rot, 2 * m);
+    copy_d(S.g, L.g, m + 1);
+    copy_d(S.res, L.res, m + 1);
+    copy_d(S.coef, L.coef, cap);
+    copy_d(S.G, L.G, 2 * cap);
+    copy_d(S.scal, L.scal, LSB_S_COUNT);
+    if (tid < (int)(sizeof(lsb_flags) / sizeof(int)))
+      reinterpret_cast<int*>(S.flags)[tid] = reinterpret_cast<const int*>(L.flags)[tid];
+  }
+  if (trace && tid == 0 && (crank == 1 || crank == 0)) {
+    if (crank == 1)
+      for (int k = 0; k < 5; ++k) g_ptrace[k] = tr[k];
+    else
+      for (int k = 5; k < 8; ++k) g_ptrace[k] = tr[k];
+    if (crank == 1) g_ptrace[8] = tr[8];
+  }
 }
 
-// Cluster shape for (n, cap): 16 CTAs at most, ~256 rows each, V's own
-// rows + the T block in shared memory.  Returns the CTA count, 0 if no fit.
-static int persist_plan(int64_t n, int cap, int* rows_out, int* tcap_out, size_t* smem_out) {
-  if (n < 1 || cap < 2 || cap > kPMaxCap || cap > kSmall) return 0;
-  // one control CTA + row CTAs of ~256 rows
+// Cluster shape for (n, cap, m): one control CTA + up to 15 row CTAs of
+// ~256 rows, each CTA holding its rows of all cap basis columns plus the
+// small state in shared memory.  Returns the CTA count, 0 if no fit.
+static int persist_plan(int64_t n, int cap, int m, int* rows_out, size_t* smem_out) {
+  if (n < 1 || cap < 2 || cap > kPMaxCap || cap > kSmall || m + 2 > cap) return 0;
   int csize = 1 + (int)((n + 255) / 256);
   const int forced = tuning(LSB_TUNE_PERSIST_CTAS);
   if (forced >= 2 && forced <= kPMaxCluster) csize = forced;
   if (csize < 2) csize = 2;
   if (csize > kPMaxCluster) csize = kPMaxCluster;
   const int64_t rows = (n + csize - 2) / (csize - 1);
-  const size_t base = sizeof(double) * ((size_t)cap * rows + (2 * kPMaxCluster + 4) * cap);
-  if (base > kPMaxSmem) return 0;
-  int t_cap = 0;             // T block staged while p*p doubles fit
-  while (t_cap < cap - 1 &&
-         base + sizeof(double) * (size_t)(t_cap + 1) * (t_cap + 1) <= kPMaxSmem)
-    ++t_cap;
+  const size_t smem = sizeof(double) * ((size_t)cap * rows + (2 * kPMaxCluster + 1) * cap +
+                                        StateLayout::make(cap, m).total);
+  if (smem > kPMaxSmem) return 0;
   *rows_out = (int)rows;
-  *tcap_out = t_cap;
-  *smem_out = base + sizeof(double) * (size_t)t_cap * t_cap;
+  *smem_out = smem;
   return csize;
 }
 
 int persist_trace(long long* out, int count) {
-  if (count > kTraceSlots * kPMaxCap) count = kTraceSlots * kPMaxCap;
+  if (count > kTraceSlots) count = kTraceSlots;
   if (cudaMemcpyFromSymbol(out, g_ptrace, sizeof(long long) * count) != cudaSuccess)
     return check_launch("persist_trace");
   return LSB_OK;
 }
 
 int persist_fits(int64_t n, int cap) {
-  int rows, tc;
+  int rows;
   size_t sm;
-  return persist_plan(n, cap, &rows, &tc, &sm) > 0;
+  return persist_plan(n, cap, cap - 2, &rows, &sm) > 0;
 }
 
 int launch_cycle_persistent(const lsb_arnoldi& S, const lsb_csr* A, int ks, cudaStream_t st) {
   if (!A || S.g_parts != 1 || S.m + 2 > S.cap || A->n_rows != S.n || A->n_cols != S.n ||
       A->x_lo != 0 || A->nnz >= (1LL << 31))
     return LSB_ERANGE;
-  int rows = 0, t_cap = 0;
+  int rows = 0;
   size_t smem = 0;
-  const int csize = persist_plan(S.n, S.cap, &rows, &t_cap, &smem);
+  const int csize = persist_plan(S.n, S.cap, S.m, &rows, &smem);
   if (!csize) return LSB_ERANGE;
   static bool attr = false;
   if (!attr) {
@@ -333,7 +392,7 @@ int launch_cycle_persistent(const lsb_arnoldi& S, const lsb_csr* A, int ks, cuda
   const lsb_csr Av = *A;
   const bool trace = tuning(LSB_TUNE_PERSIST_TRACE) == 1;
   cudaLaunchKernelEx(&cfg, persist_cycle_kernel, S, Av, rows, FastDiv::make((uint32_t)rows), ks,
-                     t_cap, trace);
+                     trace);
   return check_launch("cycle_persistent");
 }
 

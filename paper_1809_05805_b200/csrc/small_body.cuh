@@ -39,9 +39,7 @@ struct SmallResident {
 
 __device__ __forceinline__ void small_stamp(const SmallResident* rs, int k) {
   if (rs && rs->trace && threadIdx.x == 0) {
-    long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    rs->trace[k] = t;
+    rs->trace[k] = clock64();   // SM cycles (CTA 0 only)
   }
 }
 
@@ -73,7 +71,6 @@ __device__ inline void settle_block(const lsb_arnoldi& S, SmallShared& sh, int i
   if (!(rs && rs->resident))
     for (int e = t; e < 2 * (gc - 1); e += blockDim.x) sh.rot[e] = S.rot[e];
   __syncthreads();
-  small_stamp(rs, 3);
   if (t == 0) {
     double* g = rs && rs->g ? rs->g : S.g;
     const double res = givens_fold(sh.col, sh.rot, g, gc);
@@ -165,14 +162,15 @@ __device__ inline void mgs_small_body(const lsb_arnoldi& S, SmallShared& sh, dou
   for (int e = t; e < p - 1; e += blockDim.x) sh.a[e] = __ddiv_rn(sh.a[e], beta);
   if (t == 0) sh.y[p - 1] = __ddiv_rn(sh.y[p - 1], beta);
   __syncthreads();
-  if (rs.warp_dots && st) {   // one warp per row j, lanes over l, butterfly sum
+  if (rs.warp_dots) {   // one warp per row j, lanes over l, butterfly sum
     const int lane = t & 31, nw = blockDim.x >> 5;
     for (int j = t >> 5; j < p - 1; j += nw) {
       double acc = 0.0;
-      for (int l = j + lane; l < p - 1; l += 32) acc = fma(sT[j * lt + l], sh.a[l], acc);
+      for (int l = j + lane; l < p - 1; l += 32)
+        acc = fma(st ? sT[j * lt + l] : S.T[(int64_t)j * cap + l], sh.a[l], acc);
       acc = warp_sum(acc);
       if (lane == 0) {
-        sT[j * lt + (p - 1)] = -acc;
+        if (st) sT[j * lt + (p - 1)] = -acc;
         S.T[(int64_t)j * cap + (p - 1)] = -acc;
       }
     }
@@ -198,11 +196,12 @@ __device__ inline void mgs_small_body(const lsb_arnoldi& S, SmallShared& sh, dou
   __syncthreads();
   small_stamp(&rs, 1);
   // c = T[:p,:p]^T y  (/beta);  R[:p, p] = c
-  if (rs.warp_dots && st) {
+  if (rs.warp_dots) {
     const int lane = t & 31, nw = blockDim.x >> 5;
     for (int j = t >> 5; j < p; j += nw) {
       double acc = 0.0;
-      for (int l = lane; l <= j; l += 32) acc = fma(sT[l * lt + j], sh.y[l], acc);
+      for (int l = lane; l <= j; l += 32)
+        acc = fma(st ? sT[l * lt + j] : S.T[(int64_t)l * cap + j], sh.y[l], acc);
       acc = warp_sum(acc);
       if (lane == 0) {
         if (ks) acc = __ddiv_rn(acc, beta);

@@ -775,14 +775,14 @@ def _persist_problem(P, kind):
         O = orc.convdiff27(14)
         A = P.CsrMatrix(O.n_rows, O.n_cols, O.row_ptr, O.col_idx, O.values)
         return A, P.gen_rhs("random", A, 3), 40, 1e-8, {}
-    if kind == "lap3d_18":           # n = 5,832, GMRES(50): 16 CTAs x 365 rows x 52 columns
-        A = P.gen_laplace3d(18)
+    if kind == "lap3d_15":           # n = 3,375, GMRES(50): 15 row CTAs x 225 rows x 52 columns
+        A = P.gen_laplace3d(15)
         return A, P.gen_rhs("random", A, 5), 50, 1e-6, {}
     A = P.CsrMatrix.diagonal([2.0, 3.0, 4.0, 5.0])   # happy breakdown inside the cycle
     return A, np.ones(4), 10, 1e-14, {}
 
 
-@pytest.mark.parametrize("kind", ["c1", "c1_jacobi", "conv27_csr", "lap3d_18", "breakdown"])
+@pytest.mark.parametrize("kind", ["c1", "c1_jacobi", "conv27_csr", "lap3d_15", "breakdown"])
 @pytest.mark.parametrize("meth", ["one_sync_mgs", "pipeline2"])
 def test_persistent_cycle_matches_per_iteration_kernels(P, monkeypatch, kind, meth):
     """lsb_cycle_persistent (one cluster launch per restart cycle) against the

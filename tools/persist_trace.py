@@ -39,22 +39,14 @@ def main():
     eng.cycle()
     torch.cuda.synchronize()
     lib.lsb_set_tuning(_abi.TUNE_PERSIST_TRACE, 0)
-    n = 10 * (a.m + 1)
-    buf = (C.c_int64 * n)()
-    _abi.call("lsb_persist_trace", buf, n)
-    t = np.array(buf, dtype=np.float64).reshape(a.m + 1, 10)
-    names = ["spmv+dots", "barrier1", "gather", "small", "k2", "barrier3+gate"]
-    d = np.zeros((a.m, 6))
-    for i in range(a.m):
-        seg = [t[i, 1] - t[i, 0], t[i, 2] - t[i, 1], t[i, 3] - t[i, 2], t[i, 4] - t[i, 3],
-               t[i, 5] - t[i, 4], t[i + 1, 0] - t[i, 5]]
-        d[i] = seg
-    print("mean ns per iteration:", {k: round(float(v), 1) for k, v in zip(names, d[1:].mean(0))})
-    print("total us per iteration:", round(float(d[1:].sum(1).mean()) / 1e3, 2))
-    sm = np.stack([t[2:a.m, 6] - t[2:a.m, 3], t[2:a.m, 7] - t[2:a.m, 6], t[2:a.m, 8] - t[2:a.m, 7],
-                   t[2:a.m, 9] - t[2:a.m, 8], t[2:a.m, 4] - t[2:a.m, 9]], 1)
-    print("small-state split ns (front, T col, c, settle sync, givens+tail):",
-          [round(float(v), 1) for v in sm.mean(0)])
+    buf = (C.c_int64 * 16)()
+    _abi.call("lsb_persist_trace", buf, 16)
+    t = np.array(buf, dtype=np.float64)
+    its = max(t[8], 1)
+    names = ["row CTA: spmv+dots", "wait b1", "wait b2 (gather+small)", "K2", "wait b3 (fold)",
+             "ctl: front", "ctl: T col", "ctl: c"]
+    print("mean SM cycles per iteration:", {k: round(float(v) / its, 1) for k, v in zip(names, t[:8])})
+    print("row-CTA total cycles per iteration:", round(float(t[:5].sum()) / its, 1))
 
 
 if __name__ == "__main__":
