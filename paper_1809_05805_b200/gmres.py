@@ -304,6 +304,8 @@ class _DeviceSolve:
         self.engine = eng
         self._mark("engine")
         eng.load(self.b, self.x0)
+        # the host result buffer is faulted in while the device iterates
+        self._xhost = D.HostBuffer(eng.n) if self.host and eng.n >= D._STAGE_MIN else None
         led.iteration = 0
         rep = eng.prologue()
         self._mark("prologue")
@@ -444,7 +446,8 @@ class _DeviceSolve:
 
     def _result(self, eng):
         x = eng.x_view().clone()
-        out = D.out_like(x, self.host), self.history
+        hb = getattr(self, "_xhost", None)
+        out = D.out_like(x, self.host, hb), self.history
         self._mark("result")
         if self._trace is not None:
             import sys
