@@ -126,6 +126,92 @@ __device__ __forceinline__ void copy_d(double* dst, const double* src, int n) {
   for (int e = threadIdx.x; e < n; e += blockDim.x) dst[e] = src[e];
 }
 
+// K5 of the control CTA (gram_schmidt.py:226-245 with krylov_scale; the
+// Givens fold is deferred), arranged for latency: warp 0 runs the breakdown
+// test (beta, ||R[:p-1,p-1]||, CPython hypot -- gram_schmidt.py:96-106)
+// while warps 1..15 speculatively compute the new T column and
+// c = T^T y / beta; the results are committed only if the column did not
+// break down.  Same arithmetic (and the same warp-tree sums) as
+// mgs_small_body with SmallResident::warp_dots, so the bits do not change.
+// scratch: 2*cap doubles.
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ void persist_small(const lsb_arnoldi& L, SmallShared& sh, double* scratch, int it,
+                              int p, int ks, long long* stamps) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, cap = L.cap;
+  constexpr int kW = kPT / 32 - 1;          // speculating warps
+  double* Tnew = scratch;                    // T[:p, p-1]
+  double* cnew = scratch + cap;              // c
+  for (int e = t; e < p; e += kPT) {
+    sh.a[e] = L.G[2 * e];
+    sh.y[e] = L.G[2 * e + 1];
+    if (e < p - 1) sh.col[e] = L.R[(int64_t)e * cap + (p - 1)];
+  }
+  __syncthreads();
+  if (stamps && t == 0) stamps[0] = clock64();
+  const double bsq = sh.a[p - 1];
+  const double beta = bsq > 0.0 ? sqrt(bsq) : 0.0;
+  if (wid == 0) {
+    // ---- breakdown test (lagged_front)
+    double ss = 0.0;
+    for (int j = lane; j < p - 1; j += 32) ss = fma(sh.col[j], sh.col[j], ss);
+    ss = warp_sum(ss);
+    if (lane == 0) {
+      const double tol = breakdown_tol(L, beta, sh.col, p - 1, nullptr, ss);
+      sh.beta = beta;
+      sh.tol = tol;
+      sh.broke = beta <= tol;
+      L.scal[LSB_S_BETA] = beta;
+      L.scal[LSB_S_TOL] = tol;
+      if (sh.broke) {
+        L.flags->broke_iter = it;
+        if (it == 0) { L.flags->stop_iter = it; L.flags->status = LSB_STARTUP_BREAKDOWN; }
+        sh.col[p - 1] = 0.0;
+      } else {
+        sh.col[p - 1] = beta;
+        L.R[(int64_t)(p - 1) * cap + (p - 1)] = beta;
+      }
+    }
+  } else {
+    // ---- speculative T column and c (mgs_small_body)
+    const int u = t - 32;                    // 0 .. 32*kW-1
+    for (int e = u; e < p - 1; e += 32 * kW) sh.a[e] = __ddiv_rn(sh.a[e], beta);
+    const double ylast = __ddiv_rn(sh.y[p - 1], beta);
+    named_bar(1, 32 * kW);
+    if (stamps && t == 32) stamps[1] = clock64();
+    for (int j = wid - 1; j < p - 1; j += kW) {
+      double acc = 0.0;
+      for (int l = j + lane; l < p - 1; l += 32) acc = fma(L.T[(int64_t)j * cap + l], sh.a[l], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) Tnew[j] = -acc;
+    }
+    if (u == 0) Tnew[p - 1] = 1.0;
+    named_bar(1, 32 * kW);
+    if (stamps && t == 32) stamps[2] = clock64();
+    for (int j = wid - 1; j < p; j += kW) {
+      double acc = 0.0;
+      for (int l = lane; l <= j; l += 32) {
+        const double tl = j == p - 1 ? Tnew[l] : L.T[(int64_t)l * cap + j];
+        acc = fma(tl, l == p - 1 ? ylast : sh.y[l], acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) cnew[j] = ks ? __ddiv_rn(acc, beta) : acc;
+    }
+  }
+  __syncthreads();
+  if (stamps && t == 0) stamps[3] = clock64();
+  if (!sh.broke) {                           // commit
+    for (int j = t; j < p; j += kPT) {
+      L.T[(int64_t)j * cap + (p - 1)] = Tnew[j];
+      L.coef[j] = cnew[j];
+      L.R[(int64_t)j * cap + p] = cnew[j];
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kPT, 1)
 persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, bool trace) {
   cgx::cluster_group cl = cgx::this_cluster();
@@ -139,6 +225,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, b
                                              // (pushed into CTA 0's copy over DSMEM)
   double* sc = allp + kPMaxCluster * 2 * cap;  // cap: coefficients (row CTAs' copy)
   double* st = sc + cap;                     // SL.total: the small state (CTA 0)
+  double* scratch = st + SL.total;           // 2*cap: speculative T column and c (CTA 0)
   __shared__ SmallShared sh;
   __shared__ double* s_peer[kPMaxCluster];
   // published by CTA 0: [0] beta, [1] K2 skipped (breakdown at this
@@ -248,13 +335,11 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, b
         L.G[e] = acc;
       }
       __syncthreads();
-      long long sm[4];
-      res.trace = (trace && i > 0) ? sm + 1 : nullptr;
-      if (res.trace && tid == 0) sm[0] = clock64();
+      __shared__ long long sm[4];
       // Givens fold deferred (givens_col = -i, the pipeline2 schedule of
       // gmres.py:444-462): it runs below, while the other CTAs apply K2
-      mgs_small_body(L, sh, nullptr, i, p, ks, -i, false, res);
-      if (res.trace && tid == 0 && !sh.broke) {
+      persist_small(L, sh, scratch, i, p, ks, (trace && i > 0) ? sm : nullptr);
+      if (trace && i > 0 && tid == 0 && !sh.broke) {
         tr[5] += sm[1] - sm[0];
         tr[6] += sm[2] - sm[1];
         tr[7] += sm[3] - sm[2];
@@ -341,7 +426,7 @@ static int persist_plan(int64_t n, int cap, int m, int* rows_out, size_t* smem_o
   if (csize < 2) csize = 2;
   if (csize > kPMaxCluster) csize = kPMaxCluster;
   const int64_t rows = (n + csize - 2) / (csize - 1);
-  const size_t smem = sizeof(double) * ((size_t)cap * rows + (2 * kPMaxCluster + 1) * cap +
+  const size_t smem = sizeof(double) * ((size_t)cap * rows + (2 * kPMaxCluster + 3) * cap +
                                         StateLayout::make(cap, m).total);
   if (smem > kPMaxSmem) return 0;
   *rows_out = (int)rows;

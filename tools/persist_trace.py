@@ -44,7 +44,7 @@ def main():
     t = np.array(buf, dtype=np.float64)
     its = max(t[8], 1)
     names = ["row CTA: spmv+dots", "wait b1", "wait b2 (gather+small)", "K2", "wait b3 (fold)",
-             "ctl: front", "ctl: T col", "ctl: c"]
+             "ctl: a/beta", "ctl: T col", "ctl: c + join"]
     print("mean SM cycles per iteration:", {k: round(float(v) / its, 1) for k, v in zip(names, t[:8])})
     print("row-CTA total cycles per iteration:", round(float(t[:5].sum()) / its, 1))
 
