@@ -197,6 +197,37 @@ __device__ __forceinline__ double box27_dispatch(int state, const Gx& g, const C
   }
 }
 
+// Two x-consecutive rows (ix even) of the 27-point box from the 9 (dz, dy)
+// lines around them, v[l][0..3] = x[ix-1 .. ix+2] of line l = (dz+1)*3 +
+// (dy+1).  Rows with both x neighbours share one plan (switch on the y/z
+// state); x-edge pairs take the per-row dispatch.
+template <int SY, int SZ, class Cf>
+__device__ __forceinline__ void box27_pair_row(const double (&v)[9][4], const Cf& cf, double& y0,
+                                               double& y1) {
+  y0 = box27_row<3, SY, SZ>([&](int o) { return v[o / 3][o % 3]; }, cf);
+  y1 = box27_row<3, SY, SZ>([&](int o) { return v[o / 3][o % 3 + 1]; }, cf);
+}
+
+template <class Cf>
+__device__ __forceinline__ void box27_pair(const double (&v)[9][4], int sy, int sz, bool xm,
+                                           bool xp, const Cf& cf, double& y0, double& y1) {
+  if (xm && xp) {
+    switch (sy | (sz << 2)) {
+#define LSB_P27(k) case k: box27_pair_row<((k) & 3), ((k) >> 2)>(v, cf, y0, y1); break;
+      LSB_P27(0) LSB_P27(1) LSB_P27(2) LSB_P27(3) LSB_P27(4) LSB_P27(5) LSB_P27(6)
+      LSB_P27(7) LSB_P27(8) LSB_P27(9) LSB_P27(10) LSB_P27(11) LSB_P27(12) LSB_P27(13)
+      LSB_P27(14)
+#undef LSB_P27
+      default: box27_pair_row<3, 3>(v, cf, y0, y1); break;
+    }
+  } else {
+    const int s0 = (xm ? 1 : 0) | 2 | (sy << 2) | (sz << 4);
+    const int s1 = 1 | (xp ? 2 : 0) | (sy << 2) | (sz << 4);
+    y0 = box27_dispatch(s0, [&](int o) { return v[o / 3][o % 3]; }, cf);
+    y1 = box27_dispatch(s1, [&](int o) { return v[o / 3][o % 3 + 1]; }, cf);
+  }
+}
+
 // ---------------------------------------------------------------- CPython hypot
 // math.hypot(a, b) of CPython 3.12 (Modules/mathmodule.c vector_norm):
 // lossless scaling to [0.5, 1), double-length squares and sums, one

@@ -149,13 +149,6 @@ __device__ __forceinline__ void load27_pair(const double* __restrict__ x, int64_
   }
 }
 
-template <int SY, int SZ, class Cf>
-__device__ __forceinline__ void box27_pair_row(const double (&v)[9][4], const Cf& cf, double& y0,
-                                               double& y1) {
-  y0 = box27_row<3, SY, SZ>([&](int o) { return v[o / 3][o % 3]; }, cf);
-  y1 = box27_row<3, SY, SZ>([&](int o) { return v[o / 3][o % 3 + 1]; }, cf);
-}
-
 __global__ void __launch_bounds__(256)
 stencil27_pair_kernel(const StencilK K, FastDiv fint, const double* __restrict__ x,
                       const double* __restrict__ b, double* __restrict__ y, lsb_flags* flags,
@@ -187,21 +180,7 @@ stencil27_pair_kernel(const StencilK K, FastDiv fint, const double* __restrict__
     double v[9][4];
     load27_pair(x, r, nx, plane, sy, sz, xm, xp, v);
     double y0, y1;
-    if (xm && xp) {     // both rows interior in x: one plan for the pair
-      switch (sy | (sz << 2)) {
-#define LSB_P27(k) case k: box27_pair_row<((k) & 3), ((k) >> 2)>(v, cf, y0, y1); break;
-        LSB_P27(0) LSB_P27(1) LSB_P27(2) LSB_P27(3) LSB_P27(4) LSB_P27(5) LSB_P27(6)
-        LSB_P27(7) LSB_P27(8) LSB_P27(9) LSB_P27(10) LSB_P27(11) LSB_P27(12) LSB_P27(13)
-        LSB_P27(14)
-#undef LSB_P27
-        default: box27_pair_row<3, 3>(v, cf, y0, y1); break;
-      }
-    } else {
-      const int s0 = (xm ? 1 : 0) | 2 | (sy << 2) | (sz << 4);
-      const int s1 = 1 | (xp ? 2 : 0) | (sy << 2) | (sz << 4);
-      y0 = box27_dispatch(s0, [&](int o) { return v[o / 3][o % 3]; }, cf);
-      y1 = box27_dispatch(s1, [&](int o) { return v[o / 3][o % 3 + 1]; }, cf);
-    }
+    box27_pair(v, sy, sz, xm, xp, cf, y0, y1);
     if (!isfinite(y0) || !isfinite(y1)) bad = true;
     double2 out;
     if (b) {
