@@ -89,12 +89,14 @@ struct CsrRowAccCluster {
   size_t coloff;         // column offset inside a block
   FastDiv rdiv;          // division by rows per CTA
   int rows;
+  // col / val: this CTA's nonzeros staged in shared memory at launch, or
+  // the global arrays (plain loads: the pointers may be either)
   __device__ double operator()(int64_t j) const {
-    const uint32_t c = (uint32_t)__ldg(col + j);
+    const uint32_t c = (uint32_t)col[j];
     const uint32_t blk = rdiv.div(c);            // row block; owned by CTA blk + 1
     double xv = peer[blk + 1][coloff + (c - blk * (uint32_t)rows)];
     if (d) xv = __dmul_rn(xv, __ldg(d + c));
-    return __dmul_rn(__ldg(val + j), xv);
+    return __dmul_rn(val[j], xv);
   }
 };
 
@@ -213,7 +215,8 @@ __device__ void persist_small(const lsb_arnoldi& L, SmallShared& sh, double* scr
 }
 
 __global__ void __launch_bounds__(kPT, 1)
-persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, bool trace) {
+persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, int stage_cap,
+                     bool trace) {
   cgx::cluster_group cl = cgx::this_cluster();
   const int crank = (int)cl.block_rank(), csize = (int)cl.num_blocks();
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -226,6 +229,9 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, b
   double* sc = allp + kPMaxCluster * 2 * cap;  // cap: coefficients (row CTAs' copy)
   double* st = sc + cap;                     // SL.total: the small state (CTA 0)
   double* scratch = st + SL.total;           // 2*cap: speculative T column and c (CTA 0)
+  double* cval = scratch + 2 * cap;          // stage_cap: this CTA's CSR values
+  int32_t* ccol = reinterpret_cast<int32_t*>(cval + stage_cap);   // stage_cap: columns
+  int32_t* crp = ccol + stage_cap;           // rows + 1: row offsets into them
   __shared__ SmallShared sh;
   __shared__ double* s_peer[kPMaxCluster];
   // published by CTA 0: [0] beta, [1] K2 skipped (breakdown at this
@@ -239,6 +245,23 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, b
   const int64_t r1 = min(r0 + (int64_t)rows, S.n);
   const int nr = r1 > r0 ? (int)(r1 - r0) : 0;
   for (int j = tid; j < nr; j += kPT) Vs[j] = S.V[r0 + j];   // V[:, 0] = r / beta
+  // the CTA's CSR rows into shared memory when they fit (read every iteration)
+  const int64_t blo = nr ? A.row_ptr[r0] : 0, bhi = nr ? A.row_ptr[r0 + nr] : 0;
+  const bool cstaged = bhi - blo <= stage_cap;
+  const int32_t* rowp = A.row_ptr;
+  const int32_t* colp = A.col_idx;
+  const double* valp = A.values;
+  if (cstaged) {
+    for (int64_t e = tid; e < bhi - blo; e += kPT) {
+      cval[e] = A.values[blo + e];
+      ccol[e] = A.col_idx[blo + e];
+    }
+    for (int j = tid; j <= nr; j += kPT) crp[j] = (int32_t)(A.row_ptr[r0 + j] - blo);
+    rowp = crp;
+    colp = ccol;
+    valp = cval;
+  }
+  const int64_t rbase = cstaged ? 0 : r0;    // row index base into rowp
   if (tid < csize) s_peer[tid] = tid == crank ? Vs : cl.map_shared_rank(Vs, tid);
   lsb_arnoldi L = S;   // CTA 0: the same state, shared-memory resident
   L.R = st + SL.R;
@@ -292,16 +315,17 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, b
     // ---- w = A u on the own rows (V.push(A v_i), gmres.py:411); u of
     // every row from its owner's shared memory
     for (int j = tid; j < nr; j += kPT) {
-      const int64_t r = r0 + j;
-      const int lo = __ldg(A.row_ptr + r), hi = __ldg(A.row_ptr + r + 1);
-      const double s = row_sum_fast(CsrRowAccCluster{A.col_idx + lo, A.values + lo, A.col_scale,
+      const int lo = rowp[rbase + j], hi = rowp[rbase + j + 1];
+      const double s = row_sum_fast(CsrRowAccCluster{colp + lo, valp + lo, A.col_scale,
                                                      s_peer, (size_t)(p - 1) * rows, rdiv, rows},
                                     hi - lo);
       if (!isfinite(s)) bad = true;
       sw[j] = s;
     }
     produced = p + 1;
+    if (tw) { const long long t = clock64(); tr[9] += t - tc; }
     __syncthreads();
+    if (tw) { const long long t = clock64(); tr[10] += t - tc; }
 
     // ---- partial [Q^T u, Q^T w] of the own rows: warp wid takes columns
     // wid, wid + 16, ...; lanes stride the rows
@@ -407,8 +431,11 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, b
       reinterpret_cast<int*>(S.flags)[tid] = reinterpret_cast<const int*>(L.flags)[tid];
   }
   if (trace && tid == 0 && (crank == 1 || crank == 0)) {
-    if (crank == 1)
+    if (crank == 1) {
       for (int k = 0; k < 5; ++k) g_ptrace[k] = tr[k];
+      g_ptrace[9] = tr[9];
+      g_ptrace[10] = tr[10];
+    }
     else
       for (int k = 5; k < 8; ++k) g_ptrace[k] = tr[k];
     if (crank == 1) g_ptrace[8] = tr[8];
@@ -418,7 +445,8 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, b
 // Cluster shape for (n, cap, m): one control CTA + up to 15 row CTAs of
 // ~256 rows, each CTA holding its rows of all cap basis columns plus the
 // small state in shared memory.  Returns the CTA count, 0 if no fit.
-static int persist_plan(int64_t n, int cap, int m, int* rows_out, size_t* smem_out) {
+static int persist_plan(int64_t n, int cap, int m, int* rows_out, size_t* smem_out,
+                        int* stage_out = nullptr) {
   if (n < 1 || cap < 2 || cap > kPMaxCap || cap > kSmall || m + 2 > cap) return 0;
   int csize = 1 + (int)((n + 255) / 256);
   const int forced = tuning(LSB_TUNE_PERSIST_CTAS);
@@ -429,8 +457,13 @@ static int persist_plan(int64_t n, int cap, int m, int* rows_out, size_t* smem_o
   const size_t smem = sizeof(double) * ((size_t)cap * rows + (2 * kPMaxCluster + 3) * cap +
                                         StateLayout::make(cap, m).total);
   if (smem > kPMaxSmem) return 0;
+  // what is left stages the CTA's CSR rows (12 B per nonzero + row offsets)
+  int64_t stage = ((int64_t)kPMaxSmem - (int64_t)smem - 4 * (rows + 2)) / 12;
+  stage = stage < 0 ? 0 : (stage > (1 << 20) ? (1 << 20) : stage);
+  stage &= ~(int64_t)1;                      // keeps the int32 arrays 8-byte aligned
   *rows_out = (int)rows;
-  *smem_out = smem;
+  *smem_out = smem + 12 * (size_t)stage + 4 * (size_t)(rows + 2);
+  if (stage_out) *stage_out = (int)stage;
   return csize;
 }
 
@@ -451,9 +484,9 @@ int launch_cycle_persistent(const lsb_arnoldi& S, const lsb_csr* A, int ks, cuda
   if (!A || S.g_parts != 1 || S.m + 2 > S.cap || A->n_rows != S.n || A->n_cols != S.n ||
       A->x_lo != 0 || A->nnz >= (1LL << 31))
     return LSB_ERANGE;
-  int rows = 0;
+  int rows = 0, stage = 0;
   size_t smem = 0;
-  const int csize = persist_plan(S.n, S.cap, S.m, &rows, &smem);
+  const int csize = persist_plan(S.n, S.cap, S.m, &rows, &smem, &stage);
   if (!csize) return LSB_ERANGE;
   static bool attr = false;
   if (!attr) {
@@ -477,7 +510,7 @@ int launch_cycle_persistent(const lsb_arnoldi& S, const lsb_csr* A, int ks, cuda
   const lsb_csr Av = *A;
   const bool trace = tuning(LSB_TUNE_PERSIST_TRACE) == 1;
   cudaLaunchKernelEx(&cfg, persist_cycle_kernel, S, Av, rows, FastDiv::make((uint32_t)rows), ks,
-                     trace);
+                     stage, trace);
   return check_launch("cycle_persistent");
 }
 
