@@ -14,7 +14,9 @@
 //   -> cluster barrier; CTA 0 sums the partials of all CTAs in rank order
 //      over DSMEM and runs the K5 small state (mgs_small_body: beta,
 //      breakdown test, T column, c = T^T y, Hessenberg column, Givens)
-//   -> cluster barrier; every CTA applies the K2 row update to its rows
+//   -> cluster barrier; every row CTA applies the K2 row update to its rows
+//      while the control CTA folds the Givens rotation (it arrives at the
+//      next barrier first, so the fold also overlaps the next SpMV)
 //   -> cluster barrier (the next SpMV reads the updated column).
 // Three cluster barriers per iteration replace four kernel launches and
 // three grid-wide last-CTA reductions.  Barriers are release/acquire at
@@ -53,6 +55,12 @@ __device__ __forceinline__ void cluster_barrier() {
   asm volatile(
       "barrier.cluster.arrive.release.aligned;\n\t"
       "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // Row sum in numpy's order with every product load issued before the first
@@ -234,11 +242,11 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
   int32_t* crp = ccol + stage_cap;           // rows + 1: row offsets into them
   __shared__ SmallShared sh;
   __shared__ double* s_peer[kPMaxCluster];
-  // published by CTA 0: [0] beta, [1] K2 skipped (breakdown at this
-  // iteration) -- before barrier (2); [2] next iteration runs (gated_off
-  // semantics, after the Givens fold) -- before barrier (3)
+  // published by CTA 0 before barrier (2): [0] beta, [1] breakdown at this
+  // iteration (K2 skipped, cycle over), [2] this iteration runs (0 when the
+  // previous iteration's deferred Givens fold stopped the cycle)
   __shared__ double s_pub[3];
-  __shared__ int s_go;
+  __shared__ int s_go, s_stop;
   // CTA 0 is the control CTA (reductions, small state, Givens fold) and
   // owns no rows; row block b lives in CTA b + 1
   const int64_t r0 = crank == 0 ? S.n : (int64_t)(crank - 1) * rows;
@@ -290,6 +298,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
   if (tid == 0) {
     const int stop = S.flags->stop_iter, broke = S.flags->broke_iter;
     s_go = !(stop < 0 || (broke >= 0 && broke < 0));   // gated_off(flags, 0)
+    s_stop = 0;
   }
   const double* pub0 = cl.map_shared_rank(s_pub, 0);
   const double* coef0 = cl.map_shared_rank(st + SL.coef, 0);
@@ -300,13 +309,13 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
   long long tr[kTraceSlots] = {0};
   long long tc = 0;
   bool bad = false;
-  int produced = 1;   // basis columns holding data
+  int produced = 1;   // basis columns holding data (row CTAs)
   cluster_barrier();
 
   for (int i = 0; i <= m; ++i) {
     const int p = i + 1;
     __syncthreads();
-    if (!s_go) break;    // same decision in every CTA (CTA 0's published flag)
+    if (!s_go) break;    // the cycle was stopped before it began (same in every CTA)
     const bool tw = trace && crank == 1 && tid == 0 && i > 0;
     if (tw) tc = clock64();
     double* su = Vs + (size_t)(p - 1) * rows;   // u = V[:, p-1], own rows
@@ -322,7 +331,6 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
       if (!isfinite(s)) bad = true;
       sw[j] = s;
     }
-    produced = p + 1;
     if (tw) { const long long t = clock64(); tr[9] += t - tc; }
     __syncthreads();
     if (tw) { const long long t = clock64(); tr[10] += t - tc; }
@@ -351,48 +359,65 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
 
     // ---- CTA 0: cluster sum in rank order (the partials already sit in
     // its shared memory), then the K5 small state -- all of it resident in
-    // this CTA's shared memory for the whole cycle
+    // this CTA's shared memory for the whole cycle.  Unless the previous
+    // iteration's Givens fold stopped the cycle: then this iteration never
+    // happened (its SpMV touched only the shared copy of a column that is
+    // not written back).
+    const bool tc0 = trace && crank == 0 && tid == 0 && i > 0;
+    long long c0a = 0;
+    if (tc0) c0a = clock64();
     if (crank == 0) {
-      for (int e = tid; e < 2 * p; e += kPT) {
-        double acc = 0.0;
-        for (int c = 1; c < csize; ++c) acc += allp[c * 2 * cap + e];
-        L.G[e] = acc;
-      }
-      __syncthreads();
-      __shared__ long long sm[4];
-      // Givens fold deferred (givens_col = -i, the pipeline2 schedule of
-      // gmres.py:444-462): it runs below, while the other CTAs apply K2
-      persist_small(L, sh, scratch, i, p, ks, (trace && i > 0) ? sm : nullptr);
-      if (trace && i > 0 && tid == 0 && !sh.broke) {
-        tr[5] += sm[1] - sm[0];
-        tr[6] += sm[2] - sm[1];
-        tr[7] += sm[3] - sm[2];
+      if (!s_stop) {
+        for (int e = tid; e < 2 * p; e += kPT) {
+          double acc = 0.0;
+          for (int c = 1; c < csize; ++c) acc += allp[c * 2 * cap + e];
+          L.G[e] = acc;
+        }
+        __syncthreads();
+        if (tc0) { const long long t = clock64(); tr[14] += t - c0a; }
+        __shared__ long long sm[4];
+        persist_small(L, sh, scratch, i, p, ks, (trace && i > 0) ? sm : nullptr);
+        if (tc0) { const long long t = clock64(); tr[15] += t - c0a; }
+        if (trace && i > 0 && tid == 0 && !sh.broke) {
+          tr[5] += sm[1] - sm[0];
+          tr[6] += sm[2] - sm[1];
+          tr[7] += sm[3] - sm[2];
+        }
       }
       if (tid == 0) {
         s_pub[0] = sh.beta;
         s_pub[1] = sh.broke ? 1.0 : 0.0;
+        s_pub[2] = s_stop ? 0.0 : 1.0;
       }
     }
-    cluster_barrier();   // (2) coef and beta are published
+    if (tc0) { const long long t = clock64(); tr[11] += t - c0a; c0a = t; }
+    cluster_barrier();   // (2) coef, beta, breakdown and the stop decision are published
+    if (tc0) { const long long t = clock64(); tr[12] += t - c0a; tr[13] += 1; }
     if (tw) { const long long t = clock64(); tr[2] += t - tc; tc = t; }
-
-    if (crank == 0) {    // fold Hessenberg column i-1 (sh.col) into the Givens state
-      if (i > 0) settle_block(L, sh, i, i, sh.broke, &res);
-      __syncthreads();
-      if (tid == 0) {
-        const int stop = L.flags->stop_iter, broke = L.flags->broke_iter;
-        s_pub[2] = (stop < i + 1 || (broke >= 0 && broke < i + 1)) ? 0.0 : 1.0;
-      }
+    if (pub0[2] == 0.0) break;             // fold i-1 converged: no iteration i
+    if (pub0[1] != 0.0) {                  // breakdown: K2 skipped, cycle over
+      if (crank == 0 && i > 0) settle_block(L, sh, i, i, true, &res);
+      produced = p + 1;
+      break;
     }
 
-    // ---- K2 on the own rows (gram_schmidt.py:230-242; lagged_update_kernel's
-    // row expression), skipped on breakdown
-    const double beta = pub0[0];
-    const bool skip = pub0[1] != 0.0;
-    if (crank != 0)
+    if (crank == 0) {
+      // Givens fold of Hessenberg column i-1 (gmres.py:427-435), deferred
+      // as in the pipeline2 schedule (gmres.py:444-462): the control CTA
+      // arrives at barrier (3) first, so the fold overlaps the row CTAs'
+      // K2 and, past the barrier, the next SpMV and partial dots; a
+      // convergence it detects cancels the next iteration at barrier (2).
+      cluster_arrive();
+      if (i > 0) settle_block(L, sh, i, i, false, &res);
+      __syncthreads();
+      if (tid == 0) s_stop = L.flags->stop_iter <= i;
+      cluster_wait();
+    } else {
+      // ---- K2 on the own rows (gram_schmidt.py:230-242; lagged_update_kernel's
+      // row expression)
+      const double beta = pub0[0];
       for (int k = tid; k < p; k += kPT) sc[k] = coef0[k];
-    __syncthreads();
-    if (!skip) {
+      __syncthreads();
       const double cu = sc[p - 1];
       for (int j = tid; j < nr; j += kPT) {
         double acc = 0.0;
@@ -404,12 +429,11 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
         if (ks) ww = __ddiv_rn(ww, beta);
         sw[j] = ww - acc;
       }
+      produced = p + 1;
+      if (tw) { const long long t = clock64(); tr[3] += t - tc; tc = t; }
+      cluster_barrier();   // (3) the next SpMV reads the updated column
+      if (tw) { const long long t = clock64(); tr[4] += t - tc; tr[8] += 1; }
     }
-    if (tw) { const long long t = clock64(); tr[3] += t - tc; tc = t; }
-    cluster_barrier();   // (3) the next SpMV reads the updated column; the
-                         // fold's stop decision is published
-    if (tw) { const long long t = clock64(); tr[4] += t - tc; tr[8] += 1; }
-    if (tid == 0) s_go = pub0[2] != 0.0;
   }
   if (bad) atomicOr(reinterpret_cast<int*>(cl.map_shared_rank(L.flags, 0)) + 4, 1);  // nonfinite
   // the basis columns this cycle produced, own rows, back to HBM
@@ -438,6 +462,8 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
     }
     else
       for (int k = 5; k < 8; ++k) g_ptrace[k] = tr[k];
+    if (crank == 0)
+      for (int k = 11; k < 16; ++k) g_ptrace[k] = tr[k];
     if (crank == 1) g_ptrace[8] = tr[8];
   }
 }

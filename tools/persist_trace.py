@@ -47,6 +47,10 @@ def main():
              "ctl: a/beta", "ctl: T col", "ctl: c + join"]
     print("mean SM cycles per iteration:", {k: round(float(v) / its, 1) for k, v in zip(names, t[:8])})
     print("row-CTA total cycles per iteration:", round(float(t[:5].sum()) / its, 1))
+    c0 = max(t[13], 1)
+    print("control CTA: B1 exit -> B2 arrive", round(float(t[11]) / c0, 1), "cycles; B2 arrive -> exit",
+          round(float(t[12]) / c0, 1), "| gather done at", round(float(t[14]) / c0, 1),
+          "small done at", round(float(t[15]) / c0, 1))
     print("row CTA: thread 0's SpMV rows done at", round(float(t[9]) / its, 1),
           "cycles, SpMV of the whole CTA done at", round(float(t[10]) / its, 1))
 
