@@ -778,11 +778,26 @@ def _persist_problem(P, kind):
     if kind == "lap3d_15":           # n = 3,375, GMRES(50): 15 row CTAs x 225 rows x 52 columns
         A = P.gen_laplace3d(15)
         return A, P.gen_rhs("random", A, 5), 50, 1e-6, {}
+    if kind == "ragged_csr":         # rows of 1..150 entries (> 32: the generic row sum)
+        rng = np.random.default_rng(5)
+        n = 3000
+        lens = rng.integers(1, 40, n)
+        lens[::97] = 150
+        cols = [np.unique(np.concatenate([[r], rng.choice(n, size=int(k) - 1, replace=False)]))
+                for r, k in enumerate(lens)]
+        ptr = np.concatenate([[0], np.cumsum([len(c) for c in cols])]).astype(np.int64)
+        ci = np.concatenate(cols).astype(np.int64)
+        vals = rng.standard_normal(ci.size) * 0.05
+        rows = np.repeat(np.arange(n), np.diff(ptr))
+        vals[ci == rows] = 4.0 + rng.random(n)        # diagonally dominant
+        A = P.CsrMatrix(n, n, ptr, ci, vals)
+        return A, P.gen_rhs("random", A, 9), 30, 1e-10, {}
     A = P.CsrMatrix.diagonal([2.0, 3.0, 4.0, 5.0])   # happy breakdown inside the cycle
     return A, np.ones(4), 10, 1e-14, {}
 
 
-@pytest.mark.parametrize("kind", ["c1", "c1_jacobi", "conv27_csr", "lap3d_15", "breakdown"])
+@pytest.mark.parametrize("kind", ["c1", "c1_jacobi", "conv27_csr", "lap3d_15", "ragged_csr",
+                                  "breakdown"])
 @pytest.mark.parametrize("meth", ["one_sync_mgs", "pipeline2"])
 def test_persistent_cycle_matches_per_iteration_kernels(P, monkeypatch, kind, meth):
     """lsb_cycle_persistent (one cluster launch per restart cycle) against the
