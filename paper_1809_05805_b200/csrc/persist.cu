@@ -48,7 +48,7 @@ constexpr size_t kPMaxSmem = 200 * 1024;   // + ~10 KB static <= 227 KB
 // SpMV+dots, wait at barrier 1, wait at barrier 2 (= CTA 0's gather + small
 // state), K2, wait at barrier 3 (= the fold beyond K2); [5..7] CTA 0:
 // small-state front, T column, c; [8] iterations summed.
-constexpr int kTraceSlots = 16;
+constexpr int kTraceSlots = 18;
 __device__ long long g_ptrace[kTraceSlots];
 
 __device__ __forceinline__ void cluster_barrier() {
@@ -154,6 +154,7 @@ __device__ void persist_small(const lsb_arnoldi& L, SmallShared& sh, double* scr
   constexpr int kW = kPT / 32 - 1;          // speculating warps
   double* Tnew = scratch;                    // T[:p, p-1]
   double* cnew = scratch + cap;              // c
+  if (stamps && t == 0) stamps[4] = clock64();
   for (int e = t; e < p; e += kPT) {
     sh.a[e] = L.G[2 * e];
     sh.y[e] = L.G[2 * e + 1];
@@ -220,6 +221,7 @@ __device__ void persist_small(const lsb_arnoldi& L, SmallShared& sh, double* scr
     }
   }
   __syncthreads();
+  if (stamps && t == 0) stamps[5] = clock64();
 }
 
 __global__ void __launch_bounds__(kPT, 1)
@@ -375,13 +377,15 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
         }
         __syncthreads();
         if (tc0) { const long long t = clock64(); tr[14] += t - c0a; }
-        __shared__ long long sm[4];
+        __shared__ long long sm[6];
         persist_small(L, sh, scratch, i, p, ks, (trace && i > 0) ? sm : nullptr);
         if (tc0) { const long long t = clock64(); tr[15] += t - c0a; }
         if (trace && i > 0 && tid == 0 && !sh.broke) {
           tr[5] += sm[1] - sm[0];
           tr[6] += sm[2] - sm[1];
           tr[7] += sm[3] - sm[2];
+          tr[9] += sm[0] - sm[4];     // entry -> first sync (control CTA)
+          tr[10] += sm[5] - sm[3];    // commit + final sync (control CTA)
         }
       }
       if (tid == 0) {
@@ -462,8 +466,11 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
     }
     else
       for (int k = 5; k < 8; ++k) g_ptrace[k] = tr[k];
-    if (crank == 0)
+    if (crank == 0) {
       for (int k = 11; k < 16; ++k) g_ptrace[k] = tr[k];
+      g_ptrace[6 + 10] = tr[9];
+      g_ptrace[6 + 11] = tr[10];
+    }
     if (crank == 1) g_ptrace[8] = tr[8];
   }
 }

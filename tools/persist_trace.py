@@ -39,8 +39,8 @@ def main():
     eng.cycle()
     torch.cuda.synchronize()
     lib.lsb_set_tuning(_abi.TUNE_PERSIST_TRACE, 0)
-    buf = (C.c_int64 * 16)()
-    _abi.call("lsb_persist_trace", buf, 16)
+    buf = (C.c_int64 * 18)()
+    _abi.call("lsb_persist_trace", buf, 18)
     t = np.array(buf, dtype=np.float64)
     its = max(t[8], 1)
     names = ["row CTA: spmv+dots", "wait b1", "wait b2 (gather+small)", "K2", "wait b3 (fold)",
@@ -50,7 +50,8 @@ def main():
     c0 = max(t[13], 1)
     print("control CTA: B1 exit -> B2 arrive", round(float(t[11]) / c0, 1), "cycles; B2 arrive -> exit",
           round(float(t[12]) / c0, 1), "| gather done at", round(float(t[14]) / c0, 1),
-          "small done at", round(float(t[15]) / c0, 1))
+          "small done at", round(float(t[15]) / c0, 1), "| small: entry->sync", round(float(t[16]) / c0, 1),
+          "commit", round(float(t[17]) / c0, 1))
     print("row CTA: thread 0's SpMV rows done at", round(float(t[9]) / its, 1),
           "cycles, SpMV of the whole CTA done at", round(float(t[10]) / its, 1))
 
