@@ -140,8 +140,10 @@ __device__ __forceinline__ void copy_d(double* dst, const double* src, int n) {
 // Givens fold is deferred), arranged for latency: warp 0 runs the breakdown
 // test (beta, ||R[:p-1,p-1]||, CPython hypot -- gram_schmidt.py:96-106)
 // while warps 1..15 speculatively compute the new T column and
-// c = T^T y / beta; the results are committed only if the column did not
-// break down.  Same arithmetic (and the same warp-tree sums) as
+// c = T^T y / beta straight into the state.  On a breakdown the cycle ends
+// at this iteration and those slots (T[:, p-1], R[:, p], coef) are never
+// read again -- the least squares uses the rotated triangle and the host's
+// Hessenberg view stops at column p-1.  Same arithmetic (and the same warp-tree sums) as
 // mgs_small_body with SmallResident::warp_dots, so the bits do not change.
 // scratch: 2*cap doubles.
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -152,8 +154,7 @@ __device__ void persist_small(const lsb_arnoldi& L, SmallShared& sh, double* scr
                               int p, int ks, long long* stamps) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5, cap = L.cap;
   constexpr int kW = kPT / 32 - 1;          // speculating warps
-  double* Tnew = scratch;                    // T[:p, p-1]
-  double* cnew = scratch + cap;              // c
+  double* Tnew = scratch;                    // T[:p, p-1] (read back by the c sums)
   if (stamps && t == 0) stamps[4] = clock64();
   for (int e = t; e < p; e += kPT) {
     sh.a[e] = L.G[2 * e];
@@ -184,6 +185,7 @@ __device__ void persist_small(const lsb_arnoldi& L, SmallShared& sh, double* scr
         sh.col[p - 1] = beta;
         L.R[(int64_t)(p - 1) * cap + (p - 1)] = beta;
       }
+      if (stamps) stamps[5] = clock64();
     }
   } else {
     // ---- speculative T column and c (mgs_small_body)
@@ -196,9 +198,15 @@ __device__ void persist_small(const lsb_arnoldi& L, SmallShared& sh, double* scr
       double acc = 0.0;
       for (int l = j + lane; l < p - 1; l += 32) acc = fma(L.T[(int64_t)j * cap + l], sh.a[l], acc);
       acc = warp_sum(acc);
-      if (lane == 0) Tnew[j] = -acc;
+      if (lane == 0) {
+        Tnew[j] = -acc;
+        L.T[(int64_t)j * cap + (p - 1)] = -acc;
+      }
     }
-    if (u == 0) Tnew[p - 1] = 1.0;
+    if (u == 0) {
+      Tnew[p - 1] = 1.0;
+      L.T[(int64_t)(p - 1) * cap + (p - 1)] = 1.0;
+    }
     named_bar(1, 32 * kW);
     if (stamps && t == 32) stamps[2] = clock64();
     for (int j = wid - 1; j < p; j += kW) {
@@ -208,20 +216,15 @@ __device__ void persist_small(const lsb_arnoldi& L, SmallShared& sh, double* scr
         acc = fma(tl, l == p - 1 ? ylast : sh.y[l], acc);
       }
       acc = warp_sum(acc);
-      if (lane == 0) cnew[j] = ks ? __ddiv_rn(acc, beta) : acc;
+      if (lane == 0) {
+        const double c = ks ? __ddiv_rn(acc, beta) : acc;
+        L.coef[j] = c;
+        L.R[(int64_t)j * cap + p] = c;
+      }
     }
   }
   __syncthreads();
   if (stamps && t == 0) stamps[3] = clock64();
-  if (!sh.broke) {                           // commit
-    for (int j = t; j < p; j += kPT) {
-      L.T[(int64_t)j * cap + (p - 1)] = Tnew[j];
-      L.coef[j] = cnew[j];
-      L.R[(int64_t)j * cap + p] = cnew[j];
-    }
-  }
-  __syncthreads();
-  if (stamps && t == 0) stamps[5] = clock64();
 }
 
 __global__ void __launch_bounds__(kPT, 1)
@@ -385,7 +388,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
           tr[6] += sm[2] - sm[1];
           tr[7] += sm[3] - sm[2];
           tr[9] += sm[0] - sm[4];     // entry -> first sync (control CTA)
-          tr[10] += sm[5] - sm[3];    // commit + final sync (control CTA)
+          tr[10] += sm[5] - sm[0];    // warp 0: breakdown test done (from the first sync)
         }
       }
       if (tid == 0) {

@@ -51,7 +51,7 @@ def main():
     print("control CTA: B1 exit -> B2 arrive", round(float(t[11]) / c0, 1), "cycles; B2 arrive -> exit",
           round(float(t[12]) / c0, 1), "| gather done at", round(float(t[14]) / c0, 1),
           "small done at", round(float(t[15]) / c0, 1), "| small: entry->sync", round(float(t[16]) / c0, 1),
-          "commit", round(float(t[17]) / c0, 1))
+          "warp0 tol chain done at", round(float(t[17]) / c0, 1), "after the first sync")
     print("row CTA: thread 0's SpMV rows done at", round(float(t[9]) / its, 1),
           "cycles, SpMV of the whole CTA done at", round(float(t[10]) / its, 1))
 
