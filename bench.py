@@ -388,7 +388,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=8)
+    ap.add_argument("--cpu-iters", type=int, default=16)
     ap.add_argument("--slab", type=int, default=N_SLAB, help="per-GPU cube edge (256 = config 2)")
     ap.add_argument("--kernel-timers", default="last", choices=["last", "all"],
                     help="per-kernel CUDA events in the last timed cycle only, or in every one")
