@@ -22,6 +22,49 @@ struct Stencil7 {
   int64_t lo_valid, hi_valid;  // u rows that exist in memory (ghost planes included)
 };
 
+// One row pair (lr, lr+1) of w = A u from the staged tile (numpy order:
+// first present product + sequential sum of the rest), written to the
+// shared w tile and to HBM.
+__device__ __forceinline__ void s7_tile_pair(const Stencil7& K, const double* ut, const double* zt,
+                                             const double* pt, int lr, int64_t r, int64_t n,
+                                             double* sw, double* __restrict__ wout, bool& bad) {
+  if (r >= n) { sw[lr] = sw[lr + 1] = 0.0; return; }
+  const uint32_t line = K.fx.div((uint32_t)r);
+  const int ix = (int)((uint32_t)r - line * (uint32_t)K.nx);
+  const uint32_t iz = K.fy.div(line);
+  const int iy = (int)(line - iz * (uint32_t)K.ny);
+  const bool pzm = (int)iz - 1 >= K.zlo, pzp = (int)iz + 1 <= K.zhi;
+  const bool pym = iy >= 1, pyp = iy + 1 < K.ny;
+  const bool pxm = ix >= 1, pxp = ix + 2 < K.nx;
+  const double2 zm = *reinterpret_cast<const double2*>(zt + lr);
+  const double2 zp = *reinterpret_cast<const double2*>(pt + lr);
+  const double2 ym = *reinterpret_cast<const double2*>(ut + lr - K.nx);
+  const double2 yp = *reinterpret_cast<const double2*>(ut + lr + K.nx);
+  const double2 cc = *reinterpret_cast<const double2*>(ut + lr);
+  const double xm = ut[lr - 1], xp = ut[lr + 2];
+  double f0 = 0.0, a0 = -0.0, f1 = 0.0, a1 = -0.0;
+  bool h0 = false, h1 = false;
+#define LSB_T(pres, c, v, f, a, h)                 \
+  if (pres) {                                       \
+    const double pv = __dmul_rn(c, v);              \
+    if (h) a = __dadd_rn(a, pv); else f = pv;       \
+    h = true;                                       \
+  }
+  LSB_T(pzm, K.c0, zm.x, f0, a0, h0) LSB_T(pzm, K.c0, zm.y, f1, a1, h1)
+  LSB_T(pym, K.c1, ym.x, f0, a0, h0) LSB_T(pym, K.c1, ym.y, f1, a1, h1)
+  LSB_T(pxm, K.c2, xm, f0, a0, h0)   LSB_T(true, K.c2, cc.x, f1, a1, h1)
+  LSB_T(true, K.c3, cc.x, f0, a0, h0) LSB_T(true, K.c3, cc.y, f1, a1, h1)
+  LSB_T(true, K.c4, cc.y, f0, a0, h0) LSB_T(pxp, K.c4, xp, f1, a1, h1)
+  LSB_T(pyp, K.c5, yp.x, f0, a0, h0) LSB_T(pyp, K.c5, yp.y, f1, a1, h1)
+  LSB_T(pzp, K.c6, zp.x, f0, a0, h0) LSB_T(pzp, K.c6, zp.y, f1, a1, h1)
+#undef LSB_T
+  const double s0 = __dadd_rn(f0, a0), s1 = __dadd_rn(f1, a1);
+  if (!isfinite(s0) || !isfinite(s1)) bad = true;
+  sw[lr] = s0;
+  sw[lr + 1] = s1;
+  *reinterpret_cast<double2*>(wout + r) = make_double2(s0, s1);
+}
+
 template <int R, int SLOTS, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
 mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
@@ -99,45 +142,8 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
     }
     // ---- w = A u for the tile rows (row pairs; nx even keeps pairs in a line)
 #pragma unroll 2
-    for (int j = threadIdx.x; j < kTile / 2; j += kThreads) {
-      const int lr = 2 * j;
-      const int64_t r = r0 + lr;
-      if (r >= n) { sw[lr] = sw[lr + 1] = 0.0; continue; }
-      const uint32_t line = K.fx.div((uint32_t)r);
-      const int ix = (int)((uint32_t)r - line * (uint32_t)K.nx);
-      const uint32_t iz = K.fy.div(line);
-      const int iy = (int)(line - iz * (uint32_t)K.ny);
-      const bool pzm = (int)iz - 1 >= K.zlo, pzp = (int)iz + 1 <= K.zhi;
-      const bool pym = iy >= 1, pyp = iy + 1 < K.ny;
-      const bool pxm = ix >= 1, pxp = ix + 2 < K.nx;
-      const double2 zm = *reinterpret_cast<const double2*>(zt + lr);
-      const double2 zp = *reinterpret_cast<const double2*>(pt + lr);
-      const double2 ym = *reinterpret_cast<const double2*>(ut + lr - K.nx);
-      const double2 yp = *reinterpret_cast<const double2*>(ut + lr + K.nx);
-      const double2 cc = *reinterpret_cast<const double2*>(ut + lr);
-      const double xm = ut[lr - 1], xp = ut[lr + 2];
-      double f0 = 0.0, a0 = -0.0, f1 = 0.0, a1 = -0.0;
-      bool h0 = false, h1 = false;
-#define LSB_T(pres, c, v, f, a, h)                 \
-      if (pres) {                                   \
-        const double pv = __dmul_rn(c, v);          \
-        if (h) a = __dadd_rn(a, pv); else f = pv;   \
-        h = true;                                   \
-      }
-      LSB_T(pzm, K.c0, zm.x, f0, a0, h0) LSB_T(pzm, K.c0, zm.y, f1, a1, h1)
-      LSB_T(pym, K.c1, ym.x, f0, a0, h0) LSB_T(pym, K.c1, ym.y, f1, a1, h1)
-      LSB_T(pxm, K.c2, xm, f0, a0, h0)   LSB_T(true, K.c2, cc.x, f1, a1, h1)
-      LSB_T(true, K.c3, cc.x, f0, a0, h0) LSB_T(true, K.c3, cc.y, f1, a1, h1)
-      LSB_T(true, K.c4, cc.y, f0, a0, h0) LSB_T(pxp, K.c4, xp, f1, a1, h1)
-      LSB_T(pyp, K.c5, yp.x, f0, a0, h0) LSB_T(pyp, K.c5, yp.y, f1, a1, h1)
-      LSB_T(pzp, K.c6, zp.x, f0, a0, h0) LSB_T(pzp, K.c6, zp.y, f1, a1, h1)
-#undef LSB_T
-      const double s0 = __dadd_rn(f0, a0), s1 = __dadd_rn(f1, a1);
-      if (!isfinite(s0) || !isfinite(s1)) bad = true;
-      sw[lr] = s0;
-      sw[lr + 1] = s1;
-      *reinterpret_cast<double2*>(wout + r) = make_double2(s0, s1);
-    }
+    for (int j = threadIdx.x; j < kTile / 2; j += kThreads)
+      s7_tile_pair(K, ut, zt, pt, 2 * j, r0 + 2 * j, n, sw, wout, bad);
     __syncthreads();
     // ---- column sweep: [Q^T u, Q^T w] partials (same item deal as mdot_kernel)
 #pragma unroll
@@ -214,6 +220,171 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
   if (threadIdx.x == 0) *counter = 0u;
 }
 
+// Pipelined variant: one barrier per tile, and the stencil work of tile
+// t+1 is done inside tile t's column sweep, between issuing an item's basis
+// loads and consuming them, so it hides under the load latency instead of
+// stalling all warps between two barriers.  Two w buffers: the sweep of t
+// reads sw[t], the stencil of t+1 writes sw[t+1].  Tile t+1's u data is
+// staged (TMA, issued at the top of tile t) into the other stage buffer.
+// Same arithmetic and the same item deal / summation order as
+// mdot_spmv7_kernel, so w and the partials are bitwise equal.
+template <int R, int SLOTS, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+mdot_spmv7_pipe_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
+                       double* __restrict__ wout, const Stencil7 K, double* __restrict__ out,
+                       double* __restrict__ partial, unsigned* counter, lsb_flags* flags, int it) {
+  if (gated_off(flags, it)) return;
+  constexpr int kRows = kTile / R;
+  constexpr int kLd = kRows / 64;
+  extern __shared__ __align__(16) double smem[];
+  const int H = K.nx;
+  const int span = kTile + 2 * H;
+  const int stage = span + 2 * kTile;
+  double* swb = smem + 2 * stage;              // two w tiles
+  __shared__ double red[kWarps * SLOTS][2];
+  const double* __restrict__ u = X + (int64_t)(p - 1) * ld;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int part = warp % R;
+  double acc[SLOTS][2];
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) acc[s][0] = acc[s][1] = 0.0;
+  bool bad = false;
+  __shared__ __align__(8) uint64_t bars[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto stage_all = [&](int b, int64_t t) {
+    double* base = smem + b * stage;
+    const int64_t r0 = t * kTile;
+    unsigned tx = 0;
+    const bool leader = threadIdx.x == 0;
+    stage_bulk(base, u, r0 - H, span, K.lo_valid, K.hi_valid, &bars[b], leader, &tx);
+    stage_bulk(base + span, u, r0 - K.plane, kTile, K.lo_valid, K.hi_valid, &bars[b], leader, &tx);
+    stage_bulk(base + span + kTile, u, r0 + K.plane, kTile, K.lo_valid, K.hi_valid, &bars[b],
+               leader, &tx);
+    if (leader) mbar_arrive_tx(&bars[b], tx);
+  };
+  const int64_t ntiles = (n + kTile - 1) / kTile;
+  int64_t t = blockIdx.x;
+  int buf = 0;
+  unsigned phase = 0;
+  if (t < ntiles) {            // prologue: w of the first tile, whole
+    stage_all(0, t);
+    mbar_wait(&bars[0], 0u);
+    phase ^= 1u;
+    const double* ut = smem + H;
+    const double* zt = smem + span;
+    for (int j = threadIdx.x; j < kTile / 2; j += kThreads)
+      s7_tile_pair(K, ut, zt, zt + kTile, 2 * j, t * kTile + 2 * j, n, swb, wout, bad);
+  }
+  for (; t < ntiles; t += gridDim.x) {
+    __syncthreads();           // w of tile t complete; tile t-1 fully consumed
+    const int64_t tn = t + gridDim.x;
+    const bool nxt = tn < ntiles;
+    if (nxt) stage_all(buf ^ 1, tn);
+    const int64_t r0 = t * kTile;
+    const double* ut = smem + buf * stage + H;
+    const double* sw = swb + buf * kTile;
+    const double* utn = smem + (buf ^ 1) * stage + H;
+    const double* ztn = smem + (buf ^ 1) * stage + span;
+    double* swn = swb + (buf ^ 1) * kTile;
+    const int64_t rn0 = tn * kTile;
+    const bool full = r0 + kTile <= n;
+    const int rbase = part * kRows;
+    bool ready = false;
+    auto chunk = [&](int c) {  // stencil pairs of tile tn owned by chunk c
+      if (!nxt) return;
+      if (!ready) {
+        mbar_wait(&bars[buf ^ 1], (phase >> (buf ^ 1)) & 1u);
+        phase ^= 1u << (buf ^ 1);
+        ready = true;
+      }
+      const int j0 = SLOTS == 1 ? 0 : c, j1 = SLOTS == 1 ? 2 : c + 1;
+      for (int jj = j0; jj < j1; ++jj) {
+        const int j = threadIdx.x + jj * kThreads;
+        s7_tile_pair(K, utn, ztn, ztn + kTile, 2 * j, rn0 + 2 * j, n, swn, wout, bad);
+      }
+    };
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const int k = (warp + kWarps * s) / R;
+      const bool live = k < p;
+      const double* col = X + (int64_t)k * ld + r0 + rbase;
+      double2 xv[kLd];
+      if (live && full) {
+#pragma unroll
+        for (int q = 0; q < kLd; ++q) xv[q] = ld_stream(col + 2 * (lane + 32 * q));
+      }
+      if (s < 2) chunk(s);     // overlaps the loads just issued
+      if (live) {
+        double a0 = 0.0, a1 = 0.0;
+        if (full) {
+#pragma unroll
+          for (int q = 0; q < kLd; ++q) {
+            const int lr = rbase + 2 * (lane + 32 * q);
+            const double2 yu = *reinterpret_cast<const double2*>(ut + lr);
+            const double2 yw = *reinterpret_cast<const double2*>(sw + lr);
+            a0 = fma(xv[q].x, yu.x, a0);
+            a0 = fma(xv[q].y, yu.y, a0);
+            a1 = fma(xv[q].x, yw.x, a1);
+            a1 = fma(xv[q].y, yw.y, a1);
+          }
+        } else {
+          for (int q = 0; q < kLd; ++q) {
+            const int lr = rbase + 2 * (lane + 32 * q);
+            const int64_t r = r0 + lr;
+            const double xa = r < n ? col[lr - rbase] : 0.0;
+            const double xb = r + 1 < n ? col[lr - rbase + 1] : 0.0;
+            const double ua = r < n ? ut[lr] : 0.0, ub = r + 1 < n ? ut[lr + 1] : 0.0;
+            a0 = fma(xa, ua, a0);
+            a0 = fma(xb, ub, a0);
+            a1 = fma(xa, sw[lr], a1);
+            a1 = fma(xb, sw[lr + 1], a1);
+          }
+        }
+        acc[s][0] += a0;
+        acc[s][1] += a1;
+      }
+    }
+    buf ^= 1;
+  }
+  if (bad && flags) flags->nonfinite = 1;
+
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const double x = warp_sum(acc[s][v]);
+      if (lane == 0) red[warp + kWarps * s][v] = x;
+    }
+  __syncthreads();
+  const int G = gridDim.x;
+  for (int e = threadIdx.x; e < p * 2; e += kThreads) {
+    const int k = e / 2, v = e % 2;
+    double x = red[k * R][v];
+#pragma unroll
+    for (int pr = 1; pr < R; ++pr) x += red[k * R + pr][v];
+    partial[(size_t)e * G + blockIdx.x] = x;
+  }
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(counter, 1u) == (unsigned)G - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int e = warp; e < 2 * p; e += kWarps) {
+    double x = 0.0;
+    for (int c = lane; c < G; c += 32) x += __ldcg(partial + (size_t)e * G + c);
+    x = warp_sum(x);
+    if (lane == 0) out[e] = x;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
 // 3 CTAs/SM (<= 8 items per warp, register-capped) loses to the 2-CTA
 // variant with whole-tile items at every p >= 8 (tools/kfused.py: p = 26
 // 644 vs 568 us) and ties below; kept as an opt-in (knob value 1).
@@ -222,27 +393,49 @@ static bool occ3(int p) {
   return tuning(LSB_TUNE_FUSED_OCC3) == 1;
 }
 
-static size_t smem_bytes(int nx) { return sizeof(double) * (2 * (kTile + 2 * nx + 2 * kTile) + kTile); }
+static size_t smem_bytes(int nx, bool pipe) {
+  return sizeof(double) * (2 * (kTile + 2 * nx + 2 * kTile) + (pipe ? 2 : 1) * kTile);
+}
 
-template <int R, int SLOTS, int MINB>
-static int launch_t(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cudaStream_t st) {
-  static int occ_nx = -1, occ = 0;
-  auto kern = mdot_spmv7_kernel<R, SLOTS, MINB>;
-  const size_t sm = smem_bytes(K.nx);
-  if (occ_nx != K.nx) {
+// the pipelined kernel for 2..4 items per warp, 2 CTAs/SM (tools/kpipe.py,
+// 256^3: 3-4% faster there; with one item the stencil chunks have no loads
+// to hide under, and at 8 items the extra live registers spill)
+static bool use_pipe(int slots) {
+  const int knob = tuning(LSB_TUNE_FUSED_PIPE);
+  if (knob == 2 || occ3(0)) return false;
+  return knob == 1 ? slots <= 8 : (slots >= 2 && slots <= 4);
+}
+
+template <class Kern>
+static int launch_k(Kern kern, bool pipe, int* occ_nx, int* occ, const lsb_arnoldi& S,
+                    const Stencil7& K, int p, int it, cudaStream_t st) {
+  const size_t sm = smem_bytes(K.nx, pipe);
+  if (*occ_nx != K.nx) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, sm);
-    if (occ < 1) occ = 1;
-    occ_nx = K.nx;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, kThreads, sm);
+    if (*occ < 1) *occ = 1;
+    *occ_nx = K.nx;
   }
   const int64_t ntiles = (S.n + kTile - 1) / kTile;
-  int64_t grid = (int64_t)sm_count() * occ;
+  int64_t grid = (int64_t)sm_count() * *occ;
   if (S.ws.grid > 0 && S.ws.grid < grid) grid = S.ws.grid;
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
   kern<<<(unsigned)grid, kThreads, sm, st>>>(S.V, S.ld, S.n, p, S.V + (int64_t)p * S.ld, K,
                                             S.Gloc, S.ws.partial, S.ws.counter, S.flags, it);
   return check_launch("mdot_spmv7");
+}
+
+template <int R, int SLOTS, int MINB>
+static int launch_t(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cudaStream_t st) {
+  if constexpr (MINB == 2 && SLOTS <= 8) {
+    if (use_pipe(SLOTS)) {
+      static int nx = -1, occ = 0;
+      return launch_k(mdot_spmv7_pipe_kernel<R, SLOTS, MINB>, true, &nx, &occ, S, K, p, it, st);
+    }
+  }
+  static int nx = -1, occ = 0;
+  return launch_k(mdot_spmv7_kernel<R, SLOTS, MINB>, false, &nx, &occ, S, K, p, it, st);
 }
 
 template <int R>
