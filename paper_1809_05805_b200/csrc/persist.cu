@@ -4,30 +4,36 @@
 //
 // At launch-bound sizes (C1: n = 4,096) the per-iteration kernels spend
 // their time in launch and grid-reduction latency, not in HBM traffic.  Here
-// up to 16 CTAs of one cluster each hold a contiguous row block of EVERY
-// basis column in shared memory (V never leaves the SMs during the cycle;
-// columns are mirrored to HBM for the cycle epilogue) and run the
-// iterations back to back:
-//   SpMV of the own rows: CSR, u of every row read from its owner CTA
-//     through distributed shared memory, numpy row order (the K7 bits)
-//   -> per-CTA [Q^T u, Q^T w] partials (shared memory only)
-//   -> cluster barrier; CTA 0 sums the partials of all CTAs in rank order
-//      over DSMEM and runs the K5 small state (mgs_small_body: beta,
-//      breakdown test, T column, c = T^T y, Hessenberg column, Givens)
-//   -> cluster barrier; every row CTA applies the K2 row update to its rows
-//      while the control CTA folds the Givens rotation (it arrives at the
-//      next barrier first, so the fold also overlaps the next SpMV)
-//   -> cluster barrier (the next SpMV reads the updated column).
+// one control CTA and up to 15 row CTAs form one cluster.  Each row CTA
+// holds a contiguous row block of EVERY basis column (and its CSR rows) in
+// shared memory; the control CTA holds the whole small state (R, T, the
+// rotations, g, the rotated triangle, flags).  Nothing touches HBM during
+// the cycle: V and the small state are copied in at launch and out at the
+// end, for the cycle epilogue kernels.  Per iteration:
+//   row CTAs: SpMV of the own rows (CSR, u of every row read from its
+//     owner CTA through distributed shared memory, numpy row order = the
+//     K7 bits), partial [Q^T u, Q^T w] of the own rows, pushed into the
+//     control CTA's shared memory by DSMEM stores
+//   -> cluster barrier (1); the control CTA sums the partials in rank order
+//      and runs K5: warp 0 the breakdown test, warps 1..15 the T column and
+//      c = T^T y / beta (persist_small; same arithmetic as mgs_small_body)
+//   -> cluster barrier (2); row CTAs read beta, c and the flags over DSMEM
+//      and apply the K2 row update; the control CTA arrives at barrier (3)
+//      at once and folds the Givens rotation meanwhile (pipeline2's
+//      deferral: a convergence it finds cancels the next iteration at
+//      barrier (2), so the stop semantics are exact)
+//   -> cluster barrier (3) (the next SpMV reads the updated column).
 // Three cluster barriers per iteration replace four kernel launches and
 // three grid-wide last-CTA reductions.  Barriers are release/acquire at
-// cluster scope; the flags and coefficients CTA 0 writes are read with
-// ld.global.cg.
+// cluster scope and only shared memory is written inside the loop, so no
+// barrier waits for global stores (each barrier.cluster.arrive.release
+// waits for the CTA's outstanding stores).
 //
-// Results: SpMV, beta, T, c, Givens and the K2 row expression are the
-// per-iteration kernels' own code; only the order of the mdot sum differs
-// (per-CTA warp trees + rank-ordered cluster sum instead of the K1 tree),
-// so histories agree with the multi-kernel path to rounding
-// (tests/test_gpu_parity.py).
+// Results: SpMV, beta, T, c, Givens and the K2 row expression follow the
+// per-iteration kernels; the mdot sums (per-CTA warp trees + rank-ordered
+// cluster sum instead of the K1 tree) and the small T / c dot products
+// (warp trees) are summed in a different order, so histories agree with the
+// multi-kernel path to rounding (tests/test_gpu_parity.py).
 #include <cooperative_groups.h>
 
 #include "small_body.cuh"
