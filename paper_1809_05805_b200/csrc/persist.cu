@@ -149,9 +149,9 @@ __device__ __forceinline__ void copy_d(double* dst, const double* src, int n) {
 // c = T^T y / beta straight into the state.  On a breakdown the cycle ends
 // at this iteration and those slots (T[:, p-1], R[:, p], coef) are never
 // read again -- the least squares uses the rotated triangle and the host's
-// Hessenberg view stops at column p-1.  Same arithmetic (and the same warp-tree sums) as
-// mgs_small_body with SmallResident::warp_dots, so the bits do not change.
-// scratch: 2*cap doubles.
+// Hessenberg view stops at column p-1.  Same arithmetic as mgs_small_body
+// except that the T column and c dot products are warp trees (not serial
+// sums).  scratch: cap doubles.
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -177,7 +177,7 @@ __device__ void persist_small(const lsb_arnoldi& L, SmallShared& sh, double* scr
     for (int j = lane; j < p - 1; j += 32) ss = fma(sh.col[j], sh.col[j], ss);
     ss = warp_sum(ss);
     if (lane == 0) {
-      const double tol = breakdown_tol(L, beta, sh.col, p - 1, nullptr, ss);
+      const double tol = breakdown_tol(L, beta, sh.col, p - 1, ss);
       sh.beta = beta;
       sh.tol = tol;
       sh.broke = beta <= tol;
@@ -314,9 +314,6 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
   const double* pub0 = cl.map_shared_rank(s_pub, 0);
   const double* coef0 = cl.map_shared_rank(st + SL.coef, 0);
   double* allp0 = cl.map_shared_rank(allp, 0) + crank * 2 * cap;   // this CTA's slot at CTA 0
-  SmallResident res;
-  res.resident = true;
-  res.warp_dots = true;
   long long tr[kTraceSlots] = {0};
   long long tc = 0;
   bool bad = false;
@@ -409,7 +406,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
     if (tw) { const long long t = clock64(); tr[2] += t - tc; tc = t; }
     if (pub0[2] == 0.0) break;             // fold i-1 converged: no iteration i
     if (pub0[1] != 0.0) {                  // breakdown: K2 skipped, cycle over
-      if (crank == 0 && i > 0) settle_block(L, sh, i, i, true, &res);
+      if (crank == 0 && i > 0) settle_block(L, sh, i, i, true, /*resident=*/true);
       produced = p + 1;
       break;
     }
@@ -421,7 +418,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
       // K2 and, past the barrier, the next SpMV and partial dots; a
       // convergence it detects cancels the next iteration at barrier (2).
       cluster_arrive();
-      if (i > 0) settle_block(L, sh, i, i, false, &res);
+      if (i > 0) settle_block(L, sh, i, i, false, /*resident=*/true);
       __syncthreads();
       if (tid == 0) s_stop = L.flags->stop_iter <= i;
       cluster_wait();

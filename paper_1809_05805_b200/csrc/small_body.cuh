@@ -22,40 +22,20 @@ struct SmallShared {
   int broke;
 };
 
-// Options of a persistent caller (persist.cu) that keeps the small state
-// in its shared memory across the iterations of a cycle, so the serial
-// chain never waits on an L2 round trip.  Defaults: everything from S.
-struct SmallResident {
-  int ldT = 0;                 // row stride of sT (0: p, staged from S.T each call)
-  bool resident = false;       // sT / sh.rot already hold the earlier columns
-  double* coef = nullptr;      // also write c here (and read R[:p-1, p-1] from it)
-  const double* G = nullptr;   // gathered [Q^T u, Q^T w] (interleaved) instead of S.G
-  double* g = nullptr;         // rotated rhs copy (written through to S.g)
-  bool scal_cached = false;    // btf / target below instead of S.scal
-  double btf = 0.0, target = 0.0;
-  bool warp_dots = false;      // the small dot products as warp trees (not serial)
-  long long* trace = nullptr;  // diagnostics: phase timestamps (thread 0)
-};
-
-__device__ __forceinline__ void small_stamp(const SmallResident* rs, int k) {
-  if (rs && rs->trace && threadIdx.x == 0) {
-    rs->trace[k] = clock64();   // SM cycles (CTA 0 only)
-  }
-}
-
 // tol = btf * eps * sqrt(n) * hypot(r_diag, ||r_col||)   (gram_schmidt.py:96-100)
-// ss_pre >= 0: ||r_col||^2 already reduced by the caller.
-__device__ inline double breakdown_tol(const lsb_arnoldi& S, double r_diag, const double* rcol, int len,
-                                       const SmallResident* rs = nullptr, double ss_pre = -1.0) {
+// ss_pre >= 0: ||r_col||^2 already reduced by the caller (persist.cu).
+__device__ inline double breakdown_tol(const lsb_arnoldi& S, double r_diag, const double* rcol,
+                                       int len, double ss_pre = -1.0) {
   double pre = r_diag;
   if (len > 0) {
-    double ss = 0.0;
-    if (ss_pre >= 0.0) ss = ss_pre;
-    else
+    double ss = ss_pre;
+    if (ss < 0.0) {
+      ss = 0.0;
       for (int j = 0; j < len; ++j) ss = fma(rcol[j], rcol[j], ss);
+    }
     pre = py_hypot(r_diag, sqrt(ss));
   }
-  const double btf = rs && rs->scal_cached ? rs->btf : S.scal[LSB_S_BTF];
+  const double btf = S.scal[LSB_S_BTF];
   return __dmul_rn(__dmul_rn(__dmul_rn(btf, kEps), sqrt((double)S.n_global)), pre);
 }
 
@@ -65,23 +45,18 @@ __device__ inline double breakdown_tol(const lsb_arnoldi& S, double r_diag, cons
 // breakdown.  All threads must call it.
 // resident: sh.rot already holds rotations 0..gc-2 (a persistent caller
 // that ran every earlier fold of the cycle in this CTA).
-__device__ inline void settle_block(const lsb_arnoldi& S, SmallShared& sh, int it, int gc, bool broke,
-                                    const SmallResident* rs = nullptr) {
+__device__ inline void settle_block(const lsb_arnoldi& S, SmallShared& sh, int it, int gc,
+                                    bool broke, bool resident = false) {
   const int t = threadIdx.x;
-  if (!(rs && rs->resident))
+  if (!resident)
     for (int e = t; e < 2 * (gc - 1); e += blockDim.x) sh.rot[e] = S.rot[e];
   __syncthreads();
   if (t == 0) {
-    double* g = rs && rs->g ? rs->g : S.g;
-    const double res = givens_fold(sh.col, sh.rot, g, gc);
-    if (g != S.g) {
-      S.g[gc - 1] = g[gc - 1];
-      S.g[gc] = g[gc];
-    }
+    const double res = givens_fold(sh.col, sh.rot, S.g, gc);
     S.rot[2 * (gc - 1)] = sh.rot[2 * (gc - 1)];
     S.rot[2 * (gc - 1) + 1] = sh.rot[2 * (gc - 1) + 1];
     S.res[gc] = res;
-    const double target = rs && rs->scal_cached ? rs->target : S.scal[LSB_S_TARGET];
+    const double target = S.scal[LSB_S_TARGET];
     if (res <= target || broke) {
       S.flags->stop_iter = it;
       S.flags->status = res <= target ? LSB_CONVERGED : LSB_BREAKDOWN;
@@ -93,29 +68,18 @@ __device__ inline void settle_block(const lsb_arnoldi& S, SmallShared& sh, int i
 
 // Shared front of both lagged kernels: gathered G, deferred norm beta,
 // breakdown test against R[:p-1, p-1] (gram_schmidt.py:227-229 / 261-263).
-// rprev: R[:p-1, p-1] (the previous iteration's coefficients) when the
-// caller holds them in shared memory, else read from S.R.
-__device__ inline bool lagged_front(const lsb_arnoldi& S, SmallShared& sh, int it, int p, int gc,
-                                    const SmallResident* rs = nullptr) {
+__device__ inline bool lagged_front(const lsb_arnoldi& S, SmallShared& sh, int it, int p, int gc) {
   const int t = threadIdx.x, cap = S.cap;
-  const double* rprev = rs ? rs->coef : nullptr;
-  const double* Gs = rs ? rs->G : nullptr;
   for (int e = t; e < p; e += blockDim.x) {
-    sh.a[e] = Gs ? Gs[2 * e] : gsum(S, 2 * e);
-    sh.y[e] = Gs ? Gs[2 * e + 1] : gsum(S, 2 * e + 1);
-    if (e < p - 1) sh.col[e] = rprev ? rprev[e] : S.R[(int64_t)e * cap + (p - 1)];
+    sh.a[e] = gsum(S, 2 * e);
+    sh.y[e] = gsum(S, 2 * e + 1);
+    if (e < p - 1) sh.col[e] = S.R[(int64_t)e * cap + (p - 1)];
   }
   __syncthreads();
-  double ss = -1.0;
-  if (rs && rs->warp_dots && t < 32) {
-    ss = 0.0;
-    for (int j = t; j < p - 1; j += 32) ss = fma(sh.col[j], sh.col[j], ss);
-    ss = warp_sum(ss);
-  }
   if (t == 0) {
     const double bsq = sh.a[p - 1];
     const double beta = bsq > 0.0 ? sqrt(bsq) : 0.0;
-    const double tol = breakdown_tol(S, beta, sh.col, p - 1, rs, ss);
+    const double tol = breakdown_tol(S, beta, sh.col, p - 1);
     sh.beta = beta;
     sh.tol = tol;
     sh.broke = beta <= tol;
@@ -135,97 +99,61 @@ __device__ inline bool lagged_front(const lsb_arnoldi& S, SmallShared& sh, int i
 }
 
 // mgs_lvl2 small state (gram_schmidt.py:226-245 + gmres.py:418-435): one
-// CTA, every thread calls it.  sT: the T block in shared memory when
-// use_smem (row stride p, staged from S.T), else unused.
+// CTA, every thread calls it.  sT: p*p doubles of shared memory when
+// use_smem (the T block), else unused.
 __device__ inline void mgs_small_body(const lsb_arnoldi& S, SmallShared& sh, double* sT, int it,
-                                      int p, int ks, int gc, bool use_smem,
-                                      const SmallResident& rs = SmallResident()) {
+                                      int p, int ks, int gc, bool use_smem) {
   const int t = threadIdx.x, cap = S.cap;
-  const bool broke = lagged_front(S, sh, it, p, gc, &rs);
-  small_stamp(&rs, 0);
+  const bool broke = lagged_front(S, sh, it, p, gc);
   if (broke) {
-    if (gc > 0) settle_block(S, sh, it, gc, true, &rs);
+    if (gc > 0) settle_block(S, sh, it, gc, true);
     return;
   }
   const double beta = sh.beta;
   // T block in shared memory when it fits (p x p, row stride p): the two
   // triangular mat-vecs then run at smem latency (launch sets the size)
   const bool st = use_smem;
-  const int lt = rs.ldT > 0 ? rs.ldT : p;
-  if (st && !rs.resident) {
+  if (st) {
     for (int e = t; e < (p - 1) * (p - 1); e += blockDim.x) {
       const int j = e / (p - 1), l = e - j * (p - 1);
-      sT[j * lt + l] = S.T[(int64_t)j * cap + l];
+      sT[j * p + l] = S.T[(int64_t)j * cap + l];
     }
   }
   // T[:p-1, p-1] = -(T[:p-1, :p-1] @ (G[:p-1, 0] / beta));  T[p-1, p-1] = 1
   for (int e = t; e < p - 1; e += blockDim.x) sh.a[e] = __ddiv_rn(sh.a[e], beta);
   if (t == 0) sh.y[p - 1] = __ddiv_rn(sh.y[p - 1], beta);
   __syncthreads();
-  if (rs.warp_dots) {   // one warp per row j, lanes over l, butterfly sum
-    const int lane = t & 31, nw = blockDim.x >> 5;
-    for (int j = t >> 5; j < p - 1; j += nw) {
-      double acc = 0.0;
-      for (int l = j + lane; l < p - 1; l += 32)
-        acc = fma(st ? sT[j * lt + l] : S.T[(int64_t)j * cap + l], sh.a[l], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) {
-        if (st) sT[j * lt + (p - 1)] = -acc;
-        S.T[(int64_t)j * cap + (p - 1)] = -acc;
-      }
+  for (int j = t; j < p - 1; j += blockDim.x) {
+    double acc = 0.0;
+    if (st) {
+      for (int l = j; l < p - 1; ++l) acc = fma(sT[j * p + l], sh.a[l], acc);
+      sT[j * p + (p - 1)] = -acc;
+    } else {
+      for (int l = j; l < p - 1; ++l) acc = fma(S.T[(int64_t)j * cap + l], sh.a[l], acc);
     }
-  } else {
-    for (int j = t; j < p - 1; j += blockDim.x) {
-      double acc = 0.0;
-      if (st) {
-        for (int l = j; l < p - 1; ++l) acc = fma(sT[j * lt + l], sh.a[l], acc);
-        sT[j * lt + (p - 1)] = -acc;
-      } else {
-        for (int l = j; l < p - 1; ++l) acc = fma(S.T[(int64_t)j * cap + l], sh.a[l], acc);
-      }
-      S.T[(int64_t)j * cap + (p - 1)] = -acc;
-    }
+    S.T[(int64_t)j * cap + (p - 1)] = -acc;
   }
   if (t == 0) {
     S.T[(int64_t)(p - 1) * cap + (p - 1)] = 1.0;
     if (st) {
-      sT[(p - 1) * lt + (p - 1)] = 1.0;
-      for (int l = 0; l < p - 1; ++l) sT[(p - 1) * lt + l] = 0.0;
+      sT[(p - 1) * p + (p - 1)] = 1.0;
+      for (int l = 0; l < p - 1; ++l) sT[(p - 1) * p + l] = 0.0;
     }
   }
   __syncthreads();
-  small_stamp(&rs, 1);
   // c = T[:p,:p]^T y  (/beta);  R[:p, p] = c
-  if (rs.warp_dots) {
-    const int lane = t & 31, nw = blockDim.x >> 5;
-    for (int j = t >> 5; j < p; j += nw) {
-      double acc = 0.0;
-      for (int l = lane; l <= j; l += 32)
-        acc = fma(st ? sT[l * lt + j] : S.T[(int64_t)l * cap + j], sh.y[l], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) {
-        if (ks) acc = __ddiv_rn(acc, beta);
-        S.coef[j] = acc;
-        S.R[(int64_t)j * cap + p] = acc;
-        if (rs.coef) rs.coef[j] = acc;
-      }
+  for (int j = t; j < p; j += blockDim.x) {
+    double acc = 0.0;
+    if (st) {
+      for (int l = 0; l <= j; ++l) acc = fma(sT[l * p + j], sh.y[l], acc);
+    } else {
+      for (int l = 0; l <= j; ++l) acc = fma(S.T[(int64_t)l * cap + j], sh.y[l], acc);
     }
-  } else {
-    for (int j = t; j < p; j += blockDim.x) {
-      double acc = 0.0;
-      if (st) {
-        for (int l = 0; l <= j; ++l) acc = fma(sT[l * lt + j], sh.y[l], acc);
-      } else {
-        for (int l = 0; l <= j; ++l) acc = fma(S.T[(int64_t)l * cap + j], sh.y[l], acc);
-      }
-      if (ks) acc = __ddiv_rn(acc, beta);
-      S.coef[j] = acc;
-      S.R[(int64_t)j * cap + p] = acc;
-      if (rs.coef) rs.coef[j] = acc;
-    }
+    if (ks) acc = __ddiv_rn(acc, beta);
+    S.coef[j] = acc;
+    S.R[(int64_t)j * cap + p] = acc;
   }
-  small_stamp(&rs, 2);
-  if (gc > 0) settle_block(S, sh, it, gc, false, &rs);
+  if (gc > 0) settle_block(S, sh, it, gc, false);
 }
 
 }  // namespace lsb
