@@ -13,21 +13,25 @@
 //   row CTAs: SpMV of the own rows (CSR, u of every row read from its
 //     owner CTA through distributed shared memory, numpy row order = the
 //     K7 bits), partial [Q^T u, Q^T w] of the own rows, pushed into the
-//     control CTA's shared memory by DSMEM stores
-//   -> cluster barrier (1); the control CTA sums the partials in rank order
-//      and runs K5: warp 0 the breakdown test, warps 1..15 the T column and
-//      c = T^T y / beta (persist_small; same arithmetic as mgs_small_body)
-//   -> cluster barrier (2); row CTAs read beta, c and the flags over DSMEM
-//      and apply the K2 row update; the control CTA arrives at barrier (3)
-//      at once and folds the Givens rotation meanwhile (pipeline2's
-//      deferral: a convergence it finds cancels the next iteration at
-//      barrier (2), so the stop semantics are exact)
+//     control CTA's shared memory with st.async (completion counted in
+//     bytes on the control CTA's mbarrier: the row CTA does not wait)
+//   -> handoff (1): the control CTA waits on its mbarrier, sums the
+//      partials in rank order and runs K5: warp 0 the breakdown test, warps
+//      1..15 the T column and c = T^T y / beta (persist_small; same
+//      arithmetic as mgs_small_body), then pushes c, beta and the flags
+//      into every row CTA the same way
+//   -> handoff (2): row CTAs wait on their own mbarrier and apply the K2 row
+//      update; the control CTA arrives at cluster barrier (3) at once and
+//      folds the Givens rotation meanwhile (pipeline2's deferral: a
+//      convergence it finds cancels the next iteration at handoff (2), so
+//      the stop semantics are exact)
 //   -> cluster barrier (3) (the next SpMV reads the updated column).
-// Three cluster barriers per iteration replace four kernel launches and
-// three grid-wide last-CTA reductions.  Barriers are release/acquire at
-// cluster scope and only shared memory is written inside the loop, so no
-// barrier waits for global stores (each barrier.cluster.arrive.release
-// waits for the CTA's outstanding stores).
+// Two point-to-point handoffs and one cluster barrier per iteration replace
+// four kernel launches and three grid-wide last-CTA reductions (measured on
+// this B200, tools/micro: a st.async push + reply round trip ~900 cycles at
+// 16 CTAs; a release/acquire cluster barrier 490, 1,057 after a DSMEM
+// store).  Only shared memory is written inside the loop, so the barrier's
+// release never waits for global stores.
 //
 // Results: SpMV, beta, T, c, Givens and the K2 row expression follow the
 // per-iteration kernels; the mdot sums (per-CTA warp trees + rank-ordered
@@ -62,6 +66,39 @@ __device__ __forceinline__ void cluster_barrier() {
       "barrier.cluster.arrive.release.aligned;\n\t"
       "barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// st.async: a store into another CTA's shared memory whose completion is
+// counted (in bytes) on that CTA's mbarrier -- the producer does not wait,
+// the consumer waits on its own barrier (no cluster-wide rendezvous).
+__device__ __forceinline__ uint32_t mapa_u32(const void* local_smem, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(r)
+               : "r"((uint32_t)__cvta_generic_to_shared(local_smem)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_v2(uint32_t dst, double a, double b, uint32_t bar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+          dst),
+      "d"(a), "d"(b), "r"(bar)
+      : "memory");
+}
+// Consumer side of a handoff.  A handoff that never completes is a bug;
+// trap (a loud launch failure) after ~1 s instead of hanging the device.
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, unsigned parity) {
+  unsigned done = 0;
+  long long spins = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity)
+        : "memory");
+    if (++spins > (1LL << 24)) __trap();
+  }
+}
+
 __device__ __forceinline__ void cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }
@@ -243,7 +280,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
   const StateLayout SL = StateLayout::make(cap, m);
   extern __shared__ __align__(16) double dyn[];
   double* Vs = dyn;                          // cap columns x rows: own rows of V
-  double* allp = Vs + (size_t)cap * rows;    // [16][2*cap]: every CTA's [Q^T u, Q^T w]
+  double* allp = Vs + (((size_t)cap * rows + 1) & ~(size_t)1);   // [16][2*cap]: every CTA's [Q^T u, Q^T w]
                                              // (pushed into CTA 0's copy over DSMEM)
   double* sc = allp + kPMaxCluster * 2 * cap;  // cap: coefficients (row CTAs' copy)
   double* st = sc + cap;                     // SL.total: the small state (CTA 0)
@@ -257,6 +294,8 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
   // iteration (K2 skipped, cycle over), [2] this iteration runs (0 when the
   // previous iteration's deferred Givens fold stopped the cycle)
   __shared__ double s_pub[3];
+  __shared__ __align__(16) double s_pubr[4];   // row CTAs: CTA 0's pushed s_pub
+  __shared__ __align__(8) uint64_t mb1, mb2;    // partials in (CTA 0) / coef + pub in (row CTAs)
   __shared__ int s_go, s_stop;
   // CTA 0 is the control CTA (reductions, small state, Givens fold) and
   // owns no rows; row block b lives in CTA b + 1
@@ -311,9 +350,13 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
     s_go = !(stop < 0 || (broke >= 0 && broke < 0));   // gated_off(flags, 0)
     s_stop = 0;
   }
-  const double* pub0 = cl.map_shared_rank(s_pub, 0);
-  const double* coef0 = cl.map_shared_rank(st + SL.coef, 0);
-  double* allp0 = cl.map_shared_rank(allp, 0) + crank * 2 * cap;   // this CTA's slot at CTA 0
+  if (tid == 0) {
+    mbar_init(&mb1, 1);
+    mbar_init(&mb2, 1);
+    mbar_fence_init();
+  }
+  const uint32_t allp0 = mapa_u32(allp + crank * 2 * cap, 0);   // this CTA's slot at CTA 0
+  const uint32_t mb1_0 = mapa_u32(&mb1, 0);
   long long tr[kTraceSlots] = {0};
   long long tc = 0;
   bool bad = false;
@@ -326,6 +369,8 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
     if (!s_go) break;    // the cycle was stopped before it began (same in every CTA)
     const bool tw = trace && crank == 1 && tid == 0 && i > 0;
     if (tw) tc = clock64();
+    // row CTAs expect this iteration's coefficients + flags from CTA 0
+    if (crank != 0 && tid == 0) mbar_arrive_tx(&mb2, (unsigned)(8 * (((p + 1) & ~1) + 4)));
     double* su = Vs + (size_t)(p - 1) * rows;   // u = V[:, p-1], own rows
     double* sw = Vs + (size_t)p * rows;         // w = V[:, p]
 
@@ -345,7 +390,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
 
     // ---- partial [Q^T u, Q^T w] of the own rows: warp wid takes columns
     // wid, wid + 16, ...; lanes stride the rows
-    for (int k = wid; k < p; k += kPWarps) {
+    for (int k = wid; k < p && crank != 0; k += kPWarps) {
       const double* q = Vs + (size_t)k * rows;
       double a = 0.0, b = 0.0;
 #pragma unroll 4
@@ -356,14 +401,10 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
       }
       a = warp_sum(a);
       b = warp_sum(b);
-      if (lane == 0) {   // straight into CTA 0's shared memory (DSMEM store)
-        allp0[2 * k] = a;
-        allp0[2 * k + 1] = b;
-      }
+      if (lane == 0)     // into CTA 0's shared memory, counted on its barrier
+        st_async_v2(allp0 + 16u * (uint32_t)k, a, b, mb1_0);
     }
     if (tw) { const long long t = clock64(); tr[0] += t - tc; tc = t; }
-    cluster_barrier();   // (1) every CTA's partials are complete
-    if (tw) { const long long t = clock64(); tr[1] += t - tc; tc = t; }
 
     // ---- CTA 0: cluster sum in rank order (the partials already sit in
     // its shared memory), then the K5 small state -- all of it resident in
@@ -375,6 +416,10 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
     long long c0a = 0;
     if (tc0) c0a = clock64();
     if (crank == 0) {
+      // (1) every row CTA's partials have landed (always waited: no st.async
+      // may still be in flight into this CTA when the cycle ends)
+      if (tid == 0) mbar_arrive_tx(&mb1, (unsigned)(16 * p * (csize - 1)));
+      mbar_wait_acq_cluster(&mb1, (unsigned)(i & 1));
       if (!s_stop) {
         for (int e = tid; e < 2 * p; e += kPT) {
           double acc = 0.0;
@@ -399,11 +444,29 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
         s_pub[1] = sh.broke ? 1.0 : 0.0;
         s_pub[2] = s_stop ? 0.0 : 1.0;
       }
+      __syncthreads();
+      // (2) push coefficients + flags into every row CTA (st.async, counted
+      // on the row CTA's mb2); the full byte count even when stopping
+      const int pe = (p + 1) & ~1, per = pe / 2 + 2;
+      for (int e = tid; e < (csize - 1) * per; e += kPT) {
+        const int c = 1 + e / per, q = e - (c - 1) * per;
+        const uint32_t bar = mapa_u32(&mb2, c);
+        if (q < pe / 2)
+          st_async_v2(mapa_u32(sc + 2 * q, c), L.coef[2 * q], L.coef[2 * q + 1], bar);
+        else if (q == pe / 2)
+          st_async_v2(mapa_u32(s_pubr, c), s_pub[0], s_pub[1], bar);
+        else
+          st_async_v2(mapa_u32(s_pubr + 2, c), s_pub[2], 0.0, bar);
+      }
     }
     if (tc0) { const long long t = clock64(); tr[11] += t - c0a; c0a = t; }
-    cluster_barrier();   // (2) coef, beta, breakdown and the stop decision are published
-    if (tc0) { const long long t = clock64(); tr[12] += t - c0a; tr[13] += 1; }
+    const double* pub0 = s_pub;
+    if (crank != 0) {
+      mbar_wait_acq_cluster(&mb2, (unsigned)(i & 1));
+      pub0 = s_pubr;
+    }
     if (tw) { const long long t = clock64(); tr[2] += t - tc; tc = t; }
+    if (tc0) { const long long t = clock64(); tr[12] += t - c0a; tr[13] += 1; }
     if (pub0[2] == 0.0) break;             // fold i-1 converged: no iteration i
     if (pub0[1] != 0.0) {                  // breakdown: K2 skipped, cycle over
       if (crank == 0 && i > 0) settle_block(L, sh, i, i, true, /*resident=*/true);
@@ -426,8 +489,6 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
       // ---- K2 on the own rows (gram_schmidt.py:230-242; lagged_update_kernel's
       // row expression)
       const double beta = pub0[0];
-      for (int k = tid; k < p; k += kPT) sc[k] = coef0[k];
-      __syncthreads();
       const double cu = sc[p - 1];
       for (int j = tid; j < nr; j += kPT) {
         double acc = 0.0;
@@ -493,7 +554,7 @@ static int persist_plan(int64_t n, int cap, int m, int* rows_out, size_t* smem_o
   if (csize < 2) csize = 2;
   if (csize > kPMaxCluster) csize = kPMaxCluster;
   const int64_t rows = (n + csize - 2) / (csize - 1);
-  const size_t smem = sizeof(double) * ((size_t)cap * rows + (2 * kPMaxCluster + 3) * cap +
+  const size_t smem = sizeof(double) * ((size_t)cap * rows + 1 + (2 * kPMaxCluster + 3) * cap +
                                         StateLayout::make(cap, m).total);
   if (smem > kPMaxSmem) return 0;
   // what is left stages the CTA's CSR rows (12 B per nonzero + row offsets)
