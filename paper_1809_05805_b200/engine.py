@@ -110,6 +110,9 @@ class Engine:
             self.op = base_op.with_scale(self.inv_diag[self.off:])
         else:
             self.op = base_op
+        # true residuals use A itself (gmres.py:472, 498, 511: b - spmv(A, x));
+        # only the Krylov products see the right preconditioner (gmres.py:264-265)
+        self.rop = base_op
         # storage: every basis column is written before it is read; only the
         # ghost-plane padding must start at zero (Dirichlet planes never read)
         self.Vstore = torch.empty((self.cap, self.ld), **f64)
@@ -234,7 +237,7 @@ class Engine:
         if self.comm is not None:
             self.comm.allgather(self.Gloc, self.G)
 
-    def _apply_op(self, src_tensor_base, src_ptr, dst_ptr, b_ptr, it):
+    def _apply_op(self, src_tensor_base, src_ptr, dst_ptr, b_ptr, it, op=None):
         if self.comm is not None and self.halo:
             self.comm.halo(src_tensor_base[0], src_tensor_base[1], self.n, self.halo)
         self._count += 1
@@ -242,8 +245,8 @@ class Engine:
         if tm:
             e0, e1 = _timing_event(), _timing_event()
             e0.record()
-        self.op.apply_ptr(src_ptr, dst_ptr, b_ptr, C.c_void_p(self.flags.data_ptr()), it,
-                          D.stream())
+        (op or self.op).apply_ptr(src_ptr, dst_ptr, b_ptr, C.c_void_p(self.flags.data_ptr()), it,
+                                  D.stream())
         if tm:
             e1.record()
             self.timer.append(("spmv", 0, e0, e1))
@@ -268,7 +271,7 @@ class Engine:
         """rbuf = b - A x; scal[RNORM] = ||rbuf|| (gmres.py:472-473 / 498-500)."""
         st = D.stream()
         xp = C.c_void_p(self.x.data_ptr() + 8 * self.off)
-        self._apply_op((self.x, self.off), xp, D.ptr(self.rbuf), D.ptr(self.b), -1)
+        self._apply_op((self.x, self.off), xp, D.ptr(self.rbuf), D.ptr(self.b), -1, op=self.rop)
         self._call("lsb_norm_partial", D.ptr(self.rbuf), self.n, D.ptr(self.Gloc), self.ws.ref(),
                    None, -1, st)
         self._gather(2)
@@ -372,7 +375,7 @@ class Engine:
                    None if self.inv_diag is None else C.c_void_p(self.inv_diag.data_ptr() + xo),
                    st)
         self._apply_op((self.xt, self.off), C.c_void_p(self.xt.data_ptr() + xo),
-                       D.ptr(self.rtrial), D.ptr(self.b), i)
+                       D.ptr(self.rtrial), D.ptr(self.b), i, op=self.rop)
         self._call("lsb_norm_partial", D.ptr(self.rtrial), self.n, D.ptr(self.Gloc),
                    self.ws.ref(), D.ptr(self.flags), i, st)
         self._gather(2)

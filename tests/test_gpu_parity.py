@@ -433,6 +433,37 @@ def test_jacobi_preconditioner_identity(P):
     assert np.allclose(x, [2.0, 2.0, 2.0], rtol=1e-12)
 
 
+@pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2", "mgs_l1", "cgs2", "pipeline2"])
+@pytest.mark.parametrize("persist", ["0", "1"])
+def test_jacobi_restarts_match_oracle(P, monkeypatch, meth, persist):
+    """Right Jacobi preconditioning over several restarts on a matrix with a
+    varying diagonal: the restart residuals are b - A x with A itself
+    (gmres.py:472/498/511), the Krylov products A M^-1 v (gmres.py:264-265).
+    Same iteration count, outcome and cycle starts as the oracle, curve
+    within 1e-10, same final true residual and x."""
+    monkeypatch.setenv("LSB_PERSISTENT", persist)
+    O = orc.laplace2d(24)
+    rng = np.random.default_rng(8)
+    vals = O.values.copy()
+    rows = np.repeat(np.arange(O.n_rows), np.diff(O.row_ptr))
+    diag = O.col_idx == rows
+    vals[diag] += rng.uniform(0.0, 6.0, O.n_rows)            # diagonal 4 .. 10
+    Oj = orc.Csr(O.n_rows, O.n_cols, O.row_ptr, O.col_idx, vals)
+    A = P.CsrMatrix(O.n_rows, O.n_cols, O.row_ptr, O.col_idx, vals)
+    b = orc.rhs_random(O.n_rows, 5)
+    ref = orc.gmres(Oj, b, meth, 10, 200, 1e-10, jacobi=True)
+    cfg = P.GmresConfig(restart_m=10, max_restarts=200, rel_tol=1e-10, method=meth,
+                        precond="jacobi")
+    x, h = P.solve(A, b, config=cfg, diagnostics_every=0)
+    c, cr = h.implicit_curve(), np.array(ref.curve)
+    assert len(c) == len(cr) and h.outcome == ref.outcome and h.cycle_starts == ref.cycle_starts
+    big = cr > 1e-8 * cr[0]   # below: restart residuals at the tolerance are cancellation noise
+    assert np.max(np.abs(c - cr)[big] / cr[big]) <= 1e-10
+    assert np.max(np.abs(c - cr)[~big], initial=0.0) <= 1e-14 * cr[0]
+    assert abs(h.final_true_rel_res - ref.final_true_rel_res) <= 1e-3 * ref.final_true_rel_res + 1e-15
+    assert np.linalg.norm(x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+
+
 def test_device_inputs_stay_on_device(P):
     A = P.gen_laplace3d(16)
     b = torch.as_tensor(P.gen_rhs("random", A, 42), device="cuda")
@@ -830,7 +861,9 @@ def test_persistent_cycle_matches_per_iteration_kernels(P, monkeypatch, kind, me
     assert [(e.kind, e.scalar_count, e.iteration) for e in l0.events] == \
         [(e.kind, e.scalar_count, e.iteration) for e in l1.events]
     big = c0 > 1e-8 * c0[0]   # below: restart residuals at the tolerance are cancellation noise
-    assert np.max(np.abs(c0 - c1)[big] / c0[big]) <= 1e-10
+    # each path is within 1e-10 of the reference (test_c1_laplace2d64_history,
+    # test_jacobi_restarts_match_oracle); against each other: 2e-10
+    assert np.max(np.abs(c0 - c1)[big] / c0[big]) <= 2e-10
     assert np.max(np.abs(c0 - c1)[~big], initial=0.0) <= 1e-14 * c0[0]
     assert np.linalg.norm(x1 - x0) <= 1e-8 * max(np.linalg.norm(x0), 1e-300)
 
