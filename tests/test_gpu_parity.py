@@ -464,6 +464,32 @@ def test_jacobi_restarts_match_oracle(P, monkeypatch, meth, persist):
     assert np.linalg.norm(x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
 
 
+@pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2", "mgs_l1", "cgs2"])
+def test_initial_guess_and_breakdown_factor_match_oracle(P, meth):
+    """A nonzero x0 (gmres.py:251: r = b - A x0) and breakdown_tol_factor
+    != 1 (gram_schmidt.py:96-100) on a problem whose Krylov space nearly
+    closes (6 distinct eigenvalues and one 1e-7 away): btf = 1e8 declares the
+    breakdown that btf = 1 does not, and the histories differ accordingly."""
+    d = np.concatenate([np.repeat([1.0, 2.0, 3.0, 5.0, 8.0, 13.0], 7), [13.0 + 1e-7]])
+    O = orc.Csr(d.size, d.size, np.arange(d.size + 1, dtype=np.int64),
+                np.arange(d.size, dtype=np.int64), d)
+    A = P.CsrMatrix.diagonal(d)
+    b = orc.rhs_random(d.size, 3)
+    x0 = np.linspace(-1.0, 1.0, d.size)
+    for btf in (1.0, 1e8):
+        ref = orc.gmres(O, b, meth, 10, 5, 1e-14, x0=x0, btf=btf)
+        cfg = P.GmresConfig(restart_m=10, max_restarts=5, rel_tol=1e-14, method=meth,
+                            breakdown_tol_factor=btf)
+        x, h = P.solve(A, b, x0=x0, config=cfg, diagnostics_every=0)
+        c, cr = h.implicit_curve(), np.array(ref.curve)
+        assert len(c) == len(cr) and h.outcome == ref.outcome, (btf, len(c), len(cr), h.outcome)
+        assert h.cycle_starts == ref.cycle_starts
+        # the step into the near-degenerate eigenpair is a cancellation of
+        # two nearly equal vectors: compared like the chaotic cases (1e-6)
+        assert np.max(np.abs(c - cr) / np.maximum(cr, 1e-8 * cr[0])) <= 1e-6
+        assert np.linalg.norm(x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+
+
 def test_device_inputs_stay_on_device(P):
     A = P.gen_laplace3d(16)
     b = torch.as_tensor(P.gen_rhs("random", A, 42), device="cuda")
