@@ -233,6 +233,20 @@ int lsb_settle(const lsb_arnoldi* S, int32_t it, int32_t col, void* stream);
  * not fit (lsb_cycle_persistent_fits) or the state is multi-rank. */
 int lsb_cycle_persistent(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_scale,
                          void* stream);
+/* Whole restarted solve in one cluster launch: cycles (iterations as
+ * lsb_cycle_persistent) each followed on the device by the cycle
+ * epilogue -- least squares (lsb_cycle_lsq), x += M^-1 V y
+ * (lsb_cycle_extract), r = b - A x, ||r|| (lsb_norm_partial/finish),
+ * restart test (lsb_restart_check) -- and, unless the cycle stopped, the
+ * next prologue (V[:,0] = r/||r||, lsb_cycle_begin).  Call after the host
+ * prologue and the first lsb_scale_div + lsb_cycle_begin.  x (local rows,
+ * updated in place) and b are device vectors; log receives, per cycle run,
+ * m + 22 doubles: the 8 flag ints (4 doubles' bytes), res[0..m], the
+ * LSB_S_COUNT scalars, then 1.0 (unwritten reports stay as the caller left
+ * them).  The cycles stop exactly where the host restart shell would
+ * (gmres.py:470-516). */
+int lsb_solve_persistent(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_scale, double* x,
+                         const double* b, double* log, int32_t max_cycles, void* stream);
 /* 1 if an n-row, cap-column cycle fits one cluster's shared memory
  * (n * cap <= ~450K doubles, cap <= 128), else 0.  No device needed. */
 int lsb_cycle_persistent_fits(int64_t n, int32_t cap);

@@ -54,7 +54,8 @@ int launch_stencil(const lsb_stencil*, const double*, const double*, double*, ls
 int launch_csr(const lsb_csr*, const double*, const double*, double*, lsb_flags*, int,
                cudaStream_t);
 int launch_mgs_lvl2_small(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
-int launch_cycle_persistent(const lsb_arnoldi&, const lsb_csr*, int, cudaStream_t);
+int launch_cycle_persistent(const lsb_arnoldi&, const lsb_csr*, int, cudaStream_t, double*,
+                            const double*, double*, int);
 int persist_fits(int64_t, int);
 int persist_trace(long long*, int);
 int launch_cgs2_small_a(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
@@ -178,7 +179,14 @@ int lsb_cycle_persistent(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_
                          void* stream) {
   if (int rc = check_arnoldi(S)) return rc;
   if (!A) return LSB_EINVAL;
-  return launch_cycle_persistent(*S, A, krylov_scale, S_(stream));
+  return launch_cycle_persistent(*S, A, krylov_scale, S_(stream), nullptr, nullptr, nullptr, 1);
+}
+
+int lsb_solve_persistent(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_scale, double* x,
+                         const double* b, double* log, int32_t max_cycles, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (!A || !x || !b || !log || max_cycles < 1) return LSB_EINVAL;
+  return launch_cycle_persistent(*S, A, krylov_scale, S_(stream), x, b, log, max_cycles);
 }
 
 int lsb_cycle_persistent_fits(int64_t n, int32_t cap) { return persist_fits(n, cap); }

@@ -43,6 +43,10 @@
 #include "small_body.cuh"
 #include "tile.cuh"
 
+#ifndef LSB_PERSIST_REFNORM
+#define LSB_PERSIST_REFNORM 1
+#endif
+
 namespace lsb {
 
 namespace cgx = cooperative_groups;
@@ -270,9 +274,22 @@ __device__ void persist_small(const lsb_arnoldi& L, SmallShared& sh, double* scr
   if (stamps && t == 0) stamps[3] = clock64();
 }
 
+// Multi-cycle mode (x != nullptr): after each cycle the kernel also runs the
+// cycle epilogue and the next cycle's prologue itself -- the least squares
+// (cycle_lsq), x += M^-1 V y (extract), the restart residual b - A x and its
+// norm, the restart test -- logging one report per cycle for the host, so a
+// whole restarted solve is one launch.
+struct PersistSolve {
+  double* x;          // local rows of the iterate (global), nullptr: one cycle only
+  const double* b;    // local rows of b
+  double* log;        // max_cycles reports of kLogStride(m) doubles
+  int max_cycles;
+};
+__host__ __device__ inline int log_stride(int m) { return 4 + (m + 1) + LSB_S_COUNT + 1; }
+
 __global__ void __launch_bounds__(kPT, 1)
 persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, int stage_cap,
-                     bool trace) {
+                     bool trace, PersistSolve PS) {
   cgx::cluster_group cl = cgx::this_cluster();
   const int crank = (int)cl.block_rank(), csize = (int)cl.num_blocks();
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -280,7 +297,11 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
   const StateLayout SL = StateLayout::make(cap, m);
   extern __shared__ __align__(16) double dyn[];
   double* Vs = dyn;                          // cap columns x rows: own rows of V
-  double* allp = Vs + (((size_t)cap * rows + 1) & ~(size_t)1);   // [16][2*cap]: every CTA's [Q^T u, Q^T w]
+  double* xs = Vs + (size_t)cap * rows;      // rows: x (multi-cycle; read remotely at xoff)
+  double* bs = xs + rows;                    // rows: b
+  double* rs = bs + rows;                    // rows: the restart residual
+  const size_t xoff = (size_t)cap * rows;
+  double* allp = Vs + (((size_t)(cap + 3) * rows + 1) & ~(size_t)1);   // [16][2*cap]: every CTA's [Q^T u, Q^T w]
                                              // (pushed into CTA 0's copy over DSMEM)
   double* sc = allp + kPMaxCluster * 2 * cap;  // cap: coefficients (row CTAs' copy)
   double* st = sc + cap;                     // SL.total: the small state (CTA 0)
@@ -297,6 +318,8 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
   __shared__ __align__(16) double s_pubr[4];   // row CTAs: CTA 0's pushed s_pub
   __shared__ __align__(8) uint64_t mb1, mb2;    // partials in (CTA 0) / coef + pub in (row CTAs)
   __shared__ int s_go, s_stop;
+  __shared__ __align__(16) double s_ctl[4];     // row CTAs: pushed epilogue control values
+  __shared__ __align__(16) double s_y[kPMaxCap + 2];   // row CTAs: pushed least-squares y
   // CTA 0 is the control CTA (reductions, small state, Givens fold) and
   // owns no rows; row block b lives in CTA b + 1
   const int64_t r0 = crank == 0 ? S.n : (int64_t)(crank - 1) * rows;
@@ -361,8 +384,17 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
   long long tc = 0;
   bool bad = false;
   int produced = 1;   // basis columns holding data (row CTAs)
+  const bool multi = PS.x != nullptr;
+  if (multi)
+    for (int j = tid; j < nr; j += kPT) {
+      xs[j] = PS.x[r0 + j];
+      bs[j] = PS.b[r0 + j];
+    }
+  unsigned ph1 = 0, ph2 = 0;   // completed phases of mb1 / mb2 (parity of the next wait)
   cluster_barrier();
 
+  for (int cyc = 0; cyc < (multi ? PS.max_cycles : 1); ++cyc) {
+  produced = 1;
   for (int i = 0; i <= m; ++i) {
     const int p = i + 1;
     __syncthreads();
@@ -419,7 +451,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
       // (1) every row CTA's partials have landed (always waited: no st.async
       // may still be in flight into this CTA when the cycle ends)
       if (tid == 0) mbar_arrive_tx(&mb1, (unsigned)(16 * p * (csize - 1)));
-      mbar_wait_acq_cluster(&mb1, (unsigned)(i & 1));
+      mbar_wait_acq_cluster(&mb1, ph1++ & 1u);
       if (!s_stop) {
         for (int e = tid; e < 2 * p; e += kPT) {
           double acc = 0.0;
@@ -462,7 +494,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
     if (tc0) { const long long t = clock64(); tr[11] += t - c0a; c0a = t; }
     const double* pub0 = s_pub;
     if (crank != 0) {
-      mbar_wait_acq_cluster(&mb2, (unsigned)(i & 1));
+      mbar_wait_acq_cluster(&mb2, ph2++ & 1u);
       pub0 = s_pubr;
     }
     if (tw) { const long long t = clock64(); tr[2] += t - tc; tc = t; }
@@ -506,7 +538,221 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
       if (tw) { const long long t = clock64(); tr[4] += t - tc; tr[8] += 1; }
     }
   }
-  if (bad) atomicOr(reinterpret_cast<int*>(cl.map_shared_rank(L.flags, 0)) + 4, 1);  // nonfinite
+  if (!multi) break;
+
+  // ================= cycle epilogue + next prologue (multi-cycle) =========
+  const int pe_y = (cap + 1) & ~1;
+  // row CTAs arm for the least-squares push; the control CTA for the
+  // residual-norm partials -- before the barrier that precedes those pushes
+  if (crank != 0 && tid == 0) mbar_arrive_tx(&mb2, (unsigned)(8 * (pe_y + 2)));
+  if (crank == 0 && tid == 0) mbar_arrive_tx(&mb1, (unsigned)(32 * (csize - 1)));
+  cluster_barrier();
+  if (crank == 0) {
+    // (E1) least squares on the rotated triangle (cycle_lsq_kernel,
+    // gmres.py:184-192 / 294-297): y into scratch, k and status in flags
+    if (wid == 0) {
+      const int stop = L.flags->stop_iter;
+      const int k = L.flags->status == LSB_GHYSELS_CHECK ? 0 : (stop == LSB_NO_STOP ? m : stop);
+      if (lane == 0) L.flags->k = k;
+      __syncwarp();
+      for (int ii = k - 1; ii >= 0; --ii) {
+        const double dd = L.tri[(int64_t)ii * m + ii];
+        if (dd == 0.0) {
+          if (lane == 0) { L.flags->status = LSB_SINGULAR; L.flags->k = ii; }
+          break;
+        }
+        double acc = 0.0;
+        for (int j = ii + 1 + lane; j < k; j += 32) acc = fma(L.tri[(int64_t)ii * m + j], scratch[j], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) scratch[ii] = __ddiv_rn(L.g[ii] - acc, dd);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // (E2) y, k and the status into every row CTA
+    const int kk = L.flags->k, stt = L.flags->status, per = pe_y / 2 + 1;
+    for (int e = tid; e < (csize - 1) * per; e += kPT) {
+      const int c = 1 + e / per, q = e - (c - 1) * per;
+      const uint32_t bar = mapa_u32(&mb2, c);
+      if (q < pe_y / 2)
+        st_async_v2(mapa_u32(s_y + 2 * q, c), 2 * q < kk ? scratch[2 * q] : 0.0,
+                    2 * q + 1 < kk ? scratch[2 * q + 1] : 0.0, bar);
+      else
+        st_async_v2(mapa_u32(s_ctl, c), (double)kk, (double)stt, bar);
+    }
+  } else {
+    mbar_wait_acq_cluster(&mb2, ph2++ & 1u);
+    // (E3) x += M^-1 V_k y on the own rows (extract_kernel's expression)
+    const int kk = (int)s_ctl[0], stt = (int)s_ctl[1];
+    if (kk >= 1 && stt != LSB_SINGULAR)
+      for (int j = tid; j < nr; j += kPT) {
+        double acc = 0.0;
+        for (int jj = 0; jj < kk; ++jj) acc = fma(s_y[jj], Vs[(size_t)jj * rows + j], acc);
+        if (A.col_scale) acc = __dmul_rn(acc, A.col_scale[r0 + j]);
+        xs[j] = xs[j] + acc;
+      }
+    // the next pushes from the control CTA: the rescale decision
+    if (tid == 0) mbar_arrive_tx(&mb2, 16u);
+  }
+  cluster_barrier();   // x complete everywhere (the residual SpMV reads neighbours' x)
+  {
+    // (E4) r = b - A x on the own rows (A itself: gmres.py:498), then the
+    // (max |r|, sum r^2) partial of norm_partial_kernel
+    __shared__ double s_red[kPWarps][2];
+    __shared__ int s_bad;
+    double am = 0.0, ss = 0.0;
+    for (int j = tid; j < nr; j += kPT) {
+      const int lo = rowp[rbase + j], hi = rowp[rbase + j + 1];
+      const double sx = row_sum_fast(CsrRowAccCluster{colp + lo, valp + lo, nullptr, s_peer, xoff,
+                                                      rdiv, rows},
+                                     hi - lo);
+      if (!isfinite(sx)) bad = true;
+      const double v = __dsub_rn(bs[j], sx);
+      rs[j] = v;
+      am = fmax(am, fabs(v));
+      if (isnan(v)) am = v;
+      ss = fma(v, v, ss);
+    }
+    am = warp_max(am);
+    ss = warp_sum(ss);
+    if (lane == 0) { s_red[wid][0] = am; s_red[wid][1] = ss; }
+    const int anybad = __syncthreads_or(bad ? 1 : 0);
+    if (crank != 0 && tid == 0) {
+      double a = s_red[0][0], q = s_red[0][1];
+      for (int w = 1; w < kPWarps; ++w) { a = fmax(a, s_red[w][0]); if (isnan(s_red[w][0])) a = s_red[w][0]; q += s_red[w][1]; }
+      st_async_v2(allp0, a, q, mb1_0);
+      st_async_v2(allp0 + 16u, anybad ? 1.0 : 0.0, 0.0, mb1_0);
+    }
+    bad = false;
+    (void)s_bad;
+  }
+  // (E5) the control CTA: the restart norm (norm_finish_kernel), with the
+  // exact power-of-two rescale pass when max|r| leaves [2^-450, 2^450]
+  __shared__ double s_nrm[3];   // rnorm, rescale flag, scale
+  if (crank == 0) {
+    mbar_wait_acq_cluster(&mb1, ph1++ & 1u);
+    if (tid == 0) {
+      double amax = allp[1 * 2 * cap], ssq = allp[1 * 2 * cap + 1];
+      int nf = allp[1 * 2 * cap + 2] != 0.0;
+      for (int c = 2; c < csize; ++c) {
+        amax = fmax(amax, allp[c * 2 * cap]);
+        ssq += allp[c * 2 * cap + 1];
+        nf |= allp[c * 2 * cap + 2] != 0.0;
+      }
+      if (nf) L.flags->nonfinite = 1;
+      const double lo = 0x1p-450, hi = 0x1p450;
+#if LSB_PERSIST_REFNORM
+      (void)lo; (void)hi;
+      const bool resc = !(amax == 0.0 || isnan(amax));
+      const double sc_ = amax;
+#else
+      const bool resc = !(amax == 0.0 || isnan(amax) || (amax >= lo && amax <= hi));
+      double sc_ = 1.0;
+      if (resc) {
+        int e;
+        frexp(amax, &e);
+        sc_ = ldexp(1.0, -e);
+      }
+#endif
+      s_nrm[0] = amax == 0.0 ? 0.0 : (isnan(amax) ? amax : sqrt(ssq));
+      s_nrm[1] = resc ? 1.0 : 0.0;
+      s_nrm[2] = sc_;
+      if (resc) mbar_arrive_tx(&mb1, (unsigned)(16 * (csize - 1)));
+    }
+    __syncthreads();
+    for (int c = 1 + tid; c < csize; c += kPT)
+      st_async_v2(mapa_u32(s_ctl + 2, c), s_nrm[1], s_nrm[2], mapa_u32(&mb2, c));
+    if (s_nrm[1] != 0.0) {
+      mbar_wait_acq_cluster(&mb1, ph1++ & 1u);
+      if (tid == 0) {
+        double q = allp[1 * 2 * cap];
+        for (int c = 2; c < csize; ++c) q += allp[c * 2 * cap];
+#if LSB_PERSIST_REFNORM
+        s_nrm[0] = s_nrm[2] * sqrt(q);
+#else
+        s_nrm[0] = sqrt(q) / s_nrm[2];
+#endif
+      }
+    }
+    __syncthreads();
+    // (E6) restart test, the cycle's report, continue or stop
+    if (tid == 0) {
+      const double rn = s_nrm[0];
+      L.scal[LSB_S_RNORM] = rn;
+      L.flags->restart_ok = rn <= L.scal[LSB_S_TARGET];
+      double* rep = PS.log + (int64_t)cyc * log_stride(m);
+      const double* fl = reinterpret_cast<const double*>(L.flags);
+      for (int e = 0; e < 4; ++e) rep[e] = fl[e];
+      for (int e = 0; e <= m; ++e) rep[4 + e] = L.res[e];
+      for (int e = 0; e < LSB_S_COUNT; ++e) rep[5 + m + e] = L.scal[e];
+      rep[5 + m + LSB_S_COUNT] = 1.0;
+      const bool cont = !L.flags->nonfinite && L.flags->status == LSB_RUNNING &&
+                        L.flags->stop_iter == LSB_NO_STOP && !L.flags->restart_ok &&
+                        cyc + 1 < PS.max_cycles;
+      s_nrm[1] = cont ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int c = 1 + tid; c < csize; c += kPT)
+      st_async_v2(mapa_u32(s_ctl, c), s_nrm[1], s_nrm[0], mapa_u32(&mb2, c));
+  } else {
+    mbar_wait_acq_cluster(&mb2, ph2++ & 1u);         // rescale decision
+    if (tid == 0) mbar_arrive_tx(&mb2, 16u);          // next: continue + rnorm
+    __syncthreads();
+    if (s_ctl[2] != 0.0) {                             // rescaled sum of squares
+      __shared__ double s_q[kPWarps];
+      const double scl = s_ctl[3];
+      double q = 0.0;
+      for (int j = tid; j < nr; j += kPT) {
+#if LSB_PERSIST_REFNORM
+        const double v = __ddiv_rn(rs[j], scl);
+#else
+        const double v = rs[j] * scl;
+#endif
+        q = fma(v, v, q);
+      }
+      q = warp_sum(q);
+      if (lane == 0) s_q[wid] = q;
+      __syncthreads();
+      if (tid == 0) {
+        double a = s_q[0];
+        for (int w = 1; w < kPWarps; ++w) a += s_q[w];
+        st_async_v2(allp0, a, 0.0, mb1_0);
+      }
+    }
+    mbar_wait_acq_cluster(&mb2, ph2++ & 1u);         // continue + rnorm
+  }
+  __syncthreads();
+  const bool cont = (crank == 0 ? s_nrm[1] : s_ctl[0]) != 0.0;
+  if (!cont) break;
+  // (E7) next cycle's prologue: V[:, 0] = r / beta (scale_div) and a fresh
+  // small state with g[0] = beta (cycle_begin_kernel)
+  if (crank != 0) {
+    const double rn = s_ctl[1];
+    for (int j = tid; j < nr; j += kPT) Vs[j] = __ddiv_rn(rs[j], rn);
+  } else {
+    for (int e = tid; e < cap * cap; e += kPT) { L.R[e] = 0.0; L.T[e] = 0.0; }
+    for (int e = tid; e < (m + 1) * m; e += kPT) L.tri[e] = 0.0;
+    for (int e = tid; e < 2 * m; e += kPT) L.rot[e] = 0.0;
+    for (int e = tid; e <= m; e += kPT) { L.g[e] = 0.0; L.res[e] = 0.0; }
+    for (int e = tid; e < cap; e += kPT) L.coef[e] = 0.0;
+    __syncthreads();
+    if (tid == 0) {
+      L.g[0] = L.scal[LSB_S_RNORM];
+      L.flags->stop_iter = LSB_NO_STOP;
+      L.flags->status = LSB_RUNNING;
+      L.flags->broke_iter = -1;
+      L.flags->k = 0;
+      L.flags->restart_ok = 0;
+      s_stop = 0;
+    }
+  }
+  cluster_barrier();   // V[:, 0] everywhere, state reset
+  }   // cycles
+  if (!multi && bad)
+    atomicOr(reinterpret_cast<int*>(cl.map_shared_rank(L.flags, 0)) + 4, 1);  // nonfinite
+  if (multi) {
+    for (int j = tid; j < nr; j += kPT) PS.x[r0 + j] = xs[j];
+  }
   // the basis columns this cycle produced, own rows, back to HBM
   for (int k = 0; k < produced; ++k)
     for (int j = tid; j < nr; j += kPT) S.V[(int64_t)k * S.ld + r0 + j] = Vs[(size_t)k * rows + j];
@@ -554,7 +800,7 @@ static int persist_plan(int64_t n, int cap, int m, int* rows_out, size_t* smem_o
   if (csize < 2) csize = 2;
   if (csize > kPMaxCluster) csize = kPMaxCluster;
   const int64_t rows = (n + csize - 2) / (csize - 1);
-  const size_t smem = sizeof(double) * ((size_t)cap * rows + 1 + (2 * kPMaxCluster + 3) * cap +
+  const size_t smem = sizeof(double) * ((size_t)(cap + 3) * rows + 1 + (2 * kPMaxCluster + 3) * cap +
                                         StateLayout::make(cap, m).total);
   if (smem > kPMaxSmem) return 0;
   // what is left stages the CTA's CSR rows (12 B per nonzero + row offsets)
@@ -580,7 +826,9 @@ int persist_fits(int64_t n, int cap) {
   return persist_plan(n, cap, cap - 2, &rows, &sm) > 0;
 }
 
-int launch_cycle_persistent(const lsb_arnoldi& S, const lsb_csr* A, int ks, cudaStream_t st) {
+int launch_cycle_persistent(const lsb_arnoldi& S, const lsb_csr* A, int ks, cudaStream_t st,
+                            double* x, const double* b, double* log, int max_cycles) {
+  if (x && (!b || !log || max_cycles < 1)) return LSB_EINVAL;
   if (!A || S.g_parts != 1 || S.m + 2 > S.cap || A->n_rows != S.n || A->n_cols != S.n ||
       A->x_lo != 0 || A->nnz >= (1LL << 31))
     return LSB_ERANGE;
@@ -609,8 +857,9 @@ int launch_cycle_persistent(const lsb_arnoldi& S, const lsb_csr* A, int ks, cuda
   cfg.numAttrs = 1;
   const lsb_csr Av = *A;
   const bool trace = tuning(LSB_TUNE_PERSIST_TRACE) == 1;
+  const PersistSolve ps{x, b, log, x ? max_cycles : 1};
   cudaLaunchKernelEx(&cfg, persist_cycle_kernel, S, Av, rows, FastDiv::make((uint32_t)rows), ks,
-                     stage, trace);
+                     stage, trace, ps);
   return check_launch("cycle_persistent");
 }
 

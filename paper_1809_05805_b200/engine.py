@@ -509,6 +509,34 @@ class Engine:
                            self.h_scal.numpy().copy(),
                            self.h_true.numpy().copy() if self.true_residual else None)
 
+    def solve_cycles(self, max_cycles):
+        """Every restart cycle of the solve on the device in one cluster launch
+        (lsb_solve_persistent; needs self.persistent): the first cycle's
+        prologue as enqueue_cycle, then cycles + epilogues + restart tests
+        until the restart shell would stop.  Returns one CycleReport per cycle
+        run, as cycle() would have, in order."""
+        st = D.stream()
+        S = self.Sref
+        self._call("lsb_scale_div", D.ptr(self.rbuf), self.n,
+                   C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_RNORM), self.col_ptr(0), None, -1, st)
+        self._call("lsb_cycle_begin", S, st)
+        stride = self.m + 22
+        log = torch.zeros(max_cycles * stride, dtype=D.F64, device=self.dev)
+        self._call("lsb_solve_persistent", S, C.byref(self.pcsr.c), 1,
+                   C.c_void_p(self.x.data_ptr() + 8 * self.off), D.ptr(self.b), D.ptr(log),
+                   int(max_cycles), st)
+        host = log.cpu().numpy()
+        reports = []
+        for c in range(max_cycles):
+            rec = host[c * stride:(c + 1) * stride]
+            if rec[-1] != 1.0:
+                break
+            flags = rec[:4].copy().view(np.int32)
+            reports.append(CycleReport(flags.tolist(), rec[4:5 + self.m].copy(),
+                                       rec[5 + self.m:5 + self.m + _abi.S_COUNT].copy()))
+        self.cycles_run += len(reports)
+        return reports
+
     def hessenberg(self, k):
         """Hbar_k from the R columns (R[:, j+1] rows 0..j+1 = H[:, j])."""
         R = self.R.cpu().numpy()

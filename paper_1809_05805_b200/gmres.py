@@ -10,6 +10,8 @@ including pipeline2's depth-2 look-ahead.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -324,9 +326,18 @@ class _DeviceSolve:
         outcome = None
         saw_cancellation = False
         lagged = cfg.method in ("one_sync_mgs", "two_sync_cgs2", "pipeline2")
+        # launch-bound sizes: the whole restarted solve is one cluster launch
+        # that logs every cycle's report; the shell below replays them
+        whole = eng.persistent and os.environ.get("LSB_PERSISTENT_SOLVE", "1") != "0"
+        device_reports = iter(eng.solve_cycles(cfg.max_restarts)) if whole else None
         for _cycle in range(cfg.max_restarts):
             hist.cycle_starts.append(self.global_it)
-            rep = eng.cycle()
+            if device_reports is None:
+                rep = eng.cycle()
+            else:
+                rep = next(device_reports, None)
+                if rep is None:
+                    raise RuntimeError("device solve stopped before the restart shell")
             self._mark("cycle")
             if rep.nonfinite:
                 raise NonFiniteError("spmv result contains NaN or Inf")

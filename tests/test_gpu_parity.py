@@ -874,13 +874,24 @@ def test_persistent_cycle_matches_per_iteration_kernels(P, monkeypatch, kind, me
     assert Engine(A, m, meth, tol).persistent
     x0_in = np.linspace(-1.0, 1.0, A.n_rows) if kind == "c1" else None   # nonzero initial guess
     out = {}
-    for mode in ("0", "1"):
-        monkeypatch.setenv("LSB_PERSISTENT", mode)
+    # 0: per-iteration kernels; 1: one cluster launch per cycle; 2: the whole
+    # restarted solve in one cluster launch (lsb_solve_persistent)
+    for mode, persist, whole in (("0", "0", "0"), ("1", "1", "0"), ("2", "1", "1")):
+        monkeypatch.setenv("LSB_PERSISTENT", persist)
+        monkeypatch.setenv("LSB_PERSISTENT_SOLVE", whole)
         cfg = P.GmresConfig(restart_m=m, max_restarts=200, rel_tol=tol, method=meth, **kw)
         led = P.ReductionLedger()
         x, h = P.solve(A, b, x0=x0_in, config=cfg, ledger=led, diagnostics_every=0)
         out[mode] = (x, h, led)
-    (x0, h0, l0), (x1, h1, l1) = out["0"], out["1"]
+    _compare_runs(out["0"], out["1"])
+    _compare_runs(out["0"], out["2"])
+    # the two persistent forms differ only in the restart norm's summation
+    # partition (CTA row blocks vs the grid-stride norm kernel): ulp-level
+    _compare_runs(out["1"], out["2"])
+
+
+def _compare_runs(r0, r1):
+    (x0, h0, l0), (x1, h1, l1) = r0, r1
     c0, c1 = h0.implicit_curve(), h1.implicit_curve()
     assert len(c0) == len(c1) and h0.outcome == h1.outcome
     assert h0.cycle_starts == h1.cycle_starts
