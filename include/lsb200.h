@@ -242,8 +242,11 @@ int lsb_cycle_persistent(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_
  * prologue and the first lsb_scale_div + lsb_cycle_begin.  x (local rows,
  * updated in place) and b are device vectors; log receives, per cycle run,
  * m + 22 doubles: the 8 flag ints (4 doubles' bytes), res[0..m], the
- * LSB_S_COUNT scalars, then 1.0 (unwritten reports stay as the caller left
- * them).  The cycles stop exactly where the host restart shell would
+ * LSB_S_COUNT scalars, then a marker written last behind a system fence:
+ * 2.0 when another cycle follows, 1.0 for the last one (unwritten reports
+ * stay as the caller left them).  log may be mapped pinned host memory:
+ * the host can then consume each report while later cycles run.  The
+ * cycles stop exactly where the host restart shell would
  * (gmres.py:470-516). */
 int lsb_solve_persistent(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_scale, double* x,
                          const double* b, double* log, int32_t max_cycles, void* stream);

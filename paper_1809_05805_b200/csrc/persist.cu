@@ -680,12 +680,6 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
       const double rn = s_nrm[0];
       L.scal[LSB_S_RNORM] = rn;
       L.flags->restart_ok = rn <= L.scal[LSB_S_TARGET];
-      double* rep = PS.log + (int64_t)cyc * log_stride(m);
-      const double* fl = reinterpret_cast<const double*>(L.flags);
-      for (int e = 0; e < 4; ++e) rep[e] = fl[e];
-      for (int e = 0; e <= m; ++e) rep[4 + e] = L.res[e];
-      for (int e = 0; e < LSB_S_COUNT; ++e) rep[5 + m + e] = L.scal[e];
-      rep[5 + m + LSB_S_COUNT] = 1.0;
       const bool cont = !L.flags->nonfinite && L.flags->status == LSB_RUNNING &&
                         L.flags->stop_iter == LSB_NO_STOP && !L.flags->restart_ok &&
                         cyc + 1 < PS.max_cycles;
@@ -694,6 +688,22 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
     __syncthreads();
     for (int c = 1 + tid; c < csize; c += kPT)
       st_async_v2(mapa_u32(s_ctl, c), s_nrm[1], s_nrm[0], mapa_u32(&mb2, c));
+    // the cycle's report (the log may be mapped host memory that the host
+    // polls while later cycles run): payload, system fence, then the
+    // marker -- 2.0 when another cycle follows, 1.0 for the last one
+    if (wid == 0) {
+      double* rep = PS.log + (int64_t)cyc * log_stride(m);
+      const double* fl = reinterpret_cast<const double*>(L.flags);
+      for (int e = lane; e < 4 + (m + 1) + LSB_S_COUNT; e += 32)
+        rep[e] = e < 4 ? fl[e] : (e < 5 + m ? L.res[e - 4] : L.scal[e - 5 - m]);
+      __threadfence_system();
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_system();
+        *reinterpret_cast<volatile double*>(rep + 4 + (m + 1) + LSB_S_COUNT) =
+            s_nrm[1] != 0.0 ? 2.0 : 1.0;
+      }
+    }
   } else {
     mbar_wait_acq_cluster(&mb2, ph2++ & 1u);         // rescale decision
     if (tid == 0) mbar_arrive_tx(&mb2, 16u);          // next: continue + rnorm

@@ -120,33 +120,41 @@ class Engine:
             self.Vstore[:, : self.off].zero_()
             self.Vstore[:, self.off + self.n:].zero_()
         cap, m = self.cap, self.m
-        self.R = torch.zeros((cap, cap), **f64)
-        self.T = torch.zeros((cap, cap), **f64)
-        self.L = torch.zeros((cap, cap), **f64)
-        self.rot = torch.zeros(2 * m, **f64)
-        self.g = torch.zeros(m + 1, **f64)
-        self.tri = torch.zeros((m + 1) * m, **f64)
-        self.coef = torch.zeros(cap, **f64)
-        self.coef2 = torch.zeros(cap, **f64)
-        self.Gloc = torch.zeros(2 * cap, **f64)
         parts = comm.size if comm is not None else 1
-        self.G = self.Gloc if parts == 1 else torch.zeros(parts * 2 * cap, **f64)
-        self.scal = torch.zeros(_abi.S_COUNT, **f64)
-        self.res = torch.zeros(m + 1, **f64)
-        self.flags = torch.zeros(_abi.FLAGS_INTS, dtype=torch.int32, device=self.dev)
+        # the small state lives in one zeroed arena (one fill instead of a
+        # dozen allocations + fills: launch-bound solves pay per call)
+        sizes = [("R", (cap, cap)), ("T", (cap, cap)), ("L", (cap, cap)), ("rot", (2 * m,)),
+                 ("g", (m + 1,)), ("tri", ((m + 1) * m,)), ("coef", (cap,)), ("coef2", (cap,)),
+                 ("Gloc", (2 * cap,)), ("scal", (_abi.S_COUNT,)), ("res", (m + 1,)),
+                 ("flags", ((_abi.FLAGS_INTS + 1) // 2,))]
+        if parts > 1:
+            sizes.append(("G", (parts * 2 * cap,)))
+        if diagnostics:
+            sizes.append(("gram", (cap, cap)))
+        if true_residual:
+            sizes += [("ytrial", (cap,)), ("true_res", (m + 1,))]
+        offs, tot = [], 0
+        for _, shp in sizes:
+            offs.append(tot)
+            tot += D.round_up(int(np.prod(shp)), 2)
+        self._arena = torch.zeros(tot, **f64)
+        for (name, shp), o in zip(sizes, offs):
+            setattr(self, name, self._arena[o:o + int(np.prod(shp))].view(shp))
+        self.flags = self.flags.view(torch.int32)[:_abi.FLAGS_INTS]
+        if parts == 1:
+            self.G = self.Gloc
+        if not diagnostics:
+            self.gram = None
         self.ws = D.Workspace(cap, self.dev)
         self.x = self._vec_with_halo()
-        self.b = torch.zeros(self.n, **f64)
-        self.rbuf = torch.zeros(self.n, **f64)
-        self.gram = torch.zeros((cap, cap), **f64) if diagnostics else None
+        self.b = torch.empty(self.n, **f64)       # uploaded before every read
+        self.rbuf = torch.empty(self.n, **f64)    # residual: written before read
         self.diagnostics = diagnostics
         # true-residual probe buffers (true_residual_every > 0)
         self.true_residual = bool(true_residual)
         if self.true_residual:
-            self.ytrial = torch.zeros(cap, **f64)
             self.xt = self._vec_with_halo()
             self.rtrial = torch.zeros(self.n, **f64)
-            self.true_res = torch.zeros(m + 1, **f64)
             self.h_true = torch.zeros(m + 1, dtype=D.F64).pin_memory()
         self.S = _abi.Arnoldi(
             V=self.Vstore.data_ptr() + 8 * self.off, ld=self.ld, n=self.n, n_global=self.n_global,
@@ -513,29 +521,36 @@ class Engine:
         """Every restart cycle of the solve on the device in one cluster launch
         (lsb_solve_persistent; needs self.persistent): the first cycle's
         prologue as enqueue_cycle, then cycles + epilogues + restart tests
-        until the restart shell would stop.  Returns one CycleReport per cycle
-        run, as cycle() would have, in order."""
+        until the restart shell would stop.  Yields one CycleReport per cycle
+        run, as cycle() would have, in order -- each as soon as the device
+        has written it into the mapped pinned log, so the host's per-cycle
+        bookkeeping overlaps the cycles that follow."""
         st = D.stream()
         S = self.Sref
         self._call("lsb_scale_div", D.ptr(self.rbuf), self.n,
                    C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_RNORM), self.col_ptr(0), None, -1, st)
         self._call("lsb_cycle_begin", S, st)
         stride = self.m + 22
-        log = torch.zeros(max_cycles * stride, dtype=D.F64, device=self.dev)
+        log = torch.zeros(max_cycles * stride, dtype=D.F64, pin_memory=True)
         self._call("lsb_solve_persistent", S, C.byref(self.pcsr.c), 1,
-                   C.c_void_p(self.x.data_ptr() + 8 * self.off), D.ptr(self.b), D.ptr(log),
-                   int(max_cycles), st)
-        host = log.cpu().numpy()
-        reports = []
+                   C.c_void_p(self.x.data_ptr() + 8 * self.off), D.ptr(self.b),
+                   C.c_void_p(log.data_ptr()), int(max_cycles), st)
+        done = torch.cuda.Event()
+        done.record()
+        host = log.numpy()
         for c in range(max_cycles):
-            rec = host[c * stride:(c + 1) * stride]
-            if rec[-1] != 1.0:
-                break
-            flags = rec[:4].copy().view(np.int32)
-            reports.append(CycleReport(flags.tolist(), rec[4:5 + self.m].copy(),
-                                       rec[5 + self.m:5 + self.m + _abi.S_COUNT].copy()))
-        self.cycles_run += len(reports)
-        return reports
+            mark = c * stride + stride - 1
+            spins = 0
+            while host[mark] == 0.0:
+                spins += 1
+                if spins % 256 == 0 and done.query() and host[mark] == 0.0:
+                    raise RuntimeError("lsb_solve_persistent ended without report %d" % c)
+            rec = host[c * stride:(c + 1) * stride].copy()
+            self.cycles_run += 1
+            yield CycleReport(rec[:4].view(np.int32).tolist(), rec[4:5 + self.m],
+                              rec[5 + self.m:5 + self.m + _abi.S_COUNT])
+            if rec[-1] != 2.0:
+                return
 
     def hessenberg(self, k):
         """Hbar_k from the R columns (R[:, j+1] rows 0..j+1 = H[:, j])."""

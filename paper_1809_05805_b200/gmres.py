@@ -329,7 +329,7 @@ class _DeviceSolve:
         # launch-bound sizes: the whole restarted solve is one cluster launch
         # that logs every cycle's report; the shell below replays them
         whole = eng.persistent and os.environ.get("LSB_PERSISTENT_SOLVE", "1") != "0"
-        device_reports = iter(eng.solve_cycles(cfg.max_restarts)) if whole else None
+        device_reports = eng.solve_cycles(cfg.max_restarts) if whole else None
         for _cycle in range(cfg.max_restarts):
             hist.cycle_starts.append(self.global_it)
             if device_reports is None:
@@ -426,6 +426,8 @@ class _DeviceSolve:
             if beta <= target:
                 outcome = CONVERGED
                 break
+        if device_reports is not None and next(device_reports, None) is not None:
+            raise RuntimeError("device solve ran past the restart shell")
         if outcome is None:
             outcome = CANCELLATION_FAILURE if saw_cancellation else STALLED_MAXITER
         led.iteration = self.global_it
