@@ -825,6 +825,9 @@ def _persist_problem(P, kind):
     if kind == "c1":
         A = P.gen_laplace2d(64)
         return A, P.gen_rhs("random", A, 42), 30, 1e-6, {}
+    if kind == "c1_stall":           # restart budget runs out: stalled_maxiter after 3 cycles
+        A = P.gen_laplace2d(64)
+        return A, P.gen_rhs("random", A, 42), 30, 1e-6, {"max_restarts": 3}
     if kind == "c1_jacobi":
         A = P.gen_laplace2d(48)
         return A, P.gen_rhs("random", A, 7), 30, 1e-6, {"precond": "jacobi"}
@@ -861,7 +864,7 @@ def _persist_problem(P, kind):
     return A, np.ones(4), 10, 1e-14, {}
 
 
-@pytest.mark.parametrize("kind", ["c1", "c1_jacobi", "conv27_csr", "lap3d_15", "ragged_csr",
+@pytest.mark.parametrize("kind", ["c1", "c1_stall", "c1_jacobi", "conv27_csr", "lap3d_15", "ragged_csr",
                                   "gmres1", "tiny", "breakdown"])
 @pytest.mark.parametrize("meth", ["one_sync_mgs", "pipeline2"])
 def test_persistent_cycle_matches_per_iteration_kernels(P, monkeypatch, kind, meth):
@@ -879,10 +882,13 @@ def test_persistent_cycle_matches_per_iteration_kernels(P, monkeypatch, kind, me
     for mode, persist, whole in (("0", "0", "0"), ("1", "1", "0"), ("2", "1", "1")):
         monkeypatch.setenv("LSB_PERSISTENT", persist)
         monkeypatch.setenv("LSB_PERSISTENT_SOLVE", whole)
-        cfg = P.GmresConfig(restart_m=m, max_restarts=200, rel_tol=tol, method=meth, **kw)
+        cfg = P.GmresConfig(**{"restart_m": m, "max_restarts": 200, "rel_tol": tol,
+                               "method": meth, **kw})
         led = P.ReductionLedger()
         x, h = P.solve(A, b, x0=x0_in, config=cfg, ledger=led, diagnostics_every=0)
         out[mode] = (x, h, led)
+    if kind == "c1_stall":
+        assert out["2"][1].outcome == "stalled_maxiter" and len(out["2"][1].cycle_starts) == 3
     _compare_runs(out["0"], out["1"])
     _compare_runs(out["0"], out["2"])
     # the two persistent forms differ only in the restart norm's summation
