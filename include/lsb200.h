@@ -94,6 +94,24 @@ typedef struct lsb_csr {
   int64_t x_lo;          /* x is indexed by (global col - x_lo)               */
 } lsb_csr;
 
+/* Dictionary-coded CSR: the same matrix as an lsb_csr whose values take at
+ * most 256 distinct bit patterns and whose column offsets (global col -
+ * global row) take at most 256 distinct values.  Entry j of row r:
+ * value = val_tab[val_idx[j]], column = row0 + r + off_tab[off_idx[j]].
+ * 2 bytes per nonzero instead of 12 (the CSR-VI / CSR-DU idea). */
+typedef struct lsb_csr_dict {
+  int64_t n_rows, n_cols, nnz;
+  const int32_t* row_ptr;
+  const uint8_t* val_idx;
+  const uint8_t* off_idx;
+  const double* val_tab;   /* n_val entries */
+  const int32_t* off_tab;  /* n_off entries */
+  int32_t n_val, n_off;
+  const double* col_scale;
+  int64_t row0;
+  int64_t x_lo;
+} lsb_csr_dict;
+
 /* Constant-coefficient box stencil, row i = (iz*ny + iy)*nx + ix.
  * Offsets MUST be listed in increasing linear offset (= CSR column order).
  * halo_lo/halo_hi: 1 if x holds a ghost z-plane below/above the local slab
@@ -163,6 +181,11 @@ int32_t lsb_max_columns(void);           /* largest p one mdot launch takes   */
  * Sets flags->nonfinite on NaN/Inf. */
 int lsb_spmv_csr(const lsb_csr* A, const double* x, const double* b, double* y,
                  lsb_flags* flags, int32_t it, void* stream);
+/* y = A x (b == NULL) or y = b - A x for a dictionary-coded CSR; bitwise
+ * lsb_spmv_csr on the equivalent lsb_csr (same products, same numpy
+ * reduceat summation order).  Replaces the same kernels.py:256-272 call. */
+int lsb_spmv_csr_dict(const lsb_csr_dict* A, const double* x, const double* b, double* y,
+                      lsb_flags* flags, int32_t it, void* stream);
 int lsb_spmv_stencil(const lsb_stencil* S, const double* x, const double* b, double* y,
                      lsb_flags* flags, int32_t it, void* stream);
 

@@ -49,6 +49,14 @@ class Workspace(C.Structure):
                 ("pad", C.c_int32)]
 
 
+class CsrDict(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64),
+                ("row_ptr", C.c_void_p), ("val_idx", C.c_void_p), ("off_idx", C.c_void_p),
+                ("val_tab", C.c_void_p), ("off_tab", C.c_void_p), ("n_val", C.c_int32),
+                ("n_off", C.c_int32), ("col_scale", C.c_void_p), ("row0", C.c_int64),
+                ("x_lo", C.c_int64)]
+
+
 class Csr(C.Structure):
     _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64),
                 ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p),
@@ -86,6 +94,7 @@ _SIGS = {
     "lsb_partial_len": ([_I32], _I64),
     "lsb_max_columns": ([], _I32),
     "lsb_spmv_csr": ([_P, _P, _P, _P, _P, _I32, _P], C.c_int),
+    "lsb_spmv_csr_dict": ([_P, _P, _P, _P, _P, _I32, _P], C.c_int),
     "lsb_spmv_stencil": ([_P, _P, _P, _P, _P, _I32, _P], C.c_int),
     "lsb_mdot": ([_P, _I64, _I64, _I32, _P, _P, _P, _P, _P, _I32, _P], C.c_int),
     "lsb_maxpy": ([_P, _P, _I64, _I64, _I32, _P, _I32, _P, _P, _I32, _P], C.c_int),

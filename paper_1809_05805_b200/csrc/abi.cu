@@ -53,6 +53,8 @@ int launch_stencil(const lsb_stencil*, const double*, const double*, double*, ls
                    cudaStream_t);
 int launch_csr(const lsb_csr*, const double*, const double*, double*, lsb_flags*, int,
                cudaStream_t);
+int launch_csr_dict(const lsb_csr_dict*, const double*, const double*, double*, lsb_flags*, int,
+                    cudaStream_t);
 int launch_mgs_lvl2_small(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int launch_cycle_persistent(const lsb_arnoldi&, const lsb_csr*, int, cudaStream_t, double*,
                             const double*, double*, int);
@@ -105,6 +107,12 @@ int lsb_spmv_csr(const lsb_csr* A, const double* x, const double* b, double* y, 
                  int32_t it, void* stream) {
   if (!A || !x || !y) return LSB_EINVAL;
   return launch_csr(A, x, b, y, flags, it, S_(stream));
+}
+
+int lsb_spmv_csr_dict(const lsb_csr_dict* A, const double* x, const double* b, double* y,
+                      lsb_flags* flags, int32_t it, void* stream) {
+  if (!A || !x || !y) return LSB_EINVAL;
+  return launch_csr_dict(A, x, b, y, flags, it, S_(stream));
 }
 
 int lsb_spmv_stencil(const lsb_stencil* S, const double* x, const double* b, double* y,

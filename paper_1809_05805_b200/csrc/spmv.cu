@@ -372,6 +372,63 @@ csr_kernel(const lsb_csr A, const double* __restrict__ x, const double* __restri
   if (bad && flags) flags->nonfinite = 1;
 }
 
+// Dictionary-coded CSR (value-indexed + offset-indexed, "CSR-VI/DU"): when
+// a matrix has at most 256 distinct values and at most 256 distinct column
+// offsets col - row (constant-coefficient PDE discretisations), each entry
+// is two u8 indices into per-matrix tables held in shared memory: 2 bytes
+// per nonzero streamed instead of 12.  Thread per row: lane l of a warp owns
+// row r0 + l, so entry k of 32 interior rows reads x at 32 consecutive
+// addresses (one coalesced gather).  Products and numpy's reduceat order are
+// csr_kernel's, so y is bitwise lsb_spmv_csr's.
+struct CsrDictAcc {
+  const uint8_t* vi;
+  const uint8_t* oi;
+  const double* vtab;
+  const int32_t* otab;
+  const double* x;
+  const double* d;
+  int64_t base;   // global row - x_lo
+  __device__ double operator()(int64_t j) const {
+    const int64_t c = base + otab[__ldg(oi + j)];
+    double xv = __ldg(x + c);
+    if (d) xv = __dmul_rn(xv, __ldg(d + c));
+    return __dmul_rn(vtab[__ldg(vi + j)], xv);
+  }
+};
+
+__global__ void __launch_bounds__(256)
+csr_dict_kernel(const lsb_csr_dict A, const double* __restrict__ x, const double* __restrict__ b,
+                double* __restrict__ y, lsb_flags* flags, int it) {
+  if (gated_off(flags, it)) return;
+  __shared__ double vtab[256];
+  __shared__ int32_t otab[256];
+  for (int k = threadIdx.x; k < A.n_val; k += blockDim.x) vtab[k] = A.val_tab[k];
+  for (int k = threadIdx.x; k < A.n_off; k += blockDim.x) otab[k] = A.off_tab[k];
+  __syncthreads();
+  bool bad = false;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < A.n_rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = __ldg(A.row_ptr + r), hi = __ldg(A.row_ptr + r + 1);
+    CsrDictAcc acc{A.val_idx + lo, A.off_idx + lo, vtab, otab, x, A.col_scale,
+                   A.row0 + r - A.x_lo};
+    const double s = np_row_sum(acc, hi - lo);
+    if (!isfinite(s)) bad = true;
+    y[r] = b ? __dsub_rn(b[r], s) : s;
+  }
+  if (bad && flags) flags->nonfinite = 1;
+}
+
+int launch_csr_dict(const lsb_csr_dict* A, const double* x, const double* b, double* y,
+                    lsb_flags* flags, int it, cudaStream_t st) {
+  if (A->n_rows <= 0) return LSB_OK;
+  if (A->n_val < 1 || A->n_val > 256 || A->n_off < 1 || A->n_off > 256) return LSB_EINVAL;
+  static const int occ = wave(csr_dict_kernel, 0);
+  int64_t g = (A->n_rows + 255) / 256;
+  if (g > (int64_t)sm_count() * occ) g = (int64_t)sm_count() * occ;
+  csr_dict_kernel<<<(unsigned)g, 256, 0, st>>>(*A, x, b, y, flags, it);
+  return check_launch("csr_dict");
+}
+
 // Warp-staged CSR: a warp owns 32 consecutive rows.  Their nonzeros form one
 // contiguous segment [row_ptr[r0], row_ptr[r0+32]); the warp streams it with
 // coalesced col/value loads (kCsrUnroll independent loads in flight per lane),

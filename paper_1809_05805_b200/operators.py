@@ -10,6 +10,7 @@ arrays only if a caller asks for them.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -34,6 +35,44 @@ class CsrOperator:
         self.c = _abi.Csr(A.n_rows, A.n_cols, A.nnz, self.row_ptr.data_ptr(),
                           self.col_idx.data_ptr(), self.values.data_ptr(),
                           col_scale.data_ptr() if col_scale is not None else None, 0, 0)
+        self._dictionary()
+
+    # nnz from which the dictionary form pays for its one-time build
+    DICT_MIN_NNZ = 1 << 20
+
+    def _dictionary(self):
+        """Dictionary-coded copy (lsb_csr_dict) when the values have at most
+        256 distinct bit patterns and the column offsets col - row at most 256
+        distinct values: the SpMV then streams 2 bytes per nonzero instead of
+        12, bitwise the same y.  LSB_CSR_DICT=0 never, =1 always (any size)."""
+        self.cd = None
+        mode = os.environ.get("LSB_CSR_DICT", "auto")
+        nnz = int(self.values.shape[0])
+        if mode == "0" or nnz == 0 or (mode != "1" and nnz < self.DICT_MIN_NNZ):
+            return
+        bits = self.values.view(torch.int64)          # exact: -0.0, NaN payloads kept
+        vt, vi = torch.unique(bits, return_inverse=True)
+        if vt.numel() > 256:
+            return
+        counts = self.row_ptr[1:].to(torch.int64) - self.row_ptr[:-1].to(torch.int64)
+        rows = torch.repeat_interleave(torch.arange(self.n_rows, device=bits.device), counts)
+        ot, oi = torch.unique(self.col_idx.to(torch.int64) - rows, return_inverse=True)
+        del rows
+        if ot.numel() > 256 or ot.abs().max() >= 2 ** 31:
+            return
+        self.cd_val_idx = vi.to(torch.uint8)
+        self.cd_off_idx = oi.to(torch.uint8)
+        self.cd_val_tab = vt.view(torch.float64).contiguous()
+        self.cd_off_tab = ot.to(torch.int32)
+        self.cd = self._dict_struct(self.col_scale)
+
+    def _dict_struct(self, col_scale):
+        return _abi.CsrDict(self.c.n_rows, self.c.n_cols, self.c.nnz, self.row_ptr.data_ptr(),
+                            self.cd_val_idx.data_ptr(), self.cd_off_idx.data_ptr(),
+                            self.cd_val_tab.data_ptr(), self.cd_off_tab.data_ptr(),
+                            int(self.cd_val_tab.numel()), int(self.cd_off_tab.numel()),
+                            col_scale.data_ptr() if col_scale is not None else None,
+                            self.c.row0, self.c.x_lo)
 
     @classmethod
     def from_device(cls, n_rows, n_cols, row_ptr, col_idx, values, col_scale=None):
@@ -48,6 +87,7 @@ class CsrOperator:
         op.c = _abi.Csr(op.n_rows, op.n_cols, int(values.shape[0]), row_ptr.data_ptr(),
                         col_idx.data_ptr(), values.data_ptr(),
                         col_scale.data_ptr() if col_scale is not None else None, 0, 0)
+        op._dictionary()
         return op
 
     def with_scale(self, col_scale):
@@ -57,6 +97,8 @@ class CsrOperator:
         op.c = _abi.Csr(self.c.n_rows, self.c.n_cols, self.c.nnz, self.c.row_ptr, self.c.col_idx,
                         self.c.values, col_scale.data_ptr() if col_scale is not None else None,
                         0, 0)
+        if self.cd is not None:
+            op.cd = self._dict_struct(col_scale)
         return op
 
     @property
@@ -64,6 +106,10 @@ class CsrOperator:
         return 4 * (self.n_rows + 1) + 12 * int(self.values.shape[0])
 
     def apply_ptr(self, xp, yp, bp=None, flagsp=None, it=-1, stream=None):
+        if self.cd is not None:
+            _abi.call("lsb_spmv_csr_dict", C.byref(self.cd), xp, bp, yp, flagsp, it,
+                      stream or D.stream())
+            return
         _abi.call("lsb_spmv_csr", C.byref(self.c), xp, bp, yp, flagsp, it, stream or D.stream())
 
     def apply(self, x, y, b=None, flags=None, it=-1):

@@ -120,6 +120,83 @@ def test_spmv_csr_kernels_mixed_segments(P, knob):
         lib.lsb_set_tuning(_abi.TUNE_CSR_THREAD_ROW, 0)
 
 
+def _dict_matrix(kind):
+    rng = np.random.default_rng(17)
+    if kind == "convdiff27":
+        O = orc.convdiff27(9)
+        return O.n_rows, O.row_ptr, O.col_idx, O.values
+    n = 700
+    offs = np.unique(rng.integers(-300, 300, 200))            # <= 200 distinct offsets
+    table = np.concatenate([rng.standard_normal(90) * np.exp(rng.standard_normal(90) * 6),
+                            [0.0, -0.0, 1e-300, -1e300, 5e-324]])
+    rows = []
+    for r in range(n):
+        k = 0 if r % 97 == 5 else (len(offs) if r == 350 else int(rng.integers(1, 40)))
+        c = np.unique(r + rng.choice(offs, size=min(k, len(offs)), replace=False))
+        rows.append(c[(c >= 0) & (c < n)])
+    ptr = np.concatenate([[0], np.cumsum([len(c) for c in rows])]).astype(np.int64)
+    ci = np.concatenate(rows).astype(np.int64)
+    vals = table[rng.integers(0, len(table), ci.size)]
+    return n, ptr, ci, vals
+
+
+@pytest.mark.parametrize("kind", ["convdiff27", "banded_ragged"])
+def test_spmv_csr_dict_bitwise(P, monkeypatch, kind):
+    """Dictionary-coded CSR (u8 value + u8 offset indices): y = Ax, b - Ax and
+    the column-scaled form bitwise equal to the plain CSR kernel and the
+    oracle; signed zeros and extreme magnitudes in the value table, empty rows,
+    a row of 190+ entries."""
+    from paper_1809_05805_b200.operators import CsrOperator
+    monkeypatch.setenv("LSB_CSR_DICT", "1")
+    n, ptr, ci, vals = _dict_matrix(kind)
+    O = orc.Csr(n, n, ptr, ci, vals)
+    op = CsrOperator(P.CsrMatrix(n, n, O.row_ptr, O.col_idx, O.values))
+    assert op.cd is not None
+    plain = op.with_scale(None)
+    plain.cd = None
+    rng = np.random.default_rng(5)
+    x, b, d = rng.standard_normal(n), rng.standard_normal(n), rng.uniform(0.5, 2.0, n)
+    xd, bd, dd = (torch.as_tensor(v).cuda() for v in (x, b, d))
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    y2 = torch.empty_like(y)
+    for bb, scale in ((None, None), (bd, None), (None, dd)):
+        o1 = op if scale is None else op.with_scale(scale)
+        o2 = plain if scale is None else plain.with_scale(scale)
+        o2.cd = None
+        o1.apply(xd, y, b=bb)
+        o2.apply(xd, y2, b=bb)
+        assert torch.equal(y.view(torch.int64), y2.view(torch.int64))
+    op.apply(xd, y)
+    assert np.array_equal(_np(y).view(np.int64), orc.spmv(O, x).view(np.int64))
+
+
+def test_spmv_csr_dict_declines_wide_tables(P, monkeypatch):
+    from paper_1809_05805_b200.operators import CsrOperator
+    monkeypatch.setenv("LSB_CSR_DICT", "1")
+    n = 400
+    A = P.CsrMatrix.from_coo(n, n, np.arange(n), np.arange(n), np.arange(1.0, n + 1))
+    assert CsrOperator(A).cd is None                 # 400 distinct values
+    monkeypatch.setenv("LSB_CSR_DICT", "0")
+    O = orc.convdiff27(6)
+    assert CsrOperator(P.CsrMatrix(O.n_rows, O.n_cols, O.row_ptr, O.col_idx, O.values)).cd is None
+
+
+def test_solve_csr_dict_identical(P, monkeypatch):
+    """A restarted solve through the dictionary-coded SpMV is bitwise the
+    plain-CSR solve (same y every iteration)."""
+    monkeypatch.setenv("LSB_PERSISTENT", "0")
+    O = orc.convdiff27(20)
+    out = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("LSB_CSR_DICT", mode)
+        A = P.CsrMatrix(O.n_rows, O.n_cols, O.row_ptr, O.col_idx, O.values)
+        cfg = P.GmresConfig(restart_m=30, max_restarts=20, rel_tol=1e-9, method="one_sync_mgs")
+        x, h = P.solve(A, P.gen_rhs("random", A, 3), config=cfg, diagnostics_every=0)
+        out.append((x, h.implicit_curve(), h.cycle_starts))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
+
+
 @pytest.mark.parametrize("dims", [(4, 3, 7), (6, 5, 4), (8, 8, 8), (12, 7, 5), (9, 4, 4), (10, 3, 3)])
 def test_spmv_box27_bitwise_shapes(P, dims):
     """27-point operator on boxes that exercise every edge class of the

@@ -68,9 +68,17 @@ def main():
     ms = time_spmv(st, x, y0)
     sp["stencil27"] = {"ms": ms, "GBps": 16 * n / ms / 1e6}
     csr_bytes = 12 * S.nnz + 4 * (n + 1) + 16 * n
+    dict_bytes = 2 * S.nnz + 4 * (n + 1) + 16 * n
+    plain = csr.with_scale(None)
+    plain.cd = None                      # the 12-byte-per-nonzero kernels
+    if csr.cd is not None:
+        ms = time_spmv(csr, x, y1)
+        sp["csr_dict"] = {"ms": ms, "GBps": dict_bytes / ms / 1e6,
+                          "bitwise_eq_stencil": bool(torch.equal(y0, y1)),
+                          "tables": [int(csr.cd.n_val), int(csr.cd.n_off)]}
     for key, knob in (("csr_warp_u16", 0), ("csr_warp_u8_occ3", 2), ("csr_thread_row", 1)):
         lib.lsb_set_tuning(_abi.TUNE_CSR_THREAD_ROW, knob)
-        ms = time_spmv(csr, x, y1)
+        ms = time_spmv(plain, x, y1)
         eq = bool(torch.equal(y0, y1))
         sp[key] = {"ms": ms, "GBps": csr_bytes / ms / 1e6, "bitwise_eq_stencil": eq}
     lib.lsb_set_tuning(_abi.TUNE_CSR_THREAD_ROW, 0)
@@ -88,7 +96,10 @@ def main():
         bd = torch.as_tensor(b).cuda()
         ortho = sum(8 * n * (2 * (i + 1) + 4) for i in range(1, a.m + 1))
         cyc = {}
-        for form, op, sbytes in (("stencil", st, 16 * n), ("csr", csr, csr_bytes)):
+        forms = [("stencil", st, 16 * n), ("csr", plain, csr_bytes)]
+        if csr.cd is not None:
+            forms.append(("csr_dict", csr, dict_bytes))
+        for form, op, sbytes in forms:
             eng = Engine(S, a.m, "one_sync_mgs", 1e-14, op=op, use_graph=True)
             eng.load(bd)
             eng.prologue()
