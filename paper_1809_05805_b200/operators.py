@@ -50,6 +50,13 @@ class CsrOperator:
         nnz = int(self.values.shape[0])
         if mode == "0" or nnz == 0 or (mode != "1" and nnz < self.DICT_MIN_NNZ):
             return
+        try:
+            self._build_dictionary()
+        except torch.cuda.OutOfMemoryError:   # the build's sort temporaries: keep plain CSR
+            self.cd = None
+            torch.cuda.empty_cache()
+
+    def _build_dictionary(self):
         bits = self.values.view(torch.int64)          # exact: -0.0, NaN payloads kept
         vt, vi = torch.unique(bits, return_inverse=True)
         if vt.numel() > 256:
