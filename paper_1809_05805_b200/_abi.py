@@ -24,7 +24,7 @@ MAX_OFF = 27
 # lsb_set_tuning keys (include/lsb200.h LSB_TUNE_*)
 TUNE_FUSED_OCC3, TUNE_FORCE_PARTS, TUNE_ROW_CTAS_PER_SM = 1, 2, 3
 TUNE_K3_ROWS, TUNE_K3_STAGES, TUNE_CSR_THREAD_ROW = 4, 5, 6
-TUNE_PERSIST_TRACE, TUNE_PERSIST_CTAS, TUNE_FUSED_PIPE = 7, 8, 9
+TUNE_PERSIST_TRACE, TUNE_PERSIST_CTAS, TUNE_FUSED_PIPE, TUNE_CSR_DICT = 7, 8, 9, 10
 
 
 class LsbUnavailable(RuntimeError):

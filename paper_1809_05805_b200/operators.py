@@ -67,8 +67,11 @@ class CsrOperator:
         del rows
         if ot.numel() > 256 or ot.abs().max() >= 2 ** 31:
             return
-        self.cd_val_idx = vi.to(torch.uint8)
-        self.cd_off_idx = oi.to(torch.uint8)
+        # padded to whole 32-bit words (+1): the warp-staged kernel copies
+        # the index bytes of a 32-row segment with word loads
+        pad = (-vi.numel()) % 4 + 4
+        self.cd_val_idx = torch.nn.functional.pad(vi.to(torch.uint8), (0, pad))
+        self.cd_off_idx = torch.nn.functional.pad(oi.to(torch.uint8), (0, pad))
         self.cd_val_tab = vt.view(torch.float64).contiguous()
         self.cd_off_tab = ot.to(torch.int32)
         self.cd = self._dict_struct(self.col_scale)

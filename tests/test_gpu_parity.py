@@ -131,7 +131,7 @@ def _dict_matrix(kind):
                             [0.0, -0.0, 1e-300, -1e300, 5e-324]])
     rows = []
     for r in range(n):
-        k = 0 if r % 97 == 5 else (len(offs) if r == 350 else int(rng.integers(1, 40)))
+        k = 0 if r % 97 == 5 else (len(offs) if 350 <= r < 362 else int(rng.integers(1, 40)))
         c = np.unique(r + rng.choice(offs, size=min(k, len(offs)), replace=False))
         rows.append(c[(c >= 0) & (c < n)])
     ptr = np.concatenate([[0], np.cumsum([len(c) for c in rows])]).astype(np.int64)
@@ -140,12 +140,13 @@ def _dict_matrix(kind):
     return n, ptr, ci, vals
 
 
+@pytest.mark.parametrize("knob", [0, 1])     # thread per row / warp-staged index bytes
 @pytest.mark.parametrize("kind", ["convdiff27", "banded_ragged"])
-def test_spmv_csr_dict_bitwise(P, monkeypatch, kind):
+def test_spmv_csr_dict_bitwise(P, monkeypatch, kind, knob):
     """Dictionary-coded CSR (u8 value + u8 offset indices): y = Ax, b - Ax and
     the column-scaled form bitwise equal to the plain CSR kernel and the
     oracle; signed zeros and extreme magnitudes in the value table, empty rows,
-    a row of 190+ entries."""
+    a 32-row group whose index bytes overflow the warp slab (rows of 190+)."""
     from paper_1809_05805_b200.operators import CsrOperator
     monkeypatch.setenv("LSB_CSR_DICT", "1")
     n, ptr, ci, vals = _dict_matrix(kind)
@@ -159,6 +160,16 @@ def test_spmv_csr_dict_bitwise(P, monkeypatch, kind):
     xd, bd, dd = (torch.as_tensor(v).cuda() for v in (x, b, d))
     y = torch.empty(n, dtype=torch.float64, device="cuda")
     y2 = torch.empty_like(y)
+    from paper_1809_05805_b200 import _abi
+    lib = _abi.load()
+    lib.lsb_set_tuning(_abi.TUNE_CSR_DICT, knob)
+    try:
+        _dict_cases(op, plain, O, x, xd, bd, dd, y, y2)
+    finally:
+        lib.lsb_set_tuning(_abi.TUNE_CSR_DICT, 0)
+
+
+def _dict_cases(op, plain, O, x, xd, bd, dd, y, y2):
     for bb, scale in ((None, None), (bd, None), (None, dd)):
         o1 = op if scale is None else op.with_scale(scale)
         o2 = plain if scale is None else plain.with_scale(scale)

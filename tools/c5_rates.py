@@ -72,10 +72,13 @@ def main():
     plain = csr.with_scale(None)
     plain.cd = None                      # the 12-byte-per-nonzero kernels
     if csr.cd is not None:
-        ms = time_spmv(csr, x, y1)
-        sp["csr_dict"] = {"ms": ms, "GBps": dict_bytes / ms / 1e6,
-                          "bitwise_eq_stencil": bool(torch.equal(y0, y1)),
-                          "tables": [int(csr.cd.n_val), int(csr.cd.n_off)]}
+        for key, knob in (("csr_dict", 0), ("csr_dict_warp_staged", 1)):
+            lib.lsb_set_tuning(_abi.TUNE_CSR_DICT, knob)
+            ms = time_spmv(csr, x, y1)
+            sp[key] = {"ms": ms, "GBps": dict_bytes / ms / 1e6,
+                       "bitwise_eq_stencil": bool(torch.equal(y0, y1)),
+                       "tables": [int(csr.cd.n_val), int(csr.cd.n_off)]}
+        lib.lsb_set_tuning(_abi.TUNE_CSR_DICT, 0)
     for key, knob in (("csr_warp_u16", 0), ("csr_warp_u8_occ3", 2), ("csr_thread_row", 1)):
         lib.lsb_set_tuning(_abi.TUNE_CSR_THREAD_ROW, knob)
         ms = time_spmv(plain, x, y1)
