@@ -13,6 +13,10 @@ __device__ __forceinline__ double gsum(const lsb_arnoldi& S, int e) {
   return v;
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 struct SmallShared {
   double a[kSmall];     // G[:,0] / scaled
   double y[kSmall];     // G[:,1] / y
@@ -104,6 +108,23 @@ __device__ inline bool lagged_front(const lsb_arnoldi& S, SmallShared& sh, int i
 __device__ inline void mgs_small_body(const lsb_arnoldi& S, SmallShared& sh, double* sT, int it,
                                       int p, int ks, int gc, bool use_smem) {
   const int t = threadIdx.x, cap = S.cap;
+  // The kernel is a chain of dependent L2 round trips, not work (ncu: ~2K
+  // warp instructions in ~20K cycles): issue every independent load up
+  // front -- the T block (not touched by lagged_front) and L1 prefetches of
+  // the scalars, rotations and g that the breakdown test and the Givens
+  // fold read later.
+  const bool st = use_smem;
+  if (st) {
+    for (int e = t; e < (p - 1) * (p - 1); e += blockDim.x) {
+      const int j = e / (p - 1), l = e - j * (p - 1);
+      sT[j * p + l] = S.T[(int64_t)j * cap + l];
+    }
+  }
+  if (t == 0) {
+    prefetch_l1(S.scal);
+    if (gc > 0) prefetch_l1(S.g + gc - 1);
+  }
+  if (gc > 1 && 16 * t < 2 * (gc - 1)) prefetch_l1(S.rot + 16 * t);
   const bool broke = lagged_front(S, sh, it, p, gc);
   if (broke) {
     if (gc > 0) settle_block(S, sh, it, gc, true);
@@ -112,13 +133,6 @@ __device__ inline void mgs_small_body(const lsb_arnoldi& S, SmallShared& sh, dou
   const double beta = sh.beta;
   // T block in shared memory when it fits (p x p, row stride p): the two
   // triangular mat-vecs then run at smem latency (launch sets the size)
-  const bool st = use_smem;
-  if (st) {
-    for (int e = t; e < (p - 1) * (p - 1); e += blockDim.x) {
-      const int j = e / (p - 1), l = e - j * (p - 1);
-      sT[j * p + l] = S.T[(int64_t)j * cap + l];
-    }
-  }
   // T[:p-1, p-1] = -(T[:p-1, :p-1] @ (G[:p-1, 0] / beta));  T[p-1, p-1] = 1
   for (int e = t; e < p - 1; e += blockDim.x) sh.a[e] = __ddiv_rn(sh.a[e], beta);
   if (t == 0) sh.y[p - 1] = __ddiv_rn(sh.y[p - 1], beta);
