@@ -999,6 +999,26 @@ def _compare_runs(r0, r1):
     assert np.linalg.norm(x1 - x0) <= 1e-8 * max(np.linalg.norm(x0), 1e-300)
 
 
+@pytest.mark.parametrize("mode", [("0", "0"), ("1", "0"), ("1", "1")])
+def test_persistent_nonfinite_raises_and_recovers(P, monkeypatch, mode):
+    """An overflow inside the cycle (values ~1e300 square past DBL_MAX in the
+    Krylov products) surfaces as NonFiniteError in every execution mode --
+    the whole-solve launch reports it instead of leaving the host waiting --
+    and the next solve on the device is unaffected."""
+    monkeypatch.setenv("LSB_PERSISTENT", mode[0])
+    monkeypatch.setenv("LSB_PERSISTENT_SOLVE", mode[1])
+    O = orc.laplace2d(16)
+    vals = O.values.copy() * 1e300
+    A = P.CsrMatrix(O.n_rows, O.n_cols, O.row_ptr, O.col_idx, vals)
+    cfg = P.GmresConfig(restart_m=10, max_restarts=5, rel_tol=1e-8, method="one_sync_mgs")
+    with pytest.raises(P.NonFiniteError):
+        P.solve(A, P.gen_rhs("random", A, 1), config=cfg, diagnostics_every=0)
+    B = P.gen_laplace2d(16)
+    cfg = P.GmresConfig(restart_m=10, max_restarts=200, rel_tol=1e-8, method="one_sync_mgs")
+    x, h = P.solve(B, P.gen_rhs("random", B, 1), config=cfg, diagnostics_every=0)
+    assert h.outcome == "converged" and np.all(np.isfinite(x))
+
+
 def test_persistent_cycle_is_used_at_launch_bound_sizes(P):
     from paper_1809_05805_b200.engine import Engine
     A = P.gen_laplace2d(64)
