@@ -19,6 +19,7 @@ reads one small report (flags, residuals, scalars) per cycle.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 
 import numpy as np
@@ -136,10 +137,10 @@ class Engine:
         offs, tot = [], 0
         for _, shp in sizes:
             offs.append(tot)
-            tot += D.round_up(int(np.prod(shp)), 2)
+            tot += D.round_up(math.prod(shp), 2)
         self._arena = torch.zeros(tot, **f64)
         for (name, shp), o in zip(sizes, offs):
-            setattr(self, name, self._arena[o:o + int(np.prod(shp))].view(shp))
+            setattr(self, name, self._arena[o:o + math.prod(shp)].view(shp))
         self.flags = self.flags.view(torch.int32)[:_abi.FLAGS_INTS]
         if parts == 1:
             self.G = self.Gloc
