@@ -149,7 +149,12 @@ __device__ __forceinline__ void load27_pair(const double* __restrict__ x, int64_
   }
 }
 
-__global__ void __launch_bounds__(256)
+// 128-thread CTAs: at ~94 registers a 256-thread CTA fits twice per SM
+// (16 warps); 128-thread CTAs fit five times (20 warps) -- more warps to
+// hide the FP64 and load latency of the unfused products.
+constexpr int kS27Threads = 128;
+
+__global__ void __launch_bounds__(kS27Threads)
 stencil27_pair_kernel(const StencilK K, FastDiv fint, const double* __restrict__ x,
                       const double* __restrict__ b, double* __restrict__ y, lsb_flags* flags,
                       int it) {
@@ -314,12 +319,16 @@ int launch_stencil(const lsb_stencil* S, const double* x, const double* b, doubl
   if (g < 1) g = 1;
   if (canonical27(S) && S->nx % 2 == 0 && S->nx >= 4 && !S->col_scale &&
       (uintptr_t)x % 16 == 0 && (uintptr_t)y % 16 == 0 && (!b || (uintptr_t)b % 16 == 0)) {
-    static const int occ27p = wave(stencil27_pair_kernel, 0);
-    int64_t gp = (n64 / 2 + 255) / 256;
+    static const int occ27p = [] {
+      int o = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, stencil27_pair_kernel, kS27Threads, 0);
+      return o > 0 ? o : 1;
+    }();
+    int64_t gp = (n64 / 2 + kS27Threads - 1) / kS27Threads;
     if (gp > (int64_t)sm_count() * occ27p) gp = (int64_t)sm_count() * occ27p;
     if (gp < 1) gp = 1;
     const FastDiv fint = FastDiv::make(S->nx >= 6 ? (uint32_t)(S->nx / 2 - 2) : 1u);
-    stencil27_pair_kernel<<<(unsigned)gp, 256, 0, st>>>(K, fint, x, b, y, flags, it);
+    stencil27_pair_kernel<<<(unsigned)gp, kS27Threads, 0, st>>>(K, fint, x, b, y, flags, it);
     return check_launch("stencil27_pair");
   }
   if (canonical27(S)) {
