@@ -214,6 +214,19 @@ int lsb_norm_finish(const double* parts, int32_t nparts, int32_t part_stride, co
                     int64_t n, double* out, const lsb_workspace* ws, const lsb_flags* flags,
                     int32_t it, void* stream);
 
+/* Row-partitioned norm across ranks, overflow-safe (the rescaled pass of
+ * kernels.py:113-119 with an exact power-of-two scale): after the (amax,
+ * ssq) parts of every rank are gathered, lsb_norm_scaled_partial writes
+ * this rank's sum of (x * 2^-e)^2 into out2[0] (e from the GLOBAL amax; 0
+ * when max|x| lies in [2^-450, 2^450]); after those are gathered too,
+ * lsb_norm_finish_scaled writes ||x|| -- sqrt(sum ssq) in range, else
+ * sqrt(sum scaled) * 2^e.  Same value on every rank. */
+int lsb_norm_scaled_partial(const double* parts, int32_t nparts, int32_t part_stride,
+                            const double* x, int64_t n, double* out2, const lsb_workspace* ws,
+                            void* stream);
+int lsb_norm_finish_scaled(const double* parts, const double* parts2, int32_t nparts,
+                           int32_t part_stride, int32_t part2_stride, double* out, void* stream);
+
 /* out = x / (*s) elementwise (device scalar s; e.g. V.push(r / beta)). */
 int lsb_scale_div(const double* x, int64_t n, const double* s, double* out,
                   const lsb_flags* flags, int32_t it, void* stream);

@@ -95,6 +95,8 @@ _SIGS = {
     "lsb_max_columns": ([], _I32),
     "lsb_spmv_csr": ([_P, _P, _P, _P, _P, _I32, _P], C.c_int),
     "lsb_spmv_csr_dict": ([_P, _P, _P, _P, _P, _I32, _P], C.c_int),
+    "lsb_norm_scaled_partial": ([_P, _I32, _I32, _P, _I64, _P, _P, _P], C.c_int),
+    "lsb_norm_finish_scaled": ([_P, _P, _I32, _I32, _I32, _P, _P], C.c_int),
     "lsb_spmv_stencil": ([_P, _P, _P, _P, _P, _I32, _P], C.c_int),
     "lsb_mdot": ([_P, _I64, _I64, _I32, _P, _P, _P, _P, _P, _I32, _P], C.c_int),
     "lsb_maxpy": ([_P, _P, _I64, _I64, _I32, _P, _I32, _P, _P, _I32, _P], C.c_int),

@@ -46,6 +46,9 @@ int launch_norm_partial(const double*, int64_t, double*, const lsb_workspace*, c
                         int, cudaStream_t);
 int launch_norm_finish(const double*, int, int, const double*, int64_t, double*,
                        const lsb_workspace*, const lsb_flags*, int, cudaStream_t);
+int launch_norm_scaled_partial(const double*, int, int, const double*, int64_t, double*,
+                               const lsb_workspace*, cudaStream_t);
+int launch_norm_finish_scaled(const double*, const double*, int, int, int, double*, cudaStream_t);
 int launch_scale_div(const double*, int64_t, const double*, double*, const lsb_flags*, int, int,
                      cudaStream_t);
 int launch_extract(const lsb_arnoldi&, double*, const double*, cudaStream_t);
@@ -150,6 +153,21 @@ int lsb_norm_finish(const double* parts, int32_t nparts, int32_t part_stride, co
                     int32_t it, void* stream) {
   if (nparts < 1 || !ws || (nparts > 1 && part_stride < 2)) return LSB_EINVAL;
   return launch_norm_finish(parts, nparts, part_stride, x, n, out, ws, flags, it, S_(stream));
+}
+
+int lsb_norm_scaled_partial(const double* parts, int32_t nparts, int32_t part_stride,
+                            const double* x, int64_t n, double* out2, const lsb_workspace* ws,
+                            void* stream) {
+  if (nparts < 1 || !ws || !parts || !out2 || (nparts > 1 && part_stride < 2)) return LSB_EINVAL;
+  return launch_norm_scaled_partial(parts, nparts, part_stride, x, n, out2, ws, S_(stream));
+}
+
+int lsb_norm_finish_scaled(const double* parts, const double* parts2, int32_t nparts,
+                           int32_t part_stride, int32_t part2_stride, double* out, void* stream) {
+  if (nparts < 1 || !parts || !parts2 || !out || (nparts > 1 && (part_stride < 2 || part2_stride < 1)))
+    return LSB_EINVAL;
+  return launch_norm_finish_scaled(parts, parts2, nparts, part_stride, part2_stride, out,
+                                   S_(stream));
 }
 
 int lsb_scale_div(const double* x, int64_t n, const double* s, double* out,

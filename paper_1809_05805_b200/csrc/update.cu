@@ -366,6 +366,72 @@ int launch_norm_finish(const double* parts, int nparts, int stride, const double
   return check_launch("norm_finish");
 }
 
+// Row-partitioned restart norm, second round (ranks > 1): from the gathered
+// (amax, ssq) parts, when max|x| leaves [2^-450, 2^450] each rank forms its
+// sum of (x * 2^-e)^2 with the exponent e of the GLOBAL amax (the same exact
+// power-of-two scale on every rank), else 0.  The caller all-gathers that
+// and finishes with lsb_norm_finish_scaled.
+__device__ __forceinline__ bool norm_needs_rescale(const double* parts, int nparts, int stride,
+                                                   double& amax, double& ssq) {
+  amax = parts[0];
+  ssq = parts[1];
+  for (int q = 1; q < nparts; ++q) {
+    amax = fmax(amax, parts[(int64_t)q * stride]);
+    ssq += parts[(int64_t)q * stride + 1];
+  }
+  return !(amax == 0.0 || isnan(amax) || (amax >= 0x1p-450 && amax <= 0x1p450));
+}
+
+__global__ void __launch_bounds__(kThreads)
+norm_scaled_partial_kernel(const double* parts, int nparts, int stride,
+                           const double* __restrict__ x, int64_t n, double* out2,
+                           double* partial, unsigned* counter) {
+  double amax, ssq;
+  const bool resc = norm_needs_rescale(parts, nparts, stride, amax, ssq);
+  double acc = 0.0;
+  if (resc) {
+    int e;
+    frexp(amax, &e);
+    const double s = ldexp(1.0, -e);
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+      const double v = x[r] * s;
+      acc = fma(v, v, acc);
+    }
+  }
+  const double v[2] = {acc, 0.0};
+  const int op[2] = {0, 0};
+  grid_reduce<2>(v, op, partial, counter, out2);
+}
+
+__global__ void norm_finish_scaled_kernel(const double* parts, const double* parts2, int nparts,
+                                          int stride, int stride2, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double amax, ssq;
+  if (!norm_needs_rescale(parts, nparts, stride, amax, ssq)) {
+    *out = amax == 0.0 ? 0.0 : (isnan(amax) ? amax : sqrt(ssq));
+    return;
+  }
+  int e;
+  frexp(amax, &e);
+  double q = parts2[0];
+  for (int k = 1; k < nparts; ++k) q += parts2[(int64_t)k * stride2];
+  *out = sqrt(q) / ldexp(1.0, -e);
+}
+
+int launch_norm_scaled_partial(const double* parts, int nparts, int stride, const double* x,
+                               int64_t n, double* out2, const lsb_workspace* ws, cudaStream_t st) {
+  norm_scaled_partial_kernel<<<row_grid(2 * n, 4), kThreads, 0, st>>>(
+      parts, nparts, stride, x, n, out2, ws->partial, ws->counter);
+  return check_launch("norm_scaled_partial");
+}
+
+int launch_norm_finish_scaled(const double* parts, const double* parts2, int nparts, int stride,
+                              int stride2, double* out, cudaStream_t st) {
+  norm_finish_scaled_kernel<<<1, 32, 0, st>>>(parts, parts2, nparts, stride, stride2, out);
+  return check_launch("norm_finish_scaled");
+}
+
 // ------------------------------------------------------------------ scalings
 __global__ void __launch_bounds__(kThreads)
 scale_div_kernel(const double* __restrict__ x, int64_t n, const double* s, double* out,

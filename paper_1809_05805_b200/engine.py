@@ -129,7 +129,7 @@ class Engine:
                  ("Gloc", (2 * cap,)), ("scal", (_abi.S_COUNT,)), ("res", (m + 1,)),
                  ("flags", ((_abi.FLAGS_INTS + 1) // 2,))]
         if parts > 1:
-            sizes.append(("G", (parts * 2 * cap,)))
+            sizes += [("G", (parts * 2 * cap,)), ("Gloc2", (2,)), ("G2", (parts * 2,))]
         if diagnostics:
             sizes.append(("gram", (cap, cap)))
         if true_residual:
@@ -284,9 +284,19 @@ class Engine:
         self._call("lsb_norm_partial", D.ptr(self.rbuf), self.n, D.ptr(self.Gloc), self.ws.ref(),
                    None, -1, st)
         self._gather(2)
-        self._call("lsb_norm_finish", D.ptr(self.G), self.S.g_parts, self.S.g_stride, D.ptr(self.rbuf), self.n,
-                   C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_RNORM), self.ws.ref(), None, -1,
-                   st)
+        rn = C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_RNORM)
+        if self.comm is None:
+            self._call("lsb_norm_finish", D.ptr(self.G), 1, self.S.g_stride, D.ptr(self.rbuf),
+                       self.n, rn, self.ws.ref(), None, -1, st)
+            return
+        # ranks > 1: the overflow-safe rescaled pass needs the global max|r|,
+        # so it is a second (2-double) all-gather; the restart norm runs
+        # once per cycle
+        self._call("lsb_norm_scaled_partial", D.ptr(self.G), self.S.g_parts, self.S.g_stride,
+                   D.ptr(self.rbuf), self.n, D.ptr(self.Gloc2), self.ws.ref(), st)
+        self.comm.allgather(self.Gloc2, self.G2)
+        self._call("lsb_norm_finish_scaled", D.ptr(self.G), D.ptr(self.G2), self.S.g_parts,
+                   self.S.g_stride, 2, rn, st)
 
     def enqueue_prologue(self):
         self._residual_and_norm()

@@ -56,3 +56,32 @@ def test_slab_partition_reproduces_reference(P, ranks, meth):
     x = np.concatenate([o[0] for o in out])
     xr = G[meth + "__x"]
     assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+
+
+def _rank_scaled(comm, dims, scale):
+    import paper_1809_05805_b200 as P
+    from paper_1809_05805_b200.parallel import local_rhs, slab_problem
+    op, ng = slab_problem(dims, comm)
+    b = local_rhs(dims, comm, 42) * scale
+    cfg = P.GmresConfig(restart_m=50, max_restarts=50, rel_tol=1e-6, method="one_sync_mgs")
+    x, h = P.gmres.solve_distributed(op, b, comm, ng, config=cfg)
+    return x, h.implicit_curve(), h.outcome
+
+
+@pytest.mark.parametrize("scale", [2.0 ** 600, 2.0 ** -600])
+def test_slab_partition_restart_norm_out_of_range(P, scale):
+    """|b| ~ 2^±600: the restart norm's sum of squares over- or underflows
+    unless rescaled; across ranks the exact power-of-two rescale needs the
+    global max|r| (second all-gather).  Scaling b by a power of two scales
+    every quantity exactly, so the history equals the unscaled golden one."""
+    from paper_1809_05805_b200.parallel import run_threads
+    G = np.load(os.path.join(GOLD, "laplace3d32.npz"))
+    out = run_threads(2, _rank_scaled, (32, 32, 32), scale)
+    c0 = out[0][1]
+    assert np.array_equal(out[1][1], c0)
+    cr = G["one_sync_mgs__curve"]
+    assert len(c0) == len(cr) and np.max(np.abs(c0 - cr) / cr) <= 1e-10
+    assert out[0][2] == str(G["one_sync_mgs__outcome"])
+    x = np.concatenate([o[0] for o in out]) / scale
+    xr = G["one_sync_mgs__x"]
+    assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
