@@ -162,6 +162,7 @@ typedef struct lsb_arnoldi {
 #define LSB_TUNE_PERSIST_CTAS 8   /* lsb_cycle_persistent cluster size 1..16, 0 auto */
 #define LSB_TUNE_FUSED_PIPE 9     /* fused K1+SpMV pipelined stencil: 0 auto (2-4 items/warp), 1 up to 8, 2 off */
 #define LSB_TUNE_CSR_DICT 10      /* dictionary-coded CSR: 0 thread per row, 1 warp-staged index bytes */
+#define LSB_TUNE_PDL 11           /* programmatic dependent launch of the K1/K5/K2 chain: 0 auto (n < 2^23), 1 on, 2 off */
 #define LSB_TUNE_COUNT 16
 /* Set / read a kernel-variant knob (performance only; results unchanged up
  * to the reduction tree of the affected kernel). Returns the old value. */

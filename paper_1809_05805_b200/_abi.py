@@ -24,7 +24,7 @@ MAX_OFF = 27
 # lsb_set_tuning keys (include/lsb200.h LSB_TUNE_*)
 TUNE_FUSED_OCC3, TUNE_FORCE_PARTS, TUNE_ROW_CTAS_PER_SM = 1, 2, 3
 TUNE_K3_ROWS, TUNE_K3_STAGES, TUNE_CSR_THREAD_ROW = 4, 5, 6
-TUNE_PERSIST_TRACE, TUNE_PERSIST_CTAS, TUNE_FUSED_PIPE, TUNE_CSR_DICT = 7, 8, 9, 10
+TUNE_PERSIST_TRACE, TUNE_PERSIST_CTAS, TUNE_FUSED_PIPE, TUNE_CSR_DICT, TUNE_PDL = 7, 8, 9, 10, 11
 
 
 class LsbUnavailable(RuntimeError):
@@ -157,6 +157,10 @@ def load(path=None):
         fn = getattr(lib, name)
         fn.argtypes = argt
         fn.restype = rest
+    # LSB_TUNE="key=value,..." (experiments): tuning knobs set at load
+    for item in filter(None, os.environ.get("LSB_TUNE", "").split(",")):
+        key, _, val = item.partition("=")
+        lib.lsb_set_tuning(int(key), int(val))
     if path is None:
         _lib = lib
     return lib

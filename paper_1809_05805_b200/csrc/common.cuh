@@ -311,5 +311,45 @@ __device__ inline double givens_fold(double* h, double* rot, double* g, int i) {
 // ---------------------------------------------------------------- launch helpers
 int sm_count();
 int check_launch(const char* what);
+int tuning(int key);
+
+// Programmatic dependent launch (LSB_TUNE_PDL = 1): the per-iteration chain
+// K1 -> K5 -> K2 -> K1 ... launches each kernel while its predecessor is
+// still running; every such kernel starts with pdl_enter() -- wait for the
+// predecessor's completion (and memory) before touching global memory, then
+// let the successor launch.  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Measured (tools/pdl_ab.py, C3 one-sync, L2 flushed): +4..6% at n = 2^20,
+// +1..3% at 2^21..2^22, -1.3% at 2^24 and on the C2 cycle (fused K1 and K2
+// fill the machine; early-resident waiting CTAs only get in the way) -- so
+// auto = on below 2^23 rows.
+inline bool use_pdl(int64_t n) {
+  const int k = tuning(LSB_TUNE_PDL);
+  return k == 1 || (k == 0 && n < ((int64_t)1 << 23));
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_chain(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                         cudaStream_t st, Args... args) {
+  if (!pdl) {
+    k<<<grid, block, smem, st>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 
 }  // namespace lsb

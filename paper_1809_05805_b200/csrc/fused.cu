@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
 mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
                   double* __restrict__ wout, const Stencil7 K, double* __restrict__ out,
                   double* __restrict__ partial, unsigned* counter, lsb_flags* flags, int it) {
+  pdl_enter();
   if (gated_off(flags, it)) return;
   constexpr int kRows = kTile / R;
   constexpr int kLd = kRows / 64;
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
 mdot_spmv7_pipe_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
                        double* __restrict__ wout, const Stencil7 K, double* __restrict__ out,
                        double* __restrict__ partial, unsigned* counter, lsb_flags* flags, int it) {
+  pdl_enter();
   if (gated_off(flags, it)) return;
   constexpr int kRows = kTile / R;
   constexpr int kLd = kRows / 64;
@@ -421,8 +423,8 @@ static int launch_k(Kern kern, bool pipe, int* occ_nx, int* occ, const lsb_arnol
   if (S.ws.grid > 0 && S.ws.grid < grid) grid = S.ws.grid;
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, kThreads, sm, st>>>(S.V, S.ld, S.n, p, S.V + (int64_t)p * S.ld, K,
-                                            S.Gloc, S.ws.partial, S.ws.counter, S.flags, it);
+  launch_chain(use_pdl(S.n), kern, dim3((unsigned)grid), dim3(kThreads), sm, st, S.V, S.ld, S.n, p,
+               S.V + (int64_t)p * S.ld, K, S.Gloc, S.ws.partial, S.ws.counter, S.flags, it);
   return check_launch("mdot_spmv7");
 }
 

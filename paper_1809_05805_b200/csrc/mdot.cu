@@ -27,6 +27,7 @@ mdot_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
             const double* __restrict__ y0, const double* __restrict__ y1,
             double* __restrict__ out, double* __restrict__ partial, unsigned* counter,
             const lsb_flags* gate, int it) {
+  pdl_enter();
   if (gated_off(gate, it)) return;
   constexpr int kRows = kTile / R;       // rows per item
   constexpr int kLd = kRows / 64;        // double2 loads per lane per item
@@ -172,8 +173,8 @@ static int launch_mdot_t(const double* X, int64_t ld, int64_t n, int p, const do
   if (ws->grid > 0 && ws->grid < grid) grid = ws->grid;
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
-  mdot_kernel<NV, R, SLOTS><<<(unsigned)grid, kThreads, 0, st>>>(X, ld, n, p, u, w, out,
-                                                                ws->partial, ws->counter, gate, it);
+  launch_chain(use_pdl(n), mdot_kernel<NV, R, SLOTS>, dim3((unsigned)grid), dim3(kThreads), 0, st, X, ld, n, p,
+               u, w, out, ws->partial, ws->counter, gate, it);
   return check_launch("mdot");
 }
 

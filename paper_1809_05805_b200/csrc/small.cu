@@ -18,6 +18,7 @@ namespace lsb {
 // ------------------------------------------------------------------ mgs_lvl2
 __global__ void __launch_bounds__(kSmall)
 mgs_lvl2_small_kernel(lsb_arnoldi S, int it, int p, int ks, int gc, bool use_smem) {
+  pdl_enter();
   if (gated_off(S.flags, it)) return;
   __shared__ SmallShared sh;
   extern __shared__ double sT[];
@@ -278,7 +279,8 @@ int launch_mgs_lvl2_small(const lsb_arnoldi& S, int it, int p, int ks, int gc, c
   }
   const size_t need = sizeof(double) * (size_t)p * p;
   const bool use = need <= kMaxT;
-  mgs_lvl2_small_kernel<<<1, kSmall, use ? need : 0, st>>>(S, it, p, ks, gc, use);
+  launch_chain(use_pdl(S.n), mgs_lvl2_small_kernel, dim3(1), dim3(kSmall), use ? need : 0, st, S, it, p, ks, gc,
+               use);
   return check_launch("mgs_lvl2_small");
 }
 int launch_cgs2_small_a(const lsb_arnoldi& S, int it, int p, int ks, int gc, cudaStream_t st) {

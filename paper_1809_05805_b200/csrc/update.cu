@@ -73,6 +73,7 @@ int launch_maxpy(const double* y, const double* X, int64_t ld, int64_t n, int p,
 // writes u and w.
 __global__ void __launch_bounds__(kThreads)
 lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks) {
+  pdl_enter();
   if (gated_off(S.flags, it)) return;
   if (S.flags && S.flags->broke_iter == it) return;
   extern __shared__ double sc[];
@@ -120,7 +121,8 @@ lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks) {
 int launch_lagged_update(const lsb_arnoldi& S, int it, int p, int ks, cudaStream_t st) {
   if (p < 1) return LSB_OK;
   static const int occ_ = wave(lagged_update_kernel, 2048);
-  lagged_update_kernel<<<row_grid(S.n, occ_), kThreads, coef_smem(p), st>>>(S, it, p, ks);
+  launch_chain(use_pdl(S.n), lagged_update_kernel, dim3((unsigned)row_grid(S.n, occ_)), dim3(kThreads),
+               coef_smem(p), st, S, it, p, ks);
   return check_launch("lagged_update");
 }
 
