@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 lagged_update_reduce_kernel(lsb_arnoldi S, int it, int p, int ks, int ns, int direct, int spread,
                             double* __restrict__ out, double* __restrict__ partial,
                             unsigned* counter) {
+  pdl_enter();
   if (gated_off(S.flags, it)) return;
   if (!direct && S.flags && S.flags->broke_iter == it) return;
   static_assert(T % 64 == 0 && (T <= kThreads || T % kThreads == 0), "tile rows");
@@ -244,7 +245,9 @@ int launch_k3_t(const lsb_arnoldi& S, int it, int p, int ks, int direct, cudaStr
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
   const int spread = occ < 2;
-  kern<<<(unsigned)grid, kThreads, sm, st>>>(S, it, p, ks, ns, direct, spread, S.Gloc, S.ws.partial,
+  // two-sync chain (K5a -> K3 -> K5b -> K4): PDL only for p <= 32 -- at
+  // p ~ 50 it cost 3-4% per step at n = 2^21..2^22 (tools/c3_sweep.py A/B)
+  launch_chain(use_pdl(S.n) && p <= 32, kern, dim3((unsigned)grid), dim3(kThreads), sm, st, S, it, p, ks, ns, direct, spread, S.Gloc, S.ws.partial,
                                              S.ws.counter);
   return check_launch("lagged_update_reduce");
 }

@@ -50,6 +50,7 @@ int launch_settle(const lsb_arnoldi& S, int it, int gc, cudaStream_t st) {
 // ------------------------------------------------------------------ cgs2_lvl2
 __global__ void __launch_bounds__(kSmall)
 cgs2_small_a_kernel(lsb_arnoldi S, int it, int p, int ks, int gc) {
+  pdl_enter();
   if (gated_off(S.flags, it)) return;
   __shared__ SmallShared sh;
   const int t = threadIdx.x, cap = S.cap;
@@ -79,6 +80,7 @@ cgs2_small_a_kernel(lsb_arnoldi S, int it, int p, int ks, int gc) {
 // s = gathered second-pass products; R[:p, p] = r + s   (gram_schmidt.py:276-278)
 __global__ void __launch_bounds__(kSmall)
 cgs2_small_b_kernel(lsb_arnoldi S, int it, int p) {
+  pdl_enter();
   if (gated_off(S.flags, it)) return;
   if (S.flags->broke_iter == it) return;
   for (int j = threadIdx.x; j < p; j += blockDim.x) {
@@ -285,11 +287,11 @@ int launch_mgs_lvl2_small(const lsb_arnoldi& S, int it, int p, int ks, int gc, c
 }
 int launch_cgs2_small_a(const lsb_arnoldi& S, int it, int p, int ks, int gc, cudaStream_t st) {
   if (p < 1 || S.cap > kSmall || p >= S.cap) return LSB_ERANGE;
-  cgs2_small_a_kernel<<<1, kSmall, 0, st>>>(S, it, p, ks, gc);
+  launch_chain(use_pdl(S.n) && p <= 32, cgs2_small_a_kernel, dim3(1), dim3(kSmall), 0, st, S, it, p, ks, gc);
   return check_launch("cgs2_small_a");
 }
 int launch_cgs2_small_b(const lsb_arnoldi& S, int it, int p, cudaStream_t st) {
-  cgs2_small_b_kernel<<<1, kSmall, 0, st>>>(S, it, p);
+  launch_chain(use_pdl(S.n) && p <= 32, cgs2_small_b_kernel, dim3(1), dim3(kSmall), 0, st, S, it, p);
   return check_launch("cgs2_small_b");
 }
 int launch_collect_coef(const lsb_arnoldi& S, int it, int p, int acc, cudaStream_t st) {

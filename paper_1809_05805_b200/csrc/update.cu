@@ -129,6 +129,7 @@ int launch_lagged_update(const lsb_arnoldi& S, int it, int p, int ks, cudaStream
 // w -= Q coef2   (cgs2_lvl2 second projection, gram_schmidt.py:277)
 __global__ void __launch_bounds__(kThreads)
 lagged_correct_kernel(lsb_arnoldi S, int it, int p) {
+  pdl_enter();
   if (gated_off(S.flags, it)) return;
   if (S.flags && S.flags->broke_iter == it) return;
   extern __shared__ double sc[];
@@ -161,7 +162,8 @@ lagged_correct_kernel(lsb_arnoldi S, int it, int p) {
 int launch_lagged_correct(const lsb_arnoldi& S, int it, int p, cudaStream_t st) {
   if (p < 1) return LSB_OK;
   static const int occ_ = wave(lagged_correct_kernel, 2048);
-  lagged_correct_kernel<<<row_grid(S.n, occ_), kThreads, coef_smem(p), st>>>(S, it, p);
+  launch_chain(use_pdl(S.n) && p <= 32, lagged_correct_kernel, dim3((unsigned)row_grid(S.n, occ_)),
+               dim3(kThreads), coef_smem(p), st, S, it, p);
   return check_launch("lagged_correct");
 }
 
