@@ -56,7 +56,8 @@ typedef struct lsb_flags {
   int32_t k;           /* columns consumed by the cycle's least squares     */
   int32_t nonfinite;   /* spmv produced NaN/Inf (kernels.py:271)            */
   int32_t restart_ok;  /* restart residual already <= target               */
-  int32_t pad[2];
+  int32_t comm_error;  /* LSB_COMM_TIMEOUT: a peer exchange timed out        */
+  int32_t pad;
 } lsb_flags;
 
 /* slots of the device scalar block `scal` */
@@ -162,7 +163,7 @@ typedef struct lsb_arnoldi {
 #define LSB_TUNE_PERSIST_CTAS 8   /* lsb_cycle_persistent cluster size 1..16, 0 auto */
 #define LSB_TUNE_FUSED_PIPE 9     /* fused K1+SpMV pipelined stencil: 0 auto (2-4 items/warp), 1 up to 8, 2 off */
 #define LSB_TUNE_CSR_DICT 10      /* dictionary-coded CSR: 0 thread per row, 1 warp-staged index bytes */
-#define LSB_TUNE_PDL 11           /* programmatic dependent launch of the K1/K5/K2 chain: 0 auto (n < 2^23), 1 on, 2 off */
+#define LSB_TUNE_PDL 11           /* programmatic dependent launch of the per-iteration chains (one-sync K1/K5/K2, two-sync K5a/K3/K5b/K4 while p <= 32, lsb_mdot): 0 auto (n < 2^23), 1 on, 2 off */
 #define LSB_TUNE_COUNT 16
 /* Set / read a kernel-variant knob (performance only; results unchanged up
  * to the reduction tree of the affected kernel). Returns the old value. */
@@ -380,6 +381,47 @@ int lsb_back_substitute(const double* tri, const double* g, int32_t m, int32_t k
 /* gram[row, 0..ncols) = V[:, :ncols]^T V[:, row] (measurement only). */
 int lsb_gram_row(const lsb_arnoldi* S, int32_t it, int32_t row, int32_t ncols, double* gram,
                  int64_t gram_ld, void* stream);
+
+/* ---------------------------------------------------------------- peer exchange
+ * The row-partitioned solve's two exchange steps (the
+ * reference's single-process equivalent is the reduction inside
+ * mdot_pair / mass_inner_product / norm2, kernels.py:283-347, and the
+ * SpMV's access to neighbouring rows, kernels.py:256-272) as kernels that
+ * store straight into the peers' memory over NVLink/NVSwitch and signal
+ * with release/acquire epochs kept on the device: no host call per
+ * iteration, capturable in the cycle's CUDA graph.  Pointers in mbox/sig
+ * are this process's mappings of each rank's buffers (CUDA IPC across
+ * processes, plain device pointers within one); epoch and counter are this
+ * rank's own, zero-initialised. */
+#define LSB_PEER_MAX 16
+#define LSB_COMM_TIMEOUT 1
+typedef struct lsb_peer {
+  int32_t rank, size;
+  int32_t slot;          /* doubles per mailbox slot (>= count + 1)            */
+  int32_t pad;
+  int64_t timeout_ns;    /* spin-wait limit, <= 0: 60 s                         */
+  double* mbox[LSB_PEER_MAX];   /* rank q's mailbox: [2][size][slot] doubles    */
+  int64_t* sig[LSB_PEER_MAX];   /* rank q's signal words: [size + 2] int64      */
+  int64_t* epoch;        /* this rank: [0] all-gather, [1] halo, [2] error      */
+  uint32_t* counter;     /* this rank: grid counter (self-resetting)            */
+} lsb_peer;
+/* out[q*out_stride + i] = rank q's local[i], i < count, for every rank q
+ * (one exchange; ranks must call it the same number of times).  Also ORs
+ * every rank's flags->nonfinite into this rank's. */
+int lsb_peer_allgather(const lsb_peer* P, const double* local, int32_t count, double* out,
+                       int32_t out_stride, lsb_flags* flags, void* stream);
+/* Ghost planes: lo_src (this rank's first plane) -> lo_dst (rank-1's upper
+ * ghost, NULL on rank 0), hi_src (last plane) -> hi_dst (rank+1's lower
+ * ghost, NULL on the last rank); returns on the stream once both
+ * neighbours' planes have landed here. */
+int lsb_peer_halo(const lsb_peer* P, const double* lo_src, double* lo_dst, const double* hi_src,
+                  double* hi_dst, int64_t plane, lsb_flags* flags, void* stream);
+/* CUDA IPC of an arbitrary device pointer: handle (64 bytes) of the
+ * allocation that contains ptr, and ptr's offset inside it. */
+int lsb_ipc_export(const void* ptr, void* handle64, int64_t* offset);
+/* Map a peer allocation (lazy peer access enabled) / unmap it. */
+int lsb_ipc_open(const void* handle64, void** base);
+int lsb_ipc_close(void* base);
 
 #ifdef __cplusplus
 }

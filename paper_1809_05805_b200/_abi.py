@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import warnings
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LSB200_LIB", os.path.join(_HERE, "liblsb200.so"))
@@ -38,7 +39,7 @@ class LsbError(RuntimeError):
 class Flags(C.Structure):
     _fields_ = [("stop_iter", C.c_int32), ("status", C.c_int32), ("broke_iter", C.c_int32),
                 ("k", C.c_int32), ("nonfinite", C.c_int32), ("restart_ok", C.c_int32),
-                ("pad", C.c_int32 * 2)]
+                ("comm_error", C.c_int32), ("pad", C.c_int32)]
 
 
 FLAGS_INTS = C.sizeof(Flags) // 4
@@ -80,6 +81,16 @@ class Arnoldi(C.Structure):
                 ("G", C.c_void_p), ("g_parts", C.c_int32), ("g_stride", C.c_int32),
                 ("Gloc", C.c_void_p), ("scal", C.c_void_p), ("res", C.c_void_p),
                 ("flags", C.c_void_p), ("ws", Workspace)]
+
+
+PEER_MAX = 16
+COMM_TIMEOUT = 1
+
+
+class Peer(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("size", C.c_int32), ("slot", C.c_int32), ("pad", C.c_int32),
+                ("timeout_ns", C.c_int64), ("mbox", C.c_void_p * PEER_MAX),
+                ("sig", C.c_void_p * PEER_MAX), ("epoch", C.c_void_p), ("counter", C.c_void_p)]
 
 
 _P = C.c_void_p
@@ -132,6 +143,11 @@ _SIGS = {
     "lsb_gram_row": ([_P, _I32, _I32, _I32, _P, _I64, _P], C.c_int),
     "lsb_givens_update": ([_P, _P, _P, _I32, _P, _I32, _P, _P], C.c_int),
     "lsb_back_substitute": ([_P, _P, _I32, _I32, _P, _P, _P], C.c_int),
+    "lsb_peer_allgather": ([_P, _P, _I32, _P, _I32, _P, _P], C.c_int),
+    "lsb_peer_halo": ([_P, _P, _P, _P, _P, _I64, _P, _P], C.c_int),
+    "lsb_ipc_export": ([_P, _P, _P], C.c_int),
+    "lsb_ipc_open": ([_P, _P], C.c_int),
+    "lsb_ipc_close": ([_P], C.c_int),
 }
 
 EXPORTS = tuple(_SIGS)
@@ -157,10 +173,17 @@ def load(path=None):
         fn = getattr(lib, name)
         fn.argtypes = argt
         fn.restype = rest
-    # LSB_TUNE="key=value,..." (experiments): tuning knobs set at load
+    # LSB_TUNE="key=value,..." (experiments): tuning knobs set at load;
+    # malformed or unknown entries are reported and skipped
     for item in filter(None, os.environ.get("LSB_TUNE", "").split(",")):
         key, _, val = item.partition("=")
-        lib.lsb_set_tuning(int(key), int(val))
+        try:
+            k, v = int(key), int(val)
+        except ValueError:
+            warnings.warn(f"LSB_TUNE: ignoring malformed entry {item!r}")
+            continue
+        if lib.lsb_set_tuning(k, v) != 0:
+            warnings.warn(f"LSB_TUNE: unknown tuning key {k}")
     if path is None:
         _lib = lib
     return lib

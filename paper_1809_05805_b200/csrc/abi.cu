@@ -22,6 +22,15 @@ int sm_count() {
   return g_sms;
 }
 
+int check_launch(const char* what, cudaError_t launch_status) {
+  if (launch_status != cudaSuccess) {
+    cudaGetLastError();   // clear the recorded copy
+    snprintf(g_err, sizeof g_err, "%s: %s", what, cudaGetErrorString(launch_status));
+    return LSB_ECUDA;
+  }
+  return check_launch(what);
+}
+
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -78,6 +87,30 @@ int launch_settle(const lsb_arnoldi&, int, int, cudaStream_t);
 int launch_trial_combine(const lsb_arnoldi&, int, const double*, const double*, double*,
                          const double*, cudaStream_t);
 int launch_back_substitute(const double*, const double*, int, int, double*, int*, cudaStream_t);
+int launch_peer_allgather(const lsb_peer*, const double*, int, double*, int, lsb_flags*,
+                          cudaStream_t);
+int launch_peer_halo(const lsb_peer*, const double*, double*, const double*, double*, int64_t,
+                     lsb_flags*, cudaStream_t);
+
+// cuMemGetAddressRange through the runtime's driver entry point (no link
+// dependency on libcuda: the library must load on hosts without a driver)
+typedef int (*mem_range_fn)(unsigned long long*, size_t*, unsigned long long);
+static mem_range_fn mem_range() {
+  static mem_range_fn f = nullptr;
+  if (!f) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      f = reinterpret_cast<mem_range_fn>(p);
+  }
+  return f;
+}
+static int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return LSB_OK;
+  snprintf(g_err, sizeof g_err, "%s: %s", what, cudaGetErrorString(e));
+  return LSB_ECUDA;
+}
 
 static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -353,6 +386,51 @@ int lsb_givens_update(double* rot, double* g, double* tri, int32_t m, const doub
 int lsb_back_substitute(const double* tri, const double* g, int32_t m, int32_t k, double* y,
                         int32_t* status, void* stream) {
   return launch_back_substitute(tri, g, m, k, y, status, S_(stream));
+}
+
+int lsb_peer_allgather(const lsb_peer* P, const double* local, int32_t count, double* out,
+                       int32_t out_stride, lsb_flags* flags, void* stream) {
+  return launch_peer_allgather(P, local, count, out, out_stride, flags, (cudaStream_t)stream);
+}
+
+int lsb_peer_halo(const lsb_peer* P, const double* lo_src, double* lo_dst, const double* hi_src,
+                  double* hi_dst, int64_t plane, lsb_flags* flags, void* stream) {
+  return launch_peer_halo(P, lo_src, lo_dst, hi_src, hi_dst, plane, flags, (cudaStream_t)stream);
+}
+
+int lsb_ipc_export(const void* ptr, void* handle64, int64_t* offset) {
+  if (!ptr || !handle64 || !offset) return LSB_EINVAL;
+  mem_range_fn f = mem_range();
+  if (!f) {
+    snprintf(g_err, sizeof g_err, "lsb_ipc_export: cuMemGetAddressRange unavailable");
+    return LSB_ECUDA;
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (f(&base, &size, (unsigned long long)(uintptr_t)ptr) != 0) {
+    snprintf(g_err, sizeof g_err, "lsb_ipc_export: cuMemGetAddressRange failed");
+    return LSB_ECUDA;
+  }
+  cudaIpcMemHandle_t h;
+  const int rc = cuda_status(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base), "cudaIpcGetMemHandle");
+  if (rc) return rc;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle64, &h, sizeof h);
+  *offset = (int64_t)((uintptr_t)ptr - (uintptr_t)base);
+  return LSB_OK;
+}
+
+int lsb_ipc_open(const void* handle64, void** base) {
+  if (!handle64 || !base) return LSB_EINVAL;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof h);
+  return cuda_status(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess),
+                     "cudaIpcOpenMemHandle");
+}
+
+int lsb_ipc_close(void* base) {
+  if (!base) return LSB_EINVAL;
+  return cuda_status(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle");
 }
 
 }  // extern "C"

@@ -311,6 +311,8 @@ __device__ inline double givens_fold(double* h, double* rot, double* g, int i) {
 // ---------------------------------------------------------------- launch helpers
 int sm_count();
 int check_launch(const char* what);
+// launch status of an explicit launch (cudaLaunchKernelEx), else the last error
+int check_launch(const char* what, cudaError_t launch_status);
 int tuning(int key);
 
 // Programmatic dependent launch (LSB_TUNE_PDL = 1): the per-iteration chain
@@ -333,11 +335,11 @@ inline bool use_pdl(int64_t n) {
 }
 
 template <typename... KArgs, typename... Args>
-inline void launch_chain(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                         cudaStream_t st, Args... args) {
+inline cudaError_t launch_chain(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                cudaStream_t st, Args... args) {
   if (!pdl) {
     k<<<grid, block, smem, st>>>(args...);
-    return;
+    return cudaSuccess;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -349,7 +351,7 @@ inline void launch_chain(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, s
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
 }  // namespace lsb

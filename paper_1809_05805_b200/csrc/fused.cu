@@ -423,9 +423,9 @@ static int launch_k(Kern kern, bool pipe, int* occ_nx, int* occ, const lsb_arnol
   if (S.ws.grid > 0 && S.ws.grid < grid) grid = S.ws.grid;
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
-  launch_chain(use_pdl(S.n), kern, dim3((unsigned)grid), dim3(kThreads), sm, st, S.V, S.ld, S.n, p,
+  const cudaError_t le = launch_chain(use_pdl(S.n), kern, dim3((unsigned)grid), dim3(kThreads), sm, st, S.V, S.ld, S.n, p,
                S.V + (int64_t)p * S.ld, K, S.Gloc, S.ws.partial, S.ws.counter, S.flags, it);
-  return check_launch("mdot_spmv7");
+  return check_launch("mdot_spmv7", le);
 }
 
 template <int R, int SLOTS, int MINB>

@@ -173,9 +173,9 @@ static int launch_mdot_t(const double* X, int64_t ld, int64_t n, int p, const do
   if (ws->grid > 0 && ws->grid < grid) grid = ws->grid;
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
-  launch_chain(use_pdl(n), mdot_kernel<NV, R, SLOTS>, dim3((unsigned)grid), dim3(kThreads), 0, st, X, ld, n, p,
+  const cudaError_t le = launch_chain(use_pdl(n), mdot_kernel<NV, R, SLOTS>, dim3((unsigned)grid), dim3(kThreads), 0, st, X, ld, n, p,
                u, w, out, ws->partial, ws->counter, gate, it);
-  return check_launch("mdot");
+  return check_launch("mdot", le);
 }
 
 template <int NV, int R>

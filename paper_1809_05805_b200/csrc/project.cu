@@ -247,9 +247,9 @@ int launch_k3_t(const lsb_arnoldi& S, int it, int p, int ks, int direct, cudaStr
   const int spread = occ < 2;
   // two-sync chain (K5a -> K3 -> K5b -> K4): PDL only for p <= 32 -- at
   // p ~ 50 it cost 3-4% per step at n = 2^21..2^22 (tools/c3_sweep.py A/B)
-  launch_chain(use_pdl(S.n) && p <= 32, kern, dim3((unsigned)grid), dim3(kThreads), sm, st, S, it, p, ks, ns, direct, spread, S.Gloc, S.ws.partial,
+  const cudaError_t le = launch_chain(use_pdl(S.n) && p <= 32, kern, dim3((unsigned)grid), dim3(kThreads), sm, st, S, it, p, ks, ns, direct, spread, S.Gloc, S.ws.partial,
                                              S.ws.counter);
-  return check_launch("lagged_update_reduce");
+  return check_launch("lagged_update_reduce", le);
 }
 
 template <int T>

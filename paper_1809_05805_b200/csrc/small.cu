@@ -281,18 +281,18 @@ int launch_mgs_lvl2_small(const lsb_arnoldi& S, int it, int p, int ks, int gc, c
   }
   const size_t need = sizeof(double) * (size_t)p * p;
   const bool use = need <= kMaxT;
-  launch_chain(use_pdl(S.n), mgs_lvl2_small_kernel, dim3(1), dim3(kSmall), use ? need : 0, st, S, it, p, ks, gc,
+  const cudaError_t le = launch_chain(use_pdl(S.n), mgs_lvl2_small_kernel, dim3(1), dim3(kSmall), use ? need : 0, st, S, it, p, ks, gc,
                use);
-  return check_launch("mgs_lvl2_small");
+  return check_launch("mgs_lvl2_small", le);
 }
 int launch_cgs2_small_a(const lsb_arnoldi& S, int it, int p, int ks, int gc, cudaStream_t st) {
   if (p < 1 || S.cap > kSmall || p >= S.cap) return LSB_ERANGE;
-  launch_chain(use_pdl(S.n) && p <= 32, cgs2_small_a_kernel, dim3(1), dim3(kSmall), 0, st, S, it, p, ks, gc);
-  return check_launch("cgs2_small_a");
+  const cudaError_t le = launch_chain(use_pdl(S.n) && p <= 32, cgs2_small_a_kernel, dim3(1), dim3(kSmall), 0, st, S, it, p, ks, gc);
+  return check_launch("cgs2_small_a", le);
 }
 int launch_cgs2_small_b(const lsb_arnoldi& S, int it, int p, cudaStream_t st) {
-  launch_chain(use_pdl(S.n) && p <= 32, cgs2_small_b_kernel, dim3(1), dim3(kSmall), 0, st, S, it, p);
-  return check_launch("cgs2_small_b");
+  const cudaError_t le = launch_chain(use_pdl(S.n) && p <= 32, cgs2_small_b_kernel, dim3(1), dim3(kSmall), 0, st, S, it, p);
+  return check_launch("cgs2_small_b", le);
 }
 int launch_collect_coef(const lsb_arnoldi& S, int it, int p, int acc, cudaStream_t st) {
   collect_coef_kernel<<<1, kSmall, 0, st>>>(S, it, p, acc);

@@ -121,9 +121,9 @@ lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks) {
 int launch_lagged_update(const lsb_arnoldi& S, int it, int p, int ks, cudaStream_t st) {
   if (p < 1) return LSB_OK;
   static const int occ_ = wave(lagged_update_kernel, 2048);
-  launch_chain(use_pdl(S.n), lagged_update_kernel, dim3((unsigned)row_grid(S.n, occ_)), dim3(kThreads),
+  const cudaError_t le = launch_chain(use_pdl(S.n), lagged_update_kernel, dim3((unsigned)row_grid(S.n, occ_)), dim3(kThreads),
                coef_smem(p), st, S, it, p, ks);
-  return check_launch("lagged_update");
+  return check_launch("lagged_update", le);
 }
 
 // w -= Q coef2   (cgs2_lvl2 second projection, gram_schmidt.py:277)
@@ -162,9 +162,9 @@ lagged_correct_kernel(lsb_arnoldi S, int it, int p) {
 int launch_lagged_correct(const lsb_arnoldi& S, int it, int p, cudaStream_t st) {
   if (p < 1) return LSB_OK;
   static const int occ_ = wave(lagged_correct_kernel, 2048);
-  launch_chain(use_pdl(S.n) && p <= 32, lagged_correct_kernel, dim3((unsigned)row_grid(S.n, occ_)),
+  const cudaError_t le = launch_chain(use_pdl(S.n) && p <= 32, lagged_correct_kernel, dim3((unsigned)row_grid(S.n, occ_)),
                dim3(kThreads), coef_smem(p), st, S, it, p);
-  return check_launch("lagged_correct");
+  return check_launch("lagged_correct", le);
 }
 
 // ------------------------------------------------------------------ level-1 MGS pass (K8)

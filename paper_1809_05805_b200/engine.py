@@ -40,12 +40,13 @@ DIRECT = ("mgs_l1", "cgs2")
 class CycleReport:
     """Host copy of what one cycle produced."""
 
-    __slots__ = ("stop_iter", "status", "broke_iter", "k", "nonfinite", "restart_ok", "res",
-                 "scal", "true_res")
+    __slots__ = ("stop_iter", "status", "broke_iter", "k", "nonfinite", "restart_ok",
+                 "comm_error", "res", "scal", "true_res")
 
     def __init__(self, flags, res, scal, true_res=None):
         self.stop_iter, self.status, self.broke_iter, self.k, self.nonfinite, self.restart_ok = (
             int(v) for v in flags[:6])
+        self.comm_error = int(flags[6]) if len(flags) > 6 else 0
         self.res = res
         self.scal = scal
         self.true_res = true_res
@@ -102,8 +103,11 @@ class Engine:
         self.ld = D.round_up(self.off + self.n + self.halo, 32)
         f64 = dict(dtype=D.F64, device=self.dev)
         self.inv_diag = None
+        self._peer = comm is not None and hasattr(comm, "register")
         if inv_diag is not None:
             self.inv_diag = self._vec_with_halo()
+            if self._peer and self.halo:
+                comm.register(self.inv_diag, self.off, self.n)
             self.inv_diag_view().copy_(torch.as_tensor(np.asarray(inv_diag), **f64)
                                        if not isinstance(inv_diag, torch.Tensor) else inv_diag)
             if comm is not None and self.halo:
@@ -148,6 +152,11 @@ class Engine:
             self.gram = None
         self.ws = D.Workspace(cap, self.dev)
         self.x = self._vec_with_halo()
+        if self._peer:
+            comm.flags = C.c_void_p(self.flags.data_ptr())
+            if self.halo:
+                comm.register(self.Vstore, self.off, self.n, ld=self.ld)
+                comm.register(self.x, self.off, self.n)
         self.b = torch.empty(self.n, **f64)       # uploaded before every read
         self.rbuf = torch.empty(self.n, **f64)    # residual: written before read
         self.diagnostics = diagnostics
@@ -155,6 +164,8 @@ class Engine:
         self.true_residual = bool(true_residual)
         if self.true_residual:
             self.xt = self._vec_with_halo()
+            if self._peer and self.halo:
+                comm.register(self.xt, self.off, self.n)
             self.rtrial = torch.zeros(self.n, **f64)
             self.h_true = torch.zeros(m + 1, dtype=D.F64).pin_memory()
         self.S = _abi.Arnoldi(
@@ -170,7 +181,8 @@ class Engine:
         self.scal[_abi.S_BTF] = float(btf)
         # host report buffers (pinned, cached across engines of the same m)
         self.h_flags, self.h_res, self.h_scal = _report_buffers(m)
-        self.use_graph = use_graph and comm is None
+        # multi-rank: capturable when the exchanges are device kernels (PeerComm)
+        self.use_graph = use_graph and (comm is None or getattr(comm, "graph_safe", False))
         self.graph = None
         self.cycles_run = 0
         self.launches_per_cycle = 0
@@ -408,6 +420,8 @@ class Engine:
             f64 = dict(dtype=D.F64, device=self.dev)
             self.ytrial = torch.zeros(self.cap, **f64)
             self.xt = self._vec_with_halo()
+            if self._peer and self.halo:
+                self.comm.register(self.xt, self.off, self.n)
             self.rtrial = torch.zeros(self.n, **f64)
             self.true_res = torch.zeros(self.m + 1, **f64)
 
@@ -507,8 +521,10 @@ class Engine:
                 self.graph = torch.cuda.CUDAGraph()
                 side = torch.cuda.Stream()
                 side.wait_stream(torch.cuda.current_stream())
+                # in-process ranks capture concurrently from their own threads
+                kw = {"capture_error_mode": "thread_local"} if self.comm is not None else {}
                 with torch.cuda.stream(side):
-                    with torch.cuda.graph(self.graph, stream=side):
+                    with torch.cuda.graph(self.graph, stream=side, **kw):
                         self.enqueue_cycle()
                 torch.cuda.current_stream().wait_stream(side)
             self.graph.replay()

@@ -311,6 +311,7 @@ class _DeviceSolve:
         led.iteration = 0
         rep = eng.prologue()
         self._mark("prologue")
+        self._comm_check(rep)
         if rep.nonfinite:
             raise NonFiniteError("spmv result contains NaN or Inf")
         beta = float(rep.scal[_abi.S_RNORM])
@@ -328,7 +329,8 @@ class _DeviceSolve:
         lagged = cfg.method in ("one_sync_mgs", "two_sync_cgs2", "pipeline2")
         # launch-bound sizes: the whole restarted solve is one cluster launch
         # that logs every cycle's report; the shell below replays them
-        whole = eng.persistent and os.environ.get("LSB_PERSISTENT_SOLVE", "1") != "0"
+        whole = eng.persistent and cfg.max_restarts >= 1 \
+            and os.environ.get("LSB_PERSISTENT_SOLVE", "1") != "0"
         device_reports = eng.solve_cycles(cfg.max_restarts) if whole else None
         for _cycle in range(cfg.max_restarts):
             hist.cycle_starts.append(self.global_it)
@@ -339,6 +341,7 @@ class _DeviceSolve:
                 if rep is None:
                     raise RuntimeError("device solve stopped before the restart shell")
             self._mark("cycle")
+            self._comm_check(rep)
             if rep.nonfinite:
                 raise NonFiniteError("spmv result contains NaN or Inf")
             if rep.status == _abi.STARTUP_BREAKDOWN:
@@ -438,6 +441,12 @@ class _DeviceSolve:
             hist.records[-1].true_rel_res = final_rel
         hist.outcome = outcome
         return self._result(eng)
+
+    def _comm_check(self, rep):
+        if rep.comm_error:
+            if self.comm is not None and hasattr(self.comm, "check"):
+                self.comm.check()
+            raise RuntimeError("peer exchange timed out (a rank stopped participating)")
 
     def _record(self, res, nred, gram, ncols, rep=None, i=0):
         """gmres.py:280-292: diagnostics from the device Gram rows, the
@@ -548,4 +557,4 @@ def solve_distributed(op, b_local, comm, n_global, x0_local=None, config=None, l
     if diagnostics_every:
         raise NotImplementedError("per-iteration diagnostics on the multi-rank path")
     return _DeviceSolve(op, b_local, x0_local, config, ledger, diagnostics_every, 0,
-                        use_graph=False, comm=comm, n_global=n_global).run()
+                        use_graph=True, comm=comm, n_global=n_global).run()

@@ -12,6 +12,7 @@ each neighbour (NCCL send/recv, batched).
 
 from __future__ import annotations
 
+import ctypes as C
 import os
 
 import numpy as np
@@ -56,6 +57,12 @@ class Comm:
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+
+    def exchange(self, obj):
+        """Host-side all-gather of a picklable object (setup only)."""
+        out = [None] * self.size
+        dist.all_gather_object(out, obj, group=self.group)
+        return out
 
     def max_scalar(self, v):
         dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
@@ -135,6 +142,15 @@ class ThreadComm:
                 vec[off + n:off + n + plane].copy_(slots[r + 1][0][0], non_blocking=True)
         self._exchange(pub, consume)
 
+    def exchange(self, obj):
+        g = self.g
+        g.barrier.wait()
+        g.slots[self.rank] = (obj, None)
+        g.barrier.wait()
+        out = [x[0] for x in g.slots]
+        g.barrier.wait()
+        return out
+
     def max_scalar(self, v):
         g = self.g
         g.slots[self.rank] = (float(v), None)
@@ -150,8 +166,10 @@ class ThreadComm:
         pass
 
 
-def run_threads(size, fn, *args):
-    """Run fn(comm, *args) on `size` in-process ranks; returns per-rank results."""
+def run_threads(size, fn, *args, peer=False):
+    """Run fn(comm, *args) on `size` in-process ranks; returns per-rank
+    results.  peer=True hands each rank a PeerComm over the ThreadComm (the
+    device-side exchange kernels, peers' buffers as plain pointers)."""
     import threading
     grp = ThreadGroup(size)
     out = [None] * size
@@ -161,7 +179,12 @@ def run_threads(size, fn, *args):
         try:
             s = torch.cuda.Stream()
             with torch.cuda.stream(s):
-                out[r] = fn(ThreadComm(grp, r), *args)
+                c = ThreadComm(grp, r)
+                if peer:
+                    c = PeerComm(c, ipc=False)
+                out[r] = fn(c, *args)
+                if peer:
+                    c.close()
             s.synchronize()
         except BaseException as e:  # pragma: no cover
             err.append(e)
@@ -175,6 +198,158 @@ def run_threads(size, fn, *args):
     if err:
         raise err[0]
     return out
+
+
+class _Reg:
+    __slots__ = ("base", "span", "ld", "off", "n", "ptrs")
+
+
+class PeerComm:
+    """The solver's two exchange steps as device kernels over peer memory
+    (csrc/peer.cu, lsb_peer_allgather / lsb_peer_halo): every rank's
+    mailbox, signal words and halo target vectors are mapped into every
+    rank (CUDA IPC between processes -- NVLink/NVSwitch P2P between GPUs --
+    or plain pointers between ranks sharing a process), the exchanges signal
+    with epochs kept on the device, so a multi-rank cycle needs no host
+    call per iteration and is captured in a CUDA graph like the one-GPU
+    cycle.  The host communicator `host` (Comm over torch.distributed, or
+    ThreadComm) is used only at setup and for host-side scalars/barriers.
+
+    Same interface as Comm for the engine: allgather(local, out) and
+    halo(vec, off, n, plane); plus register(...) so that halo() can address
+    the neighbours' copy of a vector, and check() to raise on a timeout."""
+
+    graph_safe = True
+
+    def __init__(self, host, ipc=True, slot=None, timeout_s=60.0):
+        from . import _abi
+        self.host = host
+        self.rank, self.size = host.rank, host.size
+        if self.size > _abi.PEER_MAX:
+            raise ValueError(f"at most {_abi.PEER_MAX} ranks")
+        self.ipc = bool(ipc)
+        self.lib = _abi.load()
+        self._opened = {}
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.slot = int(slot or 2 * 130 + 8)          # 2 cap + nonfinite word, cap <= 130
+        self.mbox = torch.zeros(2 * self.size * self.slot, dtype=torch.float64, device=dev)
+        self.sig = torch.zeros(self.size + 2, dtype=torch.int64, device=dev)
+        self.ctr = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.counter = torch.zeros(8, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize()
+        mb, sg = self._share(self.mbox), self._share(self.sig)
+        P = _abi.Peer()
+        P.rank, P.size, P.slot = self.rank, self.size, self.slot
+        P.timeout_ns = int(timeout_s * 1e9)
+        for q in range(self.size):
+            P.mbox[q], P.sig[q] = mb[q], sg[q]
+        P.epoch, P.counter = self.ctr.data_ptr(), self.counter.data_ptr()
+        self.P = P
+        self.Pref = C.byref(P)
+        self._regs = []
+        self.flags = None          # the current engine's flag block (error reporting)
+        self.host.barrier()
+
+    # ------------------------------------------------------------ setup
+    def _share(self, t):
+        """Per-rank device pointers of the peers' copies of `t` (valid here)."""
+        if not self.ipc:
+            return self.host.exchange(t.data_ptr())
+        from . import _abi
+        h = (C.c_char * 64)()
+        off = C.c_int64()
+        _abi.check(self.lib.lsb_ipc_export(C.c_void_p(t.data_ptr()), h, C.byref(off)),
+                   "lsb_ipc_export")
+        allh = self.host.exchange((bytes(h), off.value))
+        out = []
+        for q, (hb, o) in enumerate(allh):
+            if q == self.rank:
+                out.append(t.data_ptr())
+                continue
+            base = self._opened.get(hb)
+            if base is None:
+                bp = C.c_void_p()
+                _abi.check(self.lib.lsb_ipc_open(C.create_string_buffer(hb, 64), C.byref(bp)),
+                           "lsb_ipc_open")
+                base = self._opened[hb] = bp.value
+            out.append(base + o)
+        return out
+
+    def register(self, t, off, n, ld=0):
+        """Collective: make `t` (a vector with ghost padding around
+        t[off:off+n], or a 2-D array of such rows ld doubles apart) a halo
+        target.  Every rank registers the same buffers in the same order."""
+        r = _Reg()
+        r.base = t.data_ptr()
+        r.span = 8 * t.numel()
+        r.ptrs = self._share(t)
+        info = self.host.exchange((int(ld), int(off), int(n)))
+        r.ld = [i[0] for i in info]
+        r.off = [i[1] for i in info]
+        r.n = [i[2] for i in info]
+        self._regs.append(r)
+        return r
+
+    def unregister_all(self):
+        self._regs = []
+
+    def _find(self, p):
+        for r in reversed(self._regs):
+            if r.base <= p < r.base + r.span:
+                me = r.ld[self.rank]
+                j = (p - r.base) // (8 * me) if me else 0
+                return r, j
+        raise KeyError("halo on a buffer that was not registered with PeerComm.register")
+
+    # ------------------------------------------------------------ exchanges
+    def allgather(self, local, out):
+        L = local.numel()
+        rc = self.lib.lsb_peer_allgather(self.Pref, C.c_void_p(local.data_ptr()), L,
+                                         C.c_void_p(out.data_ptr()), L, self.flags,
+                                         C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        if rc:
+            from . import _abi
+            _abi.check(rc, "lsb_peer_allgather")
+
+    def halo(self, vec, off, n, plane):
+        p = vec.data_ptr()
+        r, j = self._find(p)
+        q = self.rank
+        lo_dst = hi_dst = None
+        if q > 0:
+            lo_dst = C.c_void_p(r.ptrs[q - 1] + 8 * (j * r.ld[q - 1] + r.off[q - 1] + r.n[q - 1]))
+        if q < self.size - 1:
+            hi_dst = C.c_void_p(r.ptrs[q + 1] + 8 * (j * r.ld[q + 1] + r.off[q + 1] - plane))
+        rc = self.lib.lsb_peer_halo(self.Pref, C.c_void_p(p + 8 * off), lo_dst,
+                                    C.c_void_p(p + 8 * (off + n - plane)), hi_dst, int(plane),
+                                    self.flags, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        if rc:
+            from . import _abi
+            _abi.check(rc, "lsb_peer_halo")
+
+    def check(self):
+        """Raise if an exchange kernel timed out (a peer died or diverged)."""
+        if int(self.ctr[2].item()):
+            raise RuntimeError("peer exchange timed out (a rank stopped participating)")
+
+    # ------------------------------------------------------------ host side
+    def exchange(self, obj):
+        return self.host.exchange(obj)
+
+    def max_scalar(self, v):
+        return self.host.max_scalar(v)
+
+    def barrier(self):
+        torch.cuda.current_stream().synchronize()
+        self.host.barrier()
+
+    def close(self):
+        torch.cuda.synchronize()
+        self.host.barrier()
+        for base in self._opened.values():
+            self.lib.lsb_ipc_close(C.c_void_p(base))
+        self._opened = {}
+        self._regs = []
 
 
 def slab_bounds(nz, size, rank):

@@ -224,7 +224,37 @@ def extras():
     _save("extras.npz", **out)
 
 
-def big_c2(N=256, methods=("one_sync_mgs",)):
+def jacobi():
+    """Right Jacobi preconditioning (gmres.py:106-126, 254, 264-265, 277, 297)
+    on a 2D 5-point matrix whose diagonal varies in [4, 10] (so M^-1 is not a
+    multiple of the identity), several restarts, every method."""
+    O = orc.laplace2d(24)
+    rng = np.random.default_rng(8)
+    vals = O.values.copy()
+    rows = np.repeat(np.arange(O.n_rows), np.diff(O.row_ptr))
+    vals[O.col_idx == rows] += rng.uniform(0.0, 6.0, O.n_rows)
+    A = ls.CsrMatrix(O.n_rows, O.n_cols, O.row_ptr, O.col_idx, vals)
+    b = ls.gen_rhs("random", A, 5)
+    out = dict(row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values, b=b)
+    for meth in ("one_sync_mgs", "two_sync_cgs2", "mgs_l1", "cgs2", "pipeline2", "cgs1_ghysels"):
+        led = ls.ReductionLedger()
+        cfg = ls.GmresConfig(restart_m=10, max_restarts=200, rel_tol=1e-10, method=meth,
+                             precond="jacobi")
+        x, h = ls.solve(A, b, config=cfg, ledger=led, diagnostics_every=0)
+        ev = led.events
+        out.update({f"{meth}__x": x, f"{meth}__curve": h.implicit_curve(),
+                    f"{meth}__cycle_starts": np.array(h.cycle_starts),
+                    f"{meth}__outcome": np.array(h.outcome),
+                    f"{meth}__final_true_rel_res": np.array(h.final_true_rel_res),
+                    f"{meth}__ev_kind": np.array([e.kind for e in ev]),
+                    f"{meth}__ev_count": np.array([e.scalar_count for e in ev]),
+                    f"{meth}__ev_iter": np.array([e.iteration for e in ev]),
+                    f"{meth}__ev_elig": np.array([e.overlap_eligible for e in ev])})
+        print("jacobi", meth, len(h.implicit_curve()), h.outcome, h.final_true_rel_res)
+    _save("jacobi.npz", **out)
+
+
+def big_c2(N=256, methods=("one_sync_mgs",), tag=""):
     t0 = time.perf_counter()
     A = _ref_csr(orc.laplace3d(N))
     b = ls.gen_rhs("random", A, 42)
@@ -235,7 +265,7 @@ def big_c2(N=256, methods=("one_sync_mgs",)):
         r.pop("x")
         out.update({f"{meth}__{k}": v for k, v in r.items()})
         print(f"L3D{N}", meth, len(r["curve"]), r["outcome"], r["seconds"], flush=True)
-    _save(f"laplace3d{N}.npz", **out)
+    _save(f"laplace3d{N}{tag}.npz", **out)
 
 
 def big_c5(N=64):
@@ -260,5 +290,14 @@ if __name__ == "__main__":
         ghysels()
     elif what == "c2":
         big_c2(int(sys.argv[2]) if len(sys.argv) > 2 else 256)
+    elif what == "l3d64":
+        # P = 8 slab tests (8 planes per rank): 3D 7-point 64^3, GMRES(50), tol 1e-6
+        big_c2(64, ("one_sync_mgs", "two_sync_cgs2"))
+    elif what == "c2m":
+        # one further C2 variant per process, so they can run side by side:
+        #   python tests/golden/make_golden.py c2m two_sync_cgs2   (-> laplace3d256_two_sync_cgs2.npz)
+        big_c2(256, (sys.argv[2],), tag="_" + sys.argv[2])
+    elif what == "jacobi":
+        jacobi()
     elif what == "c5":
         big_c5(int(sys.argv[2]) if len(sys.argv) > 2 else 64)

@@ -63,6 +63,9 @@ int main(void){
         sizeof(lsb_stencil), sizeof(lsb_arnoldi));
  printf("%zu %zu %zu %zu\n", offsetof(lsb_arnoldi, G), offsetof(lsb_arnoldi, Gloc),
         offsetof(lsb_arnoldi, ws), offsetof(lsb_stencil, col_scale));
+ printf("%zu %zu %zu %zu %zu %zu\n", sizeof(lsb_peer), offsetof(lsb_peer, timeout_ns),
+        offsetof(lsb_peer, sig), offsetof(lsb_peer, epoch), offsetof(lsb_peer, counter),
+        offsetof(lsb_flags, comm_error));
  return 0;}
 """
     d = "/tmp/lsb_abi_check"
@@ -73,7 +76,10 @@ int main(void){
                            os.path.join(d, "a.out"), os.path.join(d, "a.c")])
     out = subprocess.run([os.path.join(d, "a.out")], capture_output=True, text=True).stdout.split()
     sizes = [int(v) for v in out[:5]]
-    offs = [int(v) for v in out[5:]]
+    offs = [int(v) for v in out[5:9]]
+    peer = [int(v) for v in out[9:]]
+    assert peer == [C.sizeof(_abi.Peer), _abi.Peer.timeout_ns.offset, _abi.Peer.sig.offset,
+                    _abi.Peer.epoch.offset, _abi.Peer.counter.offset, _abi.Flags.comm_error.offset]
     assert sizes == [C.sizeof(_abi.Flags), C.sizeof(_abi.Workspace), C.sizeof(_abi.Csr),
                      C.sizeof(_abi.Stencil), C.sizeof(_abi.Arnoldi)]
     assert offs == [_abi.Arnoldi.G.offset, _abi.Arnoldi.Gloc.offset, _abi.Arnoldi.ws.offset,

@@ -1,8 +1,12 @@
-"""Multi-rank path with the real kernels on one GPU: P ranks run as threads
-(parallel.ThreadComm), each on its own stream, exchanging the per-iteration
-partials (all-gather + fixed-order sum) and the ghost z-planes through
-device memory exactly as the NCCL communicator does across GPUs.  The
-row-partitioned solve must reproduce the reference's golden history."""
+"""Multi-rank path with the real kernels on one GPU: P ranks run as threads,
+each on its own stream, exchanging the per-iteration partials (all-gather +
+fixed-order sum) and the ghost z-planes through device memory -- either by
+host-synchronised copies (parallel.ThreadComm, the data movement of the NCCL
+communicator) or by the peer-memory exchange kernels of the multi-GPU
+product path (parallel.PeerComm: lsb_peer_allgather / lsb_peer_halo, device
+epochs, CUDA-graph-captured cycles).  The row-partitioned solve must
+reproduce the reference's golden history; a two-process test maps the peer
+buffers with CUDA IPC, as ranks on different GPUs do."""
 
 import os
 
@@ -37,11 +41,12 @@ def _rank(comm, dims, meth, m, restarts, tol):
 
 @pytest.mark.parametrize("ranks,meth", [(2, "one_sync_mgs"), (4, "one_sync_mgs"),
                                         (2, "two_sync_cgs2"), (2, "mgs_l1"), (2, "cgs2"),
-                                        (3, "pipeline2")])
-def test_slab_partition_reproduces_reference(P, ranks, meth):
+                                        (3, "pipeline2"), (8, "one_sync_mgs")])
+@pytest.mark.parametrize("peer", [False, True], ids=["threadcomm", "peer"])
+def test_slab_partition_reproduces_reference(P, ranks, meth, peer):
     from paper_1809_05805_b200.parallel import run_threads
     G = np.load(os.path.join(GOLD, "laplace3d32.npz"))
-    out = run_threads(ranks, _rank, (32, 32, 32), meth, 50, 50, 1e-6)
+    out = run_threads(ranks, _rank, (32, 32, 32), meth, 50, 50, 1e-6, peer=peer)
     c0 = out[0][1]
     for r in range(1, ranks):   # replicated small state: identical on every rank
         assert np.array_equal(out[r][1], c0)
@@ -69,19 +74,145 @@ def _rank_scaled(comm, dims, scale):
 
 
 @pytest.mark.parametrize("scale", [2.0 ** 600, 2.0 ** -600])
-def test_slab_partition_restart_norm_out_of_range(P, scale):
+@pytest.mark.parametrize("peer", [False, True], ids=["threadcomm", "peer"])
+def test_slab_partition_restart_norm_out_of_range(P, scale, peer):
     """|b| ~ 2^±600: the restart norm's sum of squares over- or underflows
     unless rescaled; across ranks the exact power-of-two rescale needs the
     global max|r| (second all-gather).  Scaling b by a power of two scales
     every quantity exactly, so the history equals the unscaled golden one."""
     from paper_1809_05805_b200.parallel import run_threads
     G = np.load(os.path.join(GOLD, "laplace3d32.npz"))
-    out = run_threads(2, _rank_scaled, (32, 32, 32), scale)
+    out = run_threads(2, _rank_scaled, (32, 32, 32), scale, peer=peer)
     c0 = out[0][1]
     assert np.array_equal(out[1][1], c0)
     cr = G["one_sync_mgs__curve"]
     assert len(c0) == len(cr) and np.max(np.abs(c0 - cr) / cr) <= 1e-10
     assert out[0][2] == str(G["one_sync_mgs__outcome"])
     x = np.concatenate([o[0] for o in out]) / scale
+    xr = G["one_sync_mgs__x"]
+    assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+
+
+@pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2"])
+def test_p8_slabs_64cube_reproduce_reference(P, meth):
+    """Config 4's rank count (P = 8, 8 z-planes per rank) on the peer path:
+    3D 7-point 64^3 GMRES(50) against the reference's own run
+    (tests/golden/laplace3d64.npz, make_golden.py l3d64)."""
+    from paper_1809_05805_b200.parallel import run_threads
+    G = np.load(os.path.join(GOLD, "laplace3d64.npz"))
+    out = run_threads(8, _rank, (64, 64, 64), meth, 50, 100, 1e-6, peer=True)
+    c0 = out[0][1]
+    for r in range(1, 8):
+        assert np.array_equal(out[r][1], c0) and out[r][3] == out[0][3]
+    cr = G[meth + "__curve"]
+    assert len(c0) == len(cr)
+    assert np.max(np.abs(c0 - cr) / cr) <= 1e-10
+    assert out[0][5] == list(G[meth + "__cycle_starts"])
+    assert [e[1] for e in out[0][3]] == list(G[meth + "__ev_kind"])
+    assert [e[2] for e in out[0][3]] == list(G[meth + "__ev_count"])
+
+
+def _rank27(comm, N, meth):
+    import paper_1809_05805_b200 as P
+    from paper_1809_05805_b200.parallel import local_rhs, slab_problem
+    op, ng = slab_problem((N, N, N), comm, kind="convdiff27")
+    b = local_rhs((N, N, N), comm, 42)
+    led = P.ReductionLedger()
+    cfg = P.GmresConfig(restart_m=100, max_restarts=20, rel_tol=1e-10, method=meth)
+    x, h = P.gmres.solve_distributed(op, b, comm, ng, config=cfg, ledger=led)
+    return x, h.implicit_curve(), h.outcome, [e.kind for e in led.events], list(h.cycle_starts)
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+@pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2"])
+def test_convdiff27_slabs_reproduce_reference(P, ranks, meth):
+    """27-point convection-diffusion z-slabs (every plane of a slab reads
+    both neighbour planes) on the peer path against the reference's run
+    (tests/golden/convdiff27_16.npz)."""
+    from paper_1809_05805_b200.parallel import run_threads
+    G = np.load(os.path.join(GOLD, "convdiff27_16.npz"))
+    out = run_threads(ranks, _rank27, 16, meth, peer=True)
+    c0 = out[0][1]
+    for r in range(1, ranks):
+        assert np.array_equal(out[r][1], c0)
+    cr = G[meth + "__curve"]
+    assert len(c0) == len(cr) and out[0][2] == str(G[meth + "__outcome"])
+    assert np.max(np.abs(c0 - cr) / cr) <= 1e-10
+    assert out[0][4] == list(G[meth + "__cycle_starts"])
+    assert out[0][3] == list(G[meth + "__ev_kind"])
+    x = np.concatenate([o[0] for o in out])
+    xr = G[meth + "__x"]
+    assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+
+
+def test_peer_cycle_is_graph_captured(P):
+    """With PeerComm the multi-rank cycle is a CUDA graph (no host call per
+    iteration): from the second cycle on, every cycle is a replay."""
+    from paper_1809_05805_b200.parallel import run_threads, local_rhs, slab_problem
+    from paper_1809_05805_b200.engine import Engine
+
+    def body(comm):
+        op, ng = slab_problem((32, 32, 32), comm)
+        b = local_rhs((32, 32, 32), comm, 42)
+        eng = Engine(op, 20, "one_sync_mgs", 1e-14, comm=comm, n_global=ng)
+        eng.load(torch.as_tensor(b).cuda())
+        eng.prologue()
+        reps = [eng.cycle() for _ in range(3)]
+        return eng.graph is not None, [r.res.copy() for r in reps]
+
+    out = run_threads(2, body, peer=True)
+    assert out[0][0] and out[1][0]
+    for a, b in zip(out[0][1], out[1][1]):
+        assert np.array_equal(a, b)
+
+
+def _ipc_worker(rank, size, port, q):
+    import torch.distributed as dist
+    os.environ.setdefault("LSB_QUIET", "1")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=size)
+    try:
+        from paper_1809_05805_b200.parallel import Comm, PeerComm
+        comm = PeerComm(Comm(), ipc=True)
+        res = _rank(comm, (32, 32, 32), "one_sync_mgs", 50, 50, 1e-6)
+        comm.close()
+        q.put((rank, res[0], res[1], res[2], res[3], res[5]))
+    except BaseException as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_ipc_two_processes(P):
+    """Two processes (as torchrun would start them) exchange through CUDA
+    IPC mappings of each other's buffers -- the multi-GPU transport -- here
+    both on the one GPU.  Same history as the reference golden."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in ps:
+        p_.start()
+    res = {}
+    for _ in range(2):
+        item = q.get(timeout=600)
+        res[item[0]] = item
+    for p_ in ps:
+        p_.join(timeout=120)
+    for r in range(2):
+        assert len(res[r]) > 2, res[r]
+    G = np.load(os.path.join(GOLD, "laplace3d32.npz"))
+    c0, c1 = res[0][2], res[1][2]
+    assert np.array_equal(c0, c1)
+    cr = G["one_sync_mgs__curve"]
+    assert len(c0) == len(cr) and np.max(np.abs(c0 - cr) / cr) <= 1e-10
+    assert res[0][5] == list(G["one_sync_mgs__cycle_starts"])
+    x = np.concatenate([res[0][1], res[1][1]])
     xr = G["one_sync_mgs__x"]
     assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)

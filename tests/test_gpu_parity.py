@@ -521,35 +521,40 @@ def test_jacobi_preconditioner_identity(P):
     assert np.allclose(x, [2.0, 2.0, 2.0], rtol=1e-12)
 
 
-@pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2", "mgs_l1", "cgs2", "pipeline2"])
+@pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2", "mgs_l1", "cgs2", "pipeline2",
+                                  "cgs1_ghysels"])
 @pytest.mark.parametrize("persist", ["0", "1"])
-def test_jacobi_restarts_match_oracle(P, monkeypatch, meth, persist):
+def test_jacobi_restarts_match_reference(P, monkeypatch, meth, persist):
     """Right Jacobi preconditioning over several restarts on a matrix with a
-    varying diagonal: the restart residuals are b - A x with A itself
-    (gmres.py:472/498/511), the Krylov products A M^-1 v (gmres.py:264-265).
-    Same iteration count, outcome and cycle starts as the oracle, curve
-    within 1e-10, same final true residual and x."""
+    varying diagonal, against the REFERENCE's run (tests/golden/jacobi.npz,
+    make_golden.py jacobi): the restart residuals are b - A x with A itself
+    (gmres.py:472/498/511), the Krylov products A M^-1 v (gmres.py:264-265),
+    x += M^-1 V y (277, 297).  Same iteration count, outcome, cycle starts and
+    ledger, curve within 1e-10, same final true residual and x."""
     monkeypatch.setenv("LSB_PERSISTENT", persist)
-    O = orc.laplace2d(24)
-    rng = np.random.default_rng(8)
-    vals = O.values.copy()
-    rows = np.repeat(np.arange(O.n_rows), np.diff(O.row_ptr))
-    diag = O.col_idx == rows
-    vals[diag] += rng.uniform(0.0, 6.0, O.n_rows)            # diagonal 4 .. 10
-    Oj = orc.Csr(O.n_rows, O.n_cols, O.row_ptr, O.col_idx, vals)
-    A = P.CsrMatrix(O.n_rows, O.n_cols, O.row_ptr, O.col_idx, vals)
-    b = orc.rhs_random(O.n_rows, 5)
-    ref = orc.gmres(Oj, b, meth, 10, 200, 1e-10, jacobi=True)
+    G = _load("jacobi.npz")
+    n = int(G["row_ptr"].size - 1)
+    A = P.CsrMatrix(n, n, G["row_ptr"], G["col_idx"], G["values"])
+    b = G["b"]
     cfg = P.GmresConfig(restart_m=10, max_restarts=200, rel_tol=1e-10, method=meth,
                         precond="jacobi")
-    x, h = P.solve(A, b, config=cfg, diagnostics_every=0)
-    c, cr = h.implicit_curve(), np.array(ref.curve)
-    assert len(c) == len(cr) and h.outcome == ref.outcome and h.cycle_starts == ref.cycle_starts
+    led = P.ReductionLedger()
+    x, h = P.solve(A, b, config=cfg, ledger=led, diagnostics_every=0)
+    p = meth + "__"
+    c, cr = h.implicit_curve(), G[p + "curve"]
+    assert len(c) == len(cr) and h.outcome == str(G[p + "outcome"])
+    assert h.cycle_starts == list(G[p + "cycle_starts"])
+    assert [e.kind for e in led.events] == list(G[p + "ev_kind"])
+    assert [e.scalar_count for e in led.events] == list(G[p + "ev_count"])
+    assert [e.iteration for e in led.events] == list(G[p + "ev_iter"])
+    assert [e.overlap_eligible for e in led.events] == list(G[p + "ev_elig"])
     big = cr > 1e-8 * cr[0]   # below: restart residuals at the tolerance are cancellation noise
     assert np.max(np.abs(c - cr)[big] / cr[big]) <= 1e-10
     assert np.max(np.abs(c - cr)[~big], initial=0.0) <= 1e-14 * cr[0]
-    assert abs(h.final_true_rel_res - ref.final_true_rel_res) <= 1e-3 * ref.final_true_rel_res + 1e-15
-    assert np.linalg.norm(x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+    f = float(G[p + "final_true_rel_res"])
+    assert abs(h.final_true_rel_res - f) <= 1e-3 * f + 1e-15
+    xr = G[p + "x"]
+    assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
 
 
 @pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2", "mgs_l1", "cgs2"])

@@ -150,3 +150,27 @@ def test_ghysels_matches_reference(tag):
     assert len(run.curve) == len(curve) and run.outcome == str(G[p + "outcome"])
     assert np.max(np.abs(np.array(run.curve) - curve) / np.maximum(curve, 1e-300)) <= 1e-9
     assert [e[1] for e in run.ledger.events] == list(G[p + "ev_kind"])
+
+
+JACOBI_METHODS = ["one_sync_mgs", "two_sync_cgs2", "mgs_l1", "cgs2", "pipeline2", "cgs1_ghysels"]
+
+
+@pytest.mark.parametrize("meth", JACOBI_METHODS)
+def test_jacobi_matches_reference(meth):
+    """The oracle's right-Jacobi branch (oracle/lowsync_oracle.py, gmres.py:106-126,
+    264-265, 277, 297) against the reference run on a varying-diagonal matrix
+    (tests/golden/make_golden.py jacobi)."""
+    G = _load("jacobi.npz")
+    A = orc.Csr(int(G["row_ptr"].size - 1), int(G["row_ptr"].size - 1), G["row_ptr"], G["col_idx"],
+                G["values"])
+    run = orc.gmres(A, G["b"], meth, 10, 200, 1e-10, jacobi=True)
+    p = meth + "__"
+    curve = G[p + "curve"]
+    assert len(run.curve) == len(curve) and run.outcome == str(G[p + "outcome"])
+    assert run.cycle_starts == list(G[p + "cycle_starts"])
+    np.testing.assert_allclose(run.curve, curve, rtol=1e-10, atol=0)
+    ev = run.ledger.events
+    assert [e[1] for e in ev] == list(G[p + "ev_kind"])
+    assert [e[2] for e in ev] == list(G[p + "ev_count"])
+    assert [e[0] for e in ev] == list(G[p + "ev_iter"])
+    np.testing.assert_allclose(run.x, G[p + "x"], rtol=1e-9, atol=1e-12)
