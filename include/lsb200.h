@@ -422,6 +422,11 @@ int lsb_ipc_export(const void* ptr, void* handle64, int64_t* offset);
 /* Map a peer allocation (lazy peer access enabled) / unmap it. */
 int lsb_ipc_open(const void* handle64, void** base);
 int lsb_ipc_close(void* base);
+/* Load every kernel of the library into the current context now (instead
+ * of at first launch, CUDA lazy loading): returns the number of kernels
+ * loaded, or -LSB_ECUDA.  The host layer calls it once per process before
+ * the first launch. */
+int lsb_preload(void);
 
 #ifdef __cplusplus
 }

@@ -148,6 +148,7 @@ _SIGS = {
     "lsb_ipc_export": ([_P, _P, _P], C.c_int),
     "lsb_ipc_open": ([_P, _P], C.c_int),
     "lsb_ipc_close": ([_P], C.c_int),
+    "lsb_preload": ([], C.c_int),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -18,11 +18,25 @@ from .errors import DimensionError
 F64 = torch.float64
 
 
+_preloaded = set()
+
+
 def require_cuda():
     if not torch.cuda.is_available():
         raise _abi.LsbUnavailable("no CUDA device: liblsb200 has no CPU fallback")
-    _abi.load()
-    return torch.device("cuda", torch.cuda.current_device())
+    lib = _abi.load()
+    dev = torch.cuda.current_device()
+    if dev not in _preloaded:
+        # every liblsb200 kernel loaded up front (lsb_preload): a lazy first
+        # launch would wait for the device to idle (deadlock-prone while a
+        # peer exchange spins) and would land inside timed regions
+        torch.cuda.init()
+        torch.zeros(1, device=torch.device("cuda", dev))   # context exists
+        if lib.lsb_preload() < 0:
+            import warnings
+            warnings.warn("lsb_preload: " + lib.lsb_last_error().decode(errors="replace"))
+        _preloaded.add(dev)
+    return torch.device("cuda", dev)
 
 
 def stream():

@@ -106,6 +106,25 @@ static mem_range_fn mem_range() {
   }
   return f;
 }
+const void* tu_anchor_fused();
+const void* tu_anchor_mdot();
+const void* tu_anchor_project();
+const void* tu_anchor_spmv();
+const void* tu_anchor_peer();
+const void* tu_anchor_persist();
+const void* tu_anchor_small();
+const void* tu_anchor_update();
+
+template <class F>
+static F driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(p);
+}
+
 static int cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return LSB_OK;
   snprintf(g_err, sizeof g_err, "%s: %s", what, cudaGetErrorString(e));
@@ -431,6 +450,50 @@ int lsb_ipc_open(const void* handle64, void** base) {
 int lsb_ipc_close(void* base) {
   if (!base) return LSB_EINVAL;
   return cuda_status(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle");
+}
+
+int lsb_preload(void) {
+  // Load every kernel of every module of the library now.  Under CUDA's
+  // lazy loading a kernel's first launch loads it, and loading waits for
+  // the context to go idle -- which never happens while an exchange kernel
+  // of this context spins on a peer whose progress needs that launch (ranks
+  // sharing one device).  Also keeps first-launch latency out of timings.
+  typedef int (*get_module_fn)(void**, void*);
+  typedef int (*count_fn)(unsigned*, void*);
+  typedef int (*enum_fn)(void**, unsigned, void*);
+  typedef int (*load_fn)(void*);
+  static const get_module_fn get_module = driver_fn<get_module_fn>("cuFuncGetModule");
+  static const count_fn count = driver_fn<count_fn>("cuModuleGetFunctionCount");
+  static const enum_fn enumerate = driver_fn<enum_fn>("cuModuleEnumerateFunctions");
+  static const load_fn load = driver_fn<load_fn>("cuFuncLoad");
+  if (!get_module || !count || !enumerate || !load) {
+    snprintf(g_err, sizeof g_err, "lsb_preload: driver lacks cuModuleEnumerateFunctions/cuFuncLoad");
+    return -LSB_ECUDA;
+  }
+  const void* anchors[] = {tu_anchor_fused(), tu_anchor_mdot(), tu_anchor_project(),
+                           tu_anchor_spmv(), tu_anchor_peer(), tu_anchor_persist(),
+                           tu_anchor_small(), tu_anchor_update()};
+  int loaded = 0;
+  for (const void* a : anchors) {
+    cudaFunction_t f;
+    int rc = cuda_status(cudaGetFuncBySymbol(&f, a), "cudaGetFuncBySymbol");
+    if (rc) return -rc;
+    void* mod = nullptr;
+    unsigned n = 0;
+    if (get_module(&mod, (void*)f) || count(&n, mod)) {
+      snprintf(g_err, sizeof g_err, "lsb_preload: cannot enumerate a module");
+      return -LSB_ECUDA;
+    }
+    void* fs[512];
+    if (n > 512) n = 512;
+    if (enumerate(fs, n, mod)) {
+      snprintf(g_err, sizeof g_err, "lsb_preload: cuModuleEnumerateFunctions failed");
+      return -LSB_ECUDA;
+    }
+    for (unsigned k = 0; k < n; ++k)
+      if (load(fs[k]) == 0) ++loaded;
+  }
+  return loaded;
 }
 
 }  // extern "C"

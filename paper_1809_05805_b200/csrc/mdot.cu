@@ -226,4 +226,7 @@ int launch_mdot(const double* X, int64_t ld, int64_t n, int p, const double* u, 
   return LSB_OK;
 }
 
+// lsb_preload: one kernel of this translation unit (its module)
+const void* tu_anchor_mdot() { return (const void*)mdot_kernel<1, 1, 1>; }
+
 }  // namespace lsb

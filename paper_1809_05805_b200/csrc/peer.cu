@@ -204,4 +204,7 @@ int launch_peer_halo(const lsb_peer* P, const double* lo_src, double* lo_dst,
   return check_launch("peer_halo");
 }
 
+// lsb_preload: one kernel of this translation unit (its module)
+const void* tu_anchor_peer() { return (const void*)peer_allgather_kernel; }
+
 }  // namespace lsb

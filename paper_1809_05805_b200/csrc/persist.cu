@@ -873,4 +873,7 @@ int launch_cycle_persistent(const lsb_arnoldi& S, const lsb_csr* A, int ks, cuda
   return check_launch("cycle_persistent");
 }
 
+// lsb_preload: one kernel of this translation unit (its module)
+const void* tu_anchor_persist() { return (const void*)persist_cycle_kernel; }
+
 }  // namespace lsb

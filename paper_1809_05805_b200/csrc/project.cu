@@ -300,4 +300,7 @@ int launch_lagged_update_reduce(const lsb_arnoldi& S, int it, int p, int ks, int
   }
 }
 
+// lsb_preload: one kernel of this translation unit (its module)
+const void* tu_anchor_project() { return (const void*)lagged_update_reduce_kernel<1, 128>; }
+
 }  // namespace lsb

@@ -363,4 +363,7 @@ int launch_back_substitute(const double* tri, const double* g, int m, int k, dou
   return check_launch("back_substitute");
 }
 
+// lsb_preload: one kernel of this translation unit (its module)
+const void* tu_anchor_small() { return (const void*)mgs_lvl2_small_kernel; }
+
 }  // namespace lsb

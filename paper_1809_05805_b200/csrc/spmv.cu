@@ -661,4 +661,7 @@ int launch_csr(const lsb_csr* A, const double* x, const double* b, double* y, ls
   return check_launch("csr");
 }
 
+// lsb_preload: one kernel of this translation unit (its module)
+const void* tu_anchor_spmv() { return (const void*)csr_kernel; }
+
 }  // namespace lsb

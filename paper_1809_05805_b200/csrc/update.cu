@@ -514,4 +514,7 @@ int launch_trial_combine(const lsb_arnoldi& S, int it, const double* x, const do
   return check_launch("trial_combine");
 }
 
+// lsb_preload: one kernel of this translation unit (its module)
+const void* tu_anchor_update() { return (const void*)maxpy_kernel; }
+
 }  // namespace lsb

@@ -521,11 +521,20 @@ class Engine:
                 self.graph = torch.cuda.CUDAGraph()
                 side = torch.cuda.Stream()
                 side.wait_stream(torch.cuda.current_stream())
-                # in-process ranks capture concurrently from their own threads
-                kw = {"capture_error_mode": "thread_local"} if self.comm is not None else {}
                 with torch.cuda.stream(side):
-                    with torch.cuda.graph(self.graph, stream=side, **kw):
-                        self.enqueue_cycle()
+                    if self.comm is None:
+                        with torch.cuda.graph(self.graph, stream=side):
+                            self.enqueue_cycle()
+                    else:
+                        # ranks sharing a device (in-process emulation) spin
+                        # on each other's exchange kernels: no device-wide
+                        # synchronize (torch.cuda.graph's entry does one), and
+                        # capture errors only for this thread
+                        self.graph.capture_begin(capture_error_mode="thread_local")
+                        try:
+                            self.enqueue_cycle()
+                        finally:
+                            self.graph.capture_end()
                 torch.cuda.current_stream().wait_stream(side)
             self.graph.replay()
         else:

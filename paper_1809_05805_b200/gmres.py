@@ -306,6 +306,10 @@ class _DeviceSolve:
         self.engine = eng
         self._mark("engine")
         eng.load(self.b, self.x0)
+        if self.comm is not None:
+            # every rank's buffers exist (and are registered) before any
+            # exchange kernel can spin on them
+            self.comm.barrier()
         # the host result buffer is faulted in while the device iterates
         self._xhost = D.HostBuffer(eng.n) if self.host and eng.n >= D._STAGE_MIN else None
         led.iteration = 0

@@ -169,7 +169,15 @@ class ThreadComm:
 def run_threads(size, fn, *args, peer=False):
     """Run fn(comm, *args) on `size` in-process ranks; returns per-rank
     results.  peer=True hands each rank a PeerComm over the ThreadComm (the
-    device-side exchange kernels, peers' buffers as plain pointers)."""
+    device-side exchange kernels, peers' buffers as plain pointers).  On one
+    device the ranks' streams must not share a hardware work queue (a
+    spinning exchange kernel would block the kernels it waits for): set
+    CUDA_DEVICE_MAX_CONNECTIONS=32 before CUDA initialises (tests/conftest.py
+    does)."""
+    if peer and size > 1 and int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8")) < 2 * size:
+        import warnings
+        warnings.warn("run_threads(peer=True) on one device wants CUDA_DEVICE_MAX_CONNECTIONS >= "
+                      "2 x ranks set before CUDA initialises; exchanges may time out")
     import threading
     grp = ThreadGroup(size)
     out = [None] * size
@@ -221,7 +229,7 @@ class PeerComm:
 
     graph_safe = True
 
-    def __init__(self, host, ipc=True, slot=None, timeout_s=60.0):
+    def __init__(self, host, ipc=True, slot=None, timeout_s=None):
         from . import _abi
         self.host = host
         self.rank, self.size = host.rank, host.size
@@ -240,6 +248,8 @@ class PeerComm:
         mb, sg = self._share(self.mbox), self._share(self.sig)
         P = _abi.Peer()
         P.rank, P.size, P.slot = self.rank, self.size, self.slot
+        if timeout_s is None:
+            timeout_s = float(os.environ.get("LSB_PEER_TIMEOUT_S", "60"))
         P.timeout_ns = int(timeout_s * 1e9)
         for q in range(self.size):
             P.mbox[q], P.sig[q] = mb[q], sg[q]

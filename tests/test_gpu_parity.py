@@ -549,7 +549,10 @@ def test_jacobi_restarts_match_reference(P, monkeypatch, meth, persist):
     assert [e.iteration for e in led.events] == list(G[p + "ev_iter"])
     assert [e.overlap_eligible for e in led.events] == list(G[p + "ev_elig"])
     big = cr > 1e-8 * cr[0]   # below: restart residuals at the tolerance are cancellation noise
-    assert np.max(np.abs(c - cr)[big] / cr[big]) <= 1e-10
+    # cgs1_ghysels's implicit residual is the Pythagorean sqrt(|z|^2 - |y|^2):
+    # it loses digits as the radicand shrinks (same bar as its own test: 1e-7)
+    bar = 1e-7 if meth == "cgs1_ghysels" else 1e-10
+    assert np.max(np.abs(c - cr)[big] / cr[big]) <= bar
     assert np.max(np.abs(c - cr)[~big], initial=0.0) <= 1e-14 * cr[0]
     f = float(G[p + "final_true_rel_res"])
     assert abs(h.final_true_rel_res - f) <= 1e-3 * f + 1e-15
