@@ -10,13 +10,27 @@ cycle's least squares, x update and restart residual), all resident in HBM.
 same metric through the public drop-in call `solve(A, b_host, ...)` with the
 host->device copy of b and the device->host copy of x inside each step.
 
---gpus N > 1 (torchrun) runs the row-partitioned (z-slab) solve with one
-NCCL all-gather per iteration plus the halo exchange; per-GPU slab fixed at
-256^3 (weak scaling; N=8 is the 512^3 cube of config 4).
+--gpus N > 1 runs the row-partitioned (z-slab) solve, one process per GPU:
+launched under torchrun by the driver, or re-executed under
+torch.distributed.run by this script when WORLD_SIZE is unset (it exits
+non-zero if the world size then differs from N).  The per-iteration
+exchanges -- one all-gather of the 2p-vector per iteration plus the ghost
+z-planes -- are peer-memory kernels over NVLink (parallel.PeerComm, CUDA
+IPC mappings, captured in the cycle graph); NCCL (NCCL_DEBUG=INFO) carries
+setup and host scalars, and is the fallback transport when peer mappings
+are unavailable (--comm nccl forces it).  Default: weak scaling, 256^3 rows
+per GPU, the global grid doubled x -> y -> z (N=8 is the 512^3 cube of
+config 4); `value` counts 16.7M-row slab iterations/s (global it/s x N, the
+unit the driver's weak-scaling efficiency needs) and `global_it_per_s` is
+the solve's own rate.  --strong runs config 4 as stated (512^3 split over
+N GPUs, value = global it/s).
 
 --impl reference times the reference algorithm on the host cores: the
 numpy oracle port (oracle/lowsync_oracle.py, same numpy/OpenBLAS calls as
-lowsync), a bounded sample of the same workload per step.
+lowsync) on the same C2 solve -- after an untimed prefix of 23 iterations,
+each step is a window of 3 consecutive Arnoldi iterations (p = 24, 25, ...
+continuing through the restart), so the timed steps sample a
+representative mix of p.
 """
 
 from __future__ import annotations
@@ -37,6 +51,7 @@ METRIC = "Arnoldi iters/sec (n=16.7M, m=50); ortho HBM GB/s vs peak; 1/2/4/8 B20
 UNIT = "Arnoldi iterations/s"
 N_SLAB = 256
 M = 50
+C4_ONE_GPU = 104.6   # it/s, 512^3 one-sync GMRES(50) cycle on one B200 (round 1)
 
 
 def _peaks():
@@ -127,50 +142,78 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU side
-def cpu_sample(iters, threads=None):
-    """The reference algorithm (numpy oracle port) on the host cores: the
-    first `iters` Arnoldi iterations of the same C2 solve; solve time only."""
+PREFIX = 23        # untimed Arnoldi iterations before the first CPU window
+PER_WINDOW = 3     # Arnoldi iterations per CPU step
+
+
+def _blas_threads(threads):
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(threads)
+    except Exception:   # noqa: BLE001 -- env var then governs a fresh numpy
+        os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
+        return None
+
+
+def cpu_windows(n_windows, per=PER_WINDOW, prefix=PREFIX, threads=None):
+    """The reference algorithm (numpy oracle port, same numpy/OpenBLAS calls
+    as lowsync) on the host cores: ONE run of the C2 solve; after `prefix`
+    untimed iterations, `n_windows` consecutive windows of `per` Arnoldi
+    iterations (continuing through the restart at 50, whose extract and
+    restart residual belong to the cycle the GPU step times too).
+    Returns (seconds per window, threads)."""
     threads = threads or os.cpu_count()
-    os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
+    lim = _blas_threads(threads)
     from oracle import lowsync_oracle as orc
     A = orc.laplace3d(N_SLAB)
     b = orc.rhs_random(A.n_rows, 42)
-    run = orc.gmres(A, b, "one_sync_mgs", M, 1, 1e-14, max_iters=iters)
-    dt = time.perf_counter() - run.t_first_cycle   # Arnoldi iterations only (no prologue)
-    assert len(run.curve) == iters
-    return iters / dt, dt, threads
+    total = prefix + n_windows * per
+    run = orc.gmres(A, b, "one_sync_mgs", M, total // M + 2, 1e-14, max_iters=total)
+    t = run.iter_t
+    assert len(t) == total
+    out = [t[prefix + (w + 1) * per - 1] - t[prefix + w * per - 1] for w in range(n_windows)]
+    del lim
+    return out, threads
+
+
+def _config(world, slab, strong=False):
+    nx, ny, nz = (512, 512, 512) if strong else _dims(world, slab)
+    n_global = nx * ny * nz
+    return {"workload": f"3D 7-point Laplacian {nx}x{ny}x{nz} (n={n_global:,}), "
+                        "one-sync MGS-CWY GMRES(50), seed-42 unit Gaussian b, x0=0",
+            "n_per_gpu": n_global // world, "m": M, "method": "one_sync_mgs",
+            "step": "one GMRES(50) restart cycle = 50 Arnoldi iterations",
+            "rel_tol": 1e-14, "l2": "inputs larger than L2 (basis 7.0 GB per GPU)"
+            if not strong or world >= 8 else "inputs larger than L2",
+            "partition": "z-slabs" if world > 1 else "none",
+            "value_units": ("global Arnoldi iterations/s of the 512^3 solve" if strong else
+                            f"Arnoldi iterations/s of {slab}^3-row slabs (global it/s x N)")}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    per_step = 3
-    # warm-up steps are real work too (bounded); then time `steps`
-    from oracle import lowsync_oracle as orc
-    threads = os.cpu_count()
-    os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
-    A = orc.laplace3d(N_SLAB)
-    b = orc.rhs_random(A.n_rows, 42)
-    times = []
-    for s in range(args.warmup + args.steps):
-        run = orc.gmres(A, b, "one_sync_mgs", M, 1, 1e-14, max_iters=per_step)
-        dt = time.perf_counter() - run.t_first_cycle   # iterations only, as the GPU arm
-        assert len(run.curve) == per_step
-        if s >= args.warmup:
-            times.append(dt)
-    tot = sum(times)
-    value = per_step * len(times) / tot
-    sample = (f"each step: first {per_step} Arnoldi iterations (prologue excluded) of one-sync GMRES(50) "
-              f"on 256^3 7-point (numpy oracle port, same numpy/OpenBLAS calls as lowsync); "
-              f"early iterations have small p, so this overstates the full-cycle rate")
+    world = args.gpus
+    steps = args.warmup + args.steps
+    secs, threads = cpu_windows(steps)
+    timed = secs[args.warmup:]
+    tot = sum(timed)
+    value = PER_WINDOW * len(timed) / tot
+    first = PREFIX + args.warmup * PER_WINDOW + 1
+    sample = (f"one run of the 256^3 one-sync GMRES(50) solve (numpy oracle port, same "
+              f"numpy/OpenBLAS calls as lowsync): {PREFIX} untimed iterations, {args.warmup} "
+              f"warm-up windows, then each step = {PER_WINDOW} consecutive Arnoldi iterations "
+              f"(timed: iterations {first}..{first + PER_WINDOW * len(timed) - 1}, through the "
+              f"restart at {M})")
+    if world > 1:
+        sample += ("; the CPU's cost is linear in rows, so its rate on one 256^3 slab is its "
+                   "rate in the GPU arm's unit (slab iterations/s = global it/s x N)")
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(timed),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": "3D 7-point Laplacian 256^3 (n=16,777,216), one-sync MGS-CWY "
-                               "GMRES(50), seed-42 unit Gaussian b, x0=0", "n": A.n_rows, "m": M},
+        "data": "synthetic", "config": _config(world, N_SLAB),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -191,33 +234,78 @@ def _ortho_bytes(n, p, kind):
     return 0
 
 
+def _reexec_torchrun(args):
+    """--gpus N > 1 without a launcher: start N ranks under torch.distributed.run."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execvpe(sys.executable, cmd, env)
+
+
+def _make_comm(args, rank):
+    """Host communicator over NCCL, and the peer-memory exchange on top of it
+    (falls back to NCCL collectives if peer mappings are unavailable)."""
+    from paper_1809_05805_b200.parallel import Comm, PeerComm, PeerUnavailable
+    host = Comm.init()
+    if args.comm == "nccl":
+        return host, "nccl"
+    try:
+        pc = PeerComm(host, ipc=True)
+        pc.selftest()
+        return pc, "peer-ipc"
+    except PeerUnavailable as e:
+        if rank == 0:
+            sys.stderr.write(f"bench: peer exchange unavailable ({e}); using NCCL collectives\n")
+        return host, "nccl"
+
+
 def run_gpu(args):
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.emulate_ranks <= 1 and world != args.gpus:
+        sys.stderr.write(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
+    if torch.cuda.device_count() < (args.gpus if args.emulate_ranks <= 1 else 1):
+        sys.stderr.write(f"bench: --gpus {args.gpus} but only {torch.cuda.device_count()} "
+                         "CUDA devices are visible\n")
+        sys.exit(2)
     torch.cuda.set_device(local)
     if args.emulate_ranks > 1:
-        # P ranks as threads on this one GPU (parallel.ThreadComm): exercises
-        # the multi-rank path end to end; the number is NOT a scaling result
+        # P ranks as threads on this one GPU (parallel.run_threads, peer
+        # exchange kernels): exercises the multi-rank path end to end; the
+        # number is NOT a scaling result
         from paper_1809_05805_b200.parallel import run_threads
         out = run_threads(args.emulate_ranks,
-                          lambda c: _bench_core(args, c, args.emulate_ranks, c.rank, local))
+                          lambda c: _bench_core(args, c, args.emulate_ranks, c.rank, local,
+                                                "peer-threads"),
+                          peer=True)
         print(json.dumps(dict(out[0], emulated_ranks_on_one_gpu=args.emulate_ranks)), flush=True)
         return
-    comm = None
+    comm, kind = None, None
     if world > 1:
-        from paper_1809_05805_b200.parallel import Comm
-        comm = Comm.init()
-    result = _bench_core(args, comm, world, rank, local)
+        comm, kind = _make_comm(args, rank)
+    result = _bench_core(args, comm, world, rank, local, kind)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if comm is not None:
-        comm.close()
+        if kind == "peer-ipc":
+            comm.close()
+            comm.host.close()
+        else:
+            comm.close()
 
 
-def _bench_core(args, comm, world, rank, local):
+def _bench_core(args, comm, world, rank, local, comm_kind=None):
     import numpy as np
     import torch
 
@@ -226,12 +314,12 @@ def _bench_core(args, comm, world, rank, local):
     from paper_1809_05805_b200.engine import Engine
 
     slab = args.slab
-    nx, ny, nz = _dims(world, slab)
+    nx, ny, nz = (512, 512, 512) if args.strong else _dims(world, slab)
     if comm is not None:
         from paper_1809_05805_b200.parallel import slab_problem
         A_local, n_global = slab_problem((nx, ny, nz), comm)
     else:
-        A_local = P.gen_laplace3d(slab)
+        A_local = P.gen_laplace3d(nx)
         n_global = A_local.n_rows
     n = A_local.n_rows
     if comm is None:
@@ -290,7 +378,9 @@ def _bench_core(args, comm, world, rank, local):
     if comm is not None:
         ms = comm.max_scalar(ms)
     iters = M * args.steps
-    value = iters / (ms / 1e3) * world     # weak scaling: N slabs per global iteration
+    global_rate = iters / (ms / 1e3)       # Arnoldi iterations/s of the (global) solve
+    # weak scaling: one global iteration = N slab iterations (16.7M rows each)
+    value = global_rate if args.strong else global_rate * world
     # per-kernel device times: events around each launch in the timed region
     # (graph: the event nodes hold the last timed replay -- every replay runs
     # the identical 50-iteration cycle -- so one cycle's times x steps)
@@ -320,17 +410,16 @@ def _bench_core(args, comm, world, rank, local):
         pass
     ortho_t = sum(agg[k][0] for k in ortho)
     ortho_b = sum(agg[k][2] for k in ortho)
+    cfg_json = _config(world, slab, args.strong)
+    cfg_json["n_per_gpu"] = n
+    if comm is not None:
+        cfg_json["exchange"] = comm_kind
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"3D 7-point Laplacian {nx}x{ny}x{nz} (n={n_global:,}), "
-                               "one-sync MGS-CWY GMRES(50), seed-42 unit Gaussian b, x0=0",
-                   "n_per_gpu": n, "m": M, "method": "one_sync_mgs",
-                   "step": "one GMRES(50) restart cycle = 50 Arnoldi iterations",
-                   "rel_tol": 1e-14, "l2": "inputs larger than L2 (basis 7.0 GB per GPU)",
-                   "partition": "z-slabs" if world > 1 else "none",
-                   "value_units": f"global Arnoldi iterations/s x N (per-GPU slab {slab}^3)"},
+        "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg_json,
+        "global_it_per_s": global_rate,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
@@ -341,8 +430,16 @@ def _bench_core(args, comm, world, rank, local):
         "gpu_launches": eng.launches_per_cycle * args.steps,   # every liblsb200 launch timed
         "clocks": clk.summary(),
     }
+    if (nx, ny, nz) == (512, 512, 512) and world > 1:
+        # config 4 as north_star states it: the same 512^3 solve on one B200
+        # ran 104.6 it/s (profiles/r1_c4_512cube_single_gpu.txt)
+        result["c4_vs_one_gpu_512cube"] = {
+            "one_gpu_it_per_s": C4_ONE_GPU, "source": "profiles/r1_c4_512cube_single_gpu.txt",
+            "speedup": global_rate / C4_ONE_GPU,
+            "parallel_efficiency": global_rate / (world * C4_ONE_GPU)}
     del eng
-    torch.cuda.empty_cache()
+    if comm_kind != "peer-threads":   # (device-wide sync: other in-process ranks may spin)
+        torch.cuda.empty_cache()
     # e2e through the public API with host buffers: solve() on one GPU,
     # solve_distributed() per rank (each rank uploads its b rows, downloads x)
     cfg = P.GmresConfig(restart_m=M, max_restarts=1, rel_tol=1e-14, method="one_sync_mgs")
@@ -367,17 +464,19 @@ def _bench_core(args, comm, world, rank, local):
     dt = time.perf_counter() - t0
     if comm is not None:
         dt = comm.max_scalar(dt)
-    result["e2e"] = {"value": M * e2e_steps / dt * world, "unit": UNIT,
+    result["e2e"] = {"value": M * e2e_steps / dt * (1 if args.strong else world), "unit": UNIT,
                      "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                      "steps": e2e_steps,
                      "what": "solve(A, b_host) -> x_host (per rank: solve_distributed), "
                              "GmresConfig(50, 1 cycle); bytes per rank"}
-    if world == 1 and not args.no_cpu and rank == 0:
-        v, dt_cpu, thr = cpu_sample(args.cpu_iters)
+    if world == 1 and not args.no_cpu and rank == 0 and not args.strong:
+        secs, thr = cpu_windows(args.cpu_windows)
+        v = PER_WINDOW * len(secs) / sum(secs)
         result["cpu_baseline"] = {
             "value": v, "unit": UNIT, "cores": thr, "kind": "port",
-            "sample": f"first {args.cpu_iters} Arnoldi iterations of the same 256^3 one-sync "
-                      f"GMRES(50) solve, numpy oracle port ({dt_cpu:.1f} s)"}
+            "sample": f"iterations {PREFIX + 1}..{PREFIX + PER_WINDOW * len(secs)} (after "
+                      f"{PREFIX} untimed) of the same 256^3 one-sync GMRES(50) solve, numpy "
+                      f"oracle port ({sum(secs):.1f} s timed)"}
     return result
 
 
@@ -388,7 +487,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=16)
+    ap.add_argument("--cpu-windows", type=int, default=4,
+                    help="cpu_baseline: windows of 3 iterations after the 23-iteration prefix")
+    ap.add_argument("--strong", action="store_true",
+                    help="config 4 as stated: the 512^3 solve split over N GPUs (strong scaling)")
+    ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: exchange transport (peer-memory kernels, or NCCL collectives)")
     ap.add_argument("--slab", type=int, default=N_SLAB, help="per-GPU cube edge (256 = config 2)")
     ap.add_argument("--kernel-timers", default="last", choices=["last", "all"],
                     help="per-kernel CUDA events in the last timed cycle only, or in every one")
@@ -397,7 +501,19 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.emulate_ranks > 1:
+        # in-process ranks spin on each other's exchanges: one hardware queue
+        # per rank stream (read at CUDA init; see parallel.run_threads)
+        os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ \
+            and args.emulate_ranks <= 1:
+        _reexec_torchrun(args)
     if args.impl == "reference":
+        if args.strong:
+            print(json.dumps({"impl": "reference", "unavailable":
+                              "--strong (512^3) exceeds a bounded CPU sample; use the default "
+                              "weak-scaling arm"}), flush=True)
+            return
         run_reference(args)
     else:
         run_gpu(args)

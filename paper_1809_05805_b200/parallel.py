@@ -208,6 +208,10 @@ def run_threads(size, fn, *args, peer=False):
     return out
 
 
+class PeerUnavailable(RuntimeError):
+    """Peer mappings (CUDA IPC / P2P) are not available on every rank."""
+
+
 class _Reg:
     __slots__ = ("base", "span", "ld", "off", "n", "ptrs")
 
@@ -245,7 +249,7 @@ class PeerComm:
         self.ctr = torch.zeros(4, dtype=torch.int64, device=dev)
         self.counter = torch.zeros(8, dtype=torch.int32, device=dev)
         torch.cuda.synchronize()
-        mb, sg = self._share(self.mbox), self._share(self.sig)
+        mb, sg = self._share_checked(self.mbox), self._share_checked(self.sig)
         P = _abi.Peer()
         P.rank, P.size, P.slot = self.rank, self.size, self.slot
         if timeout_s is None:
@@ -261,6 +265,33 @@ class PeerComm:
         self.host.barrier()
 
     # ------------------------------------------------------------ setup
+    def _share_checked(self, t):
+        """_share with failures made collective: if any rank cannot export
+        or map, every rank raises PeerUnavailable at the same step (so a
+        caller can fall back to the NCCL communicator consistently)."""
+        err = None
+        try:
+            out = self._share(t)
+        except Exception as e:   # noqa: BLE001 -- reported below on every rank
+            out, err = None, f"rank {self.rank}: {e}"
+        errs = [e for e in self.host.exchange(err) if e]
+        if errs:
+            self._close_mappings()
+            raise PeerUnavailable("; ".join(errs))
+        return out
+
+    def selftest(self):
+        """One all-gather of the rank ids (collective); raises PeerUnavailable
+        on every rank if any rank's exchange failed or timed out."""
+        loc = torch.full((4,), float(self.rank), dtype=torch.float64, device=self.mbox.device)
+        out = torch.zeros(4 * self.size, dtype=torch.float64, device=self.mbox.device)
+        self.allgather(loc, out)
+        torch.cuda.current_stream().synchronize()
+        want = torch.arange(self.size, dtype=torch.float64).repeat_interleave(4)
+        ok = bool(torch.equal(out.cpu(), want)) and int(self.ctr[2].item()) == 0
+        if not all(self.host.exchange(ok)):
+            raise PeerUnavailable("peer all-gather self-test failed")
+
     def _share(self, t):
         """Per-rank device pointers of the peers' copies of `t` (valid here)."""
         if not self.ipc:
@@ -278,6 +309,8 @@ class PeerComm:
                 continue
             base = self._opened.get(hb)
             if base is None:
+                # a failed exchange on any rank raises on every rank (the
+                # handles were all published before anyone maps them)
                 bp = C.c_void_p()
                 _abi.check(self.lib.lsb_ipc_open(C.create_string_buffer(hb, 64), C.byref(bp)),
                            "lsb_ipc_open")
@@ -353,12 +386,15 @@ class PeerComm:
         torch.cuda.current_stream().synchronize()
         self.host.barrier()
 
-    def close(self):
-        torch.cuda.synchronize()
-        self.host.barrier()
+    def _close_mappings(self):
         for base in self._opened.values():
             self.lib.lsb_ipc_close(C.c_void_p(base))
         self._opened = {}
+
+    def close(self):
+        torch.cuda.synchronize()
+        self.host.barrier()
+        self._close_mappings()
         self._regs = []
 
 
