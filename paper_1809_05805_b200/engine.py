@@ -203,6 +203,16 @@ class Engine:
             self.pcsr = self._persist_csr(base_op)
         self.persistent = self.pcsr is not None
 
+    def reset(self, rel_tol, btf):
+        """Fresh small state for another solve on the same operator (the
+        engine cache in gmres.py): one fill of the arena, the tolerances;
+        storage, registrations and the captured cycle graph are kept."""
+        self._arena.zero_()
+        self.scal[_abi.S_RELTOL] = float(rel_tol)
+        self.scal[_abi.S_BTF] = float(btf)
+        if self._peer:
+            self.comm.flags = C.c_void_p(self.flags.data_ptr())
+
     def _persist_csr(self, base_op):
         """The operator as device CSR (bitwise the same SpMV), column-scaled
         like self.op under the Jacobi preconditioner; None if unavailable."""

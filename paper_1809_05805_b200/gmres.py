@@ -212,6 +212,33 @@ class ConvergenceHistory:
         self._stash = None
 
 
+# One engine (basis storage, small-state arena, captured cycle graph) kept
+# across solve() calls on the same operator object and configuration: a
+# service solving many right-hand sides pays the allocation and the graph
+# capture once (the e2e path).  Reused only when the previous solve's
+# history no longer holds the engine for its lazy `basis` (released,
+# collected or already materialised), so no history ever sees its basis
+# overwritten.  clear_engine_cache() drops it (frees the device memory).
+_ENGINE_CACHE = {}
+
+
+def clear_engine_cache():
+    _ENGINE_CACHE.clear()
+
+
+def _cached_engine(key, A):
+    ent = _ENGINE_CACHE.get(key)
+    if ent is None:
+        return None
+    eng, a_ref, h_ref = ent
+    if a_ref() is not A:
+        return None
+    h = h_ref() if h_ref is not None else None
+    if h is not None and h._stash is not None and h._basis is None:
+        return None
+    return eng
+
+
 class _DeviceSolve:
     """One solve: host restart shell over device cycles (gmres.py:239-516)."""
 
@@ -300,9 +327,27 @@ class _DeviceSolve:
         led = self.ledger
         hist = self.history
         inv = self.pc.inv_diag
-        eng = Engine(self.A, self.m, cfg.method, cfg.rel_tol, cfg.breakdown_tol_factor,
-                     inv_diag=inv, diagnostics=bool(self.diag_every), use_graph=self.use_graph,
-                     comm=self.comm, n_global=self.n_global, true_residual=bool(self.true_every))
+        key = (id(self.A), self.m, cfg.method, cfg.precond, bool(self.diag_every),
+               bool(self.true_every), id(self.comm), self.n_global, self.use_graph,
+               os.environ.get("LSB_PERSISTENT"))
+        # (single-rank only: reuse must be a collective decision across ranks)
+        cache = self.comm is None and os.environ.get("LSB_ENGINE_CACHE", "1") != "0"
+        eng = _cached_engine(key, self.A) if cache else None
+        if eng is not None:
+            eng.reset(cfg.rel_tol, cfg.breakdown_tol_factor)
+        else:
+            if cache:
+                _ENGINE_CACHE.clear()    # at most one engine (its basis) kept alive
+            eng = Engine(self.A, self.m, cfg.method, cfg.rel_tol, cfg.breakdown_tol_factor,
+                         inv_diag=inv, diagnostics=bool(self.diag_every),
+                         use_graph=self.use_graph, comm=self.comm, n_global=self.n_global,
+                         true_residual=bool(self.true_every))
+        if cache:
+            import weakref
+            try:
+                _ENGINE_CACHE[key] = (eng, weakref.ref(self.A), weakref.ref(self.history))
+            except TypeError:            # operator without weakref support: no reuse
+                pass
         self.engine = eng
         self._mark("engine")
         eng.load(self.b, self.x0)

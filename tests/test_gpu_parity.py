@@ -1034,3 +1034,29 @@ def test_persistent_cycle_is_used_at_launch_bound_sizes(P):
     assert eng.persistent
     assert not Engine(P.gen_laplace3d(48), 30, "one_sync_mgs", 1e-6).persistent   # n > 2^16
     assert not Engine(A, 30, "two_sync_cgs2", 1e-6).persistent
+
+
+def test_repeated_solves_reuse_the_engine(P):
+    """solve() on the same operator object and config reuses the engine
+    (storage + captured cycle graph) when the previous history no longer
+    holds it; histories are bitwise those of a fresh engine, and a history
+    still holding its lazy basis is never overwritten."""
+    from paper_1809_05805_b200 import gmres as gm
+    gm.clear_engine_cache()
+    A = P.gen_laplace2d(48)
+    b1 = orc.rhs_random(A.n_rows, 42)
+    b2 = orc.rhs_random(A.n_rows, 7)
+    cfg = P.GmresConfig(restart_m=20, max_restarts=50, rel_tol=1e-8, method="two_sync_cgs2")
+    x1, h1 = P.solve(A, b1, config=cfg, diagnostics_every=0)
+    x2, h2 = P.solve(A, b2, config=cfg, diagnostics_every=0)    # h1 alive and unread: no reuse
+    assert h1._stash[0] is not h2._stash[0]
+    basis1 = h1.basis
+    h1.release()
+    h2.release()
+    x3, h3 = P.solve(A, b1, config=cfg, diagnostics_every=0)    # reuses
+    key_eng = next(iter(gm._ENGINE_CACHE.values()))[0]
+    assert h3._stash[0] is key_eng
+    assert np.array_equal(h3.implicit_curve(), h1.implicit_curve())
+    assert h3.cycle_starts == h1.cycle_starts and np.array_equal(x3, x1)
+    assert basis1 is not None and np.array_equal(h3.basis, basis1)
+    gm.clear_engine_cache()
