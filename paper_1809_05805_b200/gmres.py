@@ -100,43 +100,73 @@ def apply_preconditioner(precond, v):
 
 
 class GivensState:
-    """Rotations, rotated triangle and rhs on the device (gmres.py:129-140)."""
+    """Rotations, rotated triangle and rhs (gmres.py:129-140).  Default:
+    numpy arrays like the reference (g, tri, the rotations list; the device
+    kernels run on staged copies and write them back); ``device="cuda"``:
+    kept on the device (rotations read back on access)."""
 
-    def __init__(self, m, beta):
-        dev = D.require_cuda()
+    def __init__(self, m, beta, device=None):
         self.m = int(m)
+        self.host = device is None
+        if self.host:
+            self.rotations = []
+            self.g = np.zeros(m + 1)
+            self.g[0] = beta
+            self.tri = np.zeros((m + 1, m))
+            return
+        dev = D.require_cuda()
         self._rot = torch.zeros(2 * max(m, 1), dtype=D.F64, device=dev)
         self.g = torch.zeros(m + 1, dtype=D.F64, device=dev)
         self.g[0] = float(beta)
         self.tri = torch.zeros((m + 1, m), dtype=D.F64, device=dev)
         self._count = 0
 
-    @property
-    def rotations(self):
-        r = self._rot[: 2 * self._count].cpu().numpy()
-        return [(float(r[2 * k]), float(r[2 * k + 1])) for k in range(self._count)]
+    def __getattr__(self, name):
+        if name == "rotations":      # device mode
+            r = self._rot[: 2 * self._count].cpu().numpy()
+            return [(float(r[2 * k]), float(r[2 * k + 1])) for k in range(self._count)]
+        raise AttributeError(name)
+
+    def _staged(self):
+        """(rot, g, tri, count) as device tensors."""
+        if not self.host:
+            return self._rot, self.g, self.tri, self._count
+        dev = D.require_cuda()
+        rot = np.zeros(2 * max(self.m, 1))
+        for k, (c, s_) in enumerate(self.rotations):
+            rot[2 * k], rot[2 * k + 1] = c, s_
+        return (torch.as_tensor(rot).to(dev), torch.as_tensor(np.array(self.g)).to(dev),
+                torch.as_tensor(np.ascontiguousarray(self.tri)).to(dev), len(self.rotations))
 
 
 def givens_update(state, h_col, i):
     """Fold Hessenberg column i (1-based, i+1 entries); returns |g[i]|
     (gmres.py:153-177) -- the same device code the solver cycle runs."""
-    if state._count != i - 1:
-        raise ValueError(f"expected {i - 1} prior rotations, have {state._count}")
+    rot, g, tri, count = state._staged()
+    if count != i - 1:
+        raise ValueError(f"expected {i - 1} prior rotations, have {count}")
     h = D.to_device_vector(h_col)
     if h.shape[0] != i + 1:
         raise ValueError(f"column {i} must have {i + 1} entries")
     res = torch.empty(1, dtype=D.F64, device=h.device)
-    _abi.call("lsb_givens_update", D.ptr(state._rot), D.ptr(state.g), D.ptr(state.tri),
-              state.m, D.ptr(h), i, D.ptr(res), D.stream())
-    state._count += 1
+    _abi.call("lsb_givens_update", D.ptr(rot), D.ptr(g), D.ptr(tri), state.m, D.ptr(h), i,
+              D.ptr(res), D.stream())
+    if state.host:
+        r = rot.cpu().numpy()
+        state.rotations.append((float(r[2 * (i - 1)]), float(r[2 * (i - 1) + 1])))
+        state.g[...] = g.cpu().numpy()
+        state.tri[...] = tri.cpu().numpy()
+    else:
+        state._count += 1
     return float(res.item())
 
 
 def solve_least_squares(state, k):
     """Back-substitution of the rotated k x k triangle (gmres.py:184-192)."""
-    y = torch.zeros(max(k, 1), dtype=D.F64, device=state.g.device)
-    st = torch.zeros(1, dtype=torch.int32, device=state.g.device)
-    _abi.call("lsb_back_substitute", D.ptr(state.tri.contiguous()), D.ptr(state.g), state.m, k,
+    _, g, tri, _ = state._staged()
+    y = torch.zeros(max(k, 1), dtype=D.F64, device=g.device)
+    st = torch.zeros(1, dtype=torch.int32, device=g.device)
+    _abi.call("lsb_back_substitute", D.ptr(tri.contiguous()), D.ptr(g), state.m, k,
               D.ptr(y), D.ptr(st), D.stream())
     bad = int(st.item())
     if bad >= 0:

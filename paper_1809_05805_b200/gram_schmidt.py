@@ -58,36 +58,76 @@ class _Scratch:
 
 
 class FactorState:
-    """R, T (compact-WY) and L (CGS2) factors on the device (gram_schmidt.py:70-93)."""
+    """R, T (compact-WY) and L (CGS2) factors (gram_schmidt.py:70-93).
 
-    def __init__(self, capacity):
-        dev = D.require_cuda()
+    Default: numpy arrays like the reference (tests read and write
+    state.R / .T / .L in place; the kernels stage them on the device and
+    write them back); ``device="cuda"``: CUDA tensors the kernels update in
+    place."""
+
+    def __init__(self, capacity, device=None):
         self.capacity = int(capacity)
-        f = dict(dtype=D.F64, device=dev)
-        self.R = torch.zeros((capacity, capacity), **f)
-        self.T = torch.zeros((capacity, capacity), **f)
-        self.L = torch.zeros((capacity, capacity), **f)
+        self.host = device is None
+        shp = (capacity, capacity)
+        if self.host:
+            self.R, self.T, self.L = np.zeros(shp), np.zeros(shp), np.zeros(shp)
+        else:
+            dev = D.require_cuda()
+            self.R, self.T, self.L = (torch.zeros(shp, dtype=D.F64, device=dev) for _ in range(3))
         self.active = 0
         self._sc = None
 
     def reset(self):
-        self.R.zero_()
-        self.T.zero_()
-        self.L.zero_()
+        for a in (self.R, self.T, self.L):
+            a[...] = 0.0
         self.active = 0
 
     def scratch(self):
         if self._sc is None:
-            self._sc = _Scratch(self.capacity, self.R.device)
+            self._sc = _Scratch(self.capacity, D.require_cuda())
         return self._sc
 
 
+def _dev_factors(state):
+    """(R, T, L) as device tensors: the state's own, or staged copies."""
+    if not state.host:
+        return state.R, state.T, state.L
+    dev = D.require_cuda()
+    return tuple(torch.as_tensor(np.ascontiguousarray(a)).to(dev) for a in (state.R, state.T,
+                                                                              state.L))
+
+
+def _write_back(state, dR, dT, dL):
+    if state.host:
+        for a, d in ((state.R, dR), (state.T, dT), (state.L, dL)):
+            a[...] = d.cpu().numpy()
+
+
 def _lagged(V, state, j, ledger, krylov_scale, btf, eligible, two):
-    p = j - 1
+    """Host-mode basis / factors (the reference's numpy storage) run on
+    staged device copies; the two columns and the factors the kernels change
+    are written back, so the mutation contract is the reference's."""
     if j > V.n_cols:
         raise ValueError(f"cannot view {j} of {V.n_cols} columns")
+    if not (V.host or state.host):
+        return _lagged_dev(V, state, j, ledger, krylov_scale, btf, eligible, two,
+                           state.R, state.T, state.L)
+    Vd = V.device_copy() if V.host else V
+    dR, dT, dL = _dev_factors(state)
+    try:
+        _lagged_dev(Vd, state, j, ledger, krylov_scale, btf, eligible, two, dR, dT, dL)
+    finally:
+        _write_back(state, dR, dT, dL)
+        if V.host:
+            p = j - 1
+            V.store[:, p - 1:p + 1] = Vd.store[p - 1:p + 1, : V.n].t().cpu().numpy()
+            V.lag = Vd.lag
+
+
+def _lagged_dev(V, state, j, ledger, krylov_scale, btf, eligible, two, Rt, Tt, Lt):
+    p = j - 1
     sc = state.scratch()
-    S = sc.struct(V.ptr(0), V.ld, V.n, state.capacity, state.R, state.T, state.L)
+    S = sc.struct(V.ptr(0), V.ld, V.n, state.capacity, Rt, Tt, Lt)
     ref = C.byref(S)
     st = D.stream()
     _reset_flags(sc.flags)
@@ -103,7 +143,7 @@ def _lagged(V, state, j, ledger, krylov_scale, btf, eligible, two):
     if int(fl[2]) == 0:  # broke_iter: HappyBreakdown before normalising u
         sv = sc.scal.cpu().numpy()
         raise HappyBreakdown(p - 1, float(sv[_abi.S_BETA]), float(sv[_abi.S_TOL]),
-                             r_col=state.R[: p - 1, p - 1].cpu().numpy().copy())
+                             r_col=Rt[: p - 1, p - 1].cpu().numpy().copy())
     if two:
         from .kernels import MDOT
         ledger.record(MDOT, p, False)
@@ -228,30 +268,31 @@ def cgs2_two_sync(Q, state, a, q_prev, ledger, breakdown_tol_factor=1.0):
     """Two-synchronisation CGS2 (gram_schmidt.py:163-192), composed from the
     device primitives (not on the GMRES path)."""
     host = D.is_host(a)
-    Q = _columns(Q)
-    p = Q.shape[1]
-    work = D.to_device_vector(a, Q.shape[0], copy=True)
+    Qd, _, _ = D.colmajor(_columns(Q))
+    n, p = Qd.shape
+    work = D.to_device_vector(a, n, copy=True)
     if p == 0:
         r_col = torch.zeros(0, dtype=D.F64, device=work.device)
     else:
-        B = mdot_pair(Q if isinstance(Q, torch.Tensor) else torch.as_tensor(Q), work,
-                      D.to_device_vector(q_prev), ledger)
+        B = mdot_pair(Qd, work, D.to_device_vector(q_prev, n), ledger)
         y, ell = B[:, 0], B[:, 1]
         if p >= 2:
-            state.L[p - 1, : p - 1] = ell[: p - 1]
+            state.L[p - 1, : p - 1] = ell[: p - 1] if not state.host else ell[: p - 1].cpu().numpy()
         Ls = state.L[:p, :p]
+        Ls = Ls if isinstance(Ls, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(Ls))
+        Ls = Ls.to(work.device)
         r_col = y - Ls @ y - Ls.T @ y
-        work = maxpy(work, Q if isinstance(Q, torch.Tensor) else torch.as_tensor(Q), -r_col)
+        work = maxpy(work, Qd, -r_col)
         state.active = p
     r_diag = norm2(work, ledger)
-    from .gram_schmidt import _check_breakdown
-    _check_breakdown(work.shape[0], r_diag, r_col.cpu().numpy(), breakdown_tol_factor, p)
+    _check_breakdown(n, r_diag, r_col.cpu().numpy(), breakdown_tol_factor, p)
     return D.out_like(work / r_diag, host), D.out_like(r_col, host), r_diag
 
 
 def _check_breakdown(n, r_diag, r_col, factor, column):
     """gram_schmidt.py:96-106 (host scalars; used by the composed kernels)."""
     import math
+    r_col = np.asarray(r_col.cpu() if isinstance(r_col, torch.Tensor) else r_col)
     eps = float(np.finfo(np.float64).eps)
     pre = math.hypot(r_diag, float(np.linalg.norm(r_col))) if len(r_col) else r_diag
     tol = factor * eps * math.sqrt(n) * pre
@@ -267,11 +308,16 @@ def apply_T(state, y, transpose=False, path="wy"):
     yv = D.to_device_vector(y)
     if yv.shape[0] != k:
         raise DimensionError(f"expected length {k}, got {yv.shape[0]}")
+    def blk(M):
+        M = M[:k, :k]
+        M = M if isinstance(M, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(M))
+        return M.to(yv.device)
+
     if path == "wy":
-        T = state.T[:k, :k]
+        T = blk(state.T)
         out = (T.T @ yv) if transpose else (T @ yv)
     elif path == "cgs2":
-        L = state.L[:k, :k]
+        L = blk(state.L)
         out = yv - L @ yv - L.T @ yv
     else:
         raise ValueError(f"unknown path {path!r}")
@@ -301,12 +347,11 @@ def qr_factorize(M, method="mgs", ledger=None, breakdown_tol_factor=1.0):
             kernel(basis, state, j, ledger, breakdown_tol_factor=breakdown_tol_factor)
         u = basis.column(k - 1)
         r_diag = norm2(u, ledger)
-        _check_breakdown(n, r_diag, state.R[: k - 1, k - 1].cpu().numpy(), breakdown_tol_factor,
-                         k - 1)
-        u.div_(r_diag)
+        _check_breakdown(n, r_diag, state.R[: k - 1, k - 1], breakdown_tol_factor, k - 1)
+        u /= r_diag
         state.R[k - 1, k - 1] = r_diag
         basis.lag = 0
-        return basis.view(k).cpu().numpy().copy(), state.R[:k, :k].cpu().numpy().copy()
+        return basis.view(k).copy(), state.R[:k, :k].copy()
     R = np.zeros((k, k))
     for jcol in range(k):
         a = M[:, jcol]
@@ -318,10 +363,9 @@ def qr_factorize(M, method="mgs", ledger=None, breakdown_tol_factor=1.0):
         elif method == "mgs":
             q, r_col, r_diag = mgs_level1(Qv, a, ledger, breakdown_tol_factor)
         else:
-            q_prev = basis.column(jcol - 1) if jcol else torch.zeros(n, dtype=D.F64,
-                                                                   device=basis.store.device)
+            q_prev = basis.column(jcol - 1) if jcol else np.zeros(n)
             q, r_col, r_diag = cgs2_two_sync(Qv, state, a, q_prev, ledger, breakdown_tol_factor)
-        R[:jcol, jcol] = np.asarray(r_col.cpu() if isinstance(r_col, torch.Tensor) else r_col)
+        R[:jcol, jcol] = np.asarray(r_col)
         R[jcol, jcol] = r_diag
-        basis.push(q if isinstance(q, torch.Tensor) else torch.as_tensor(q))
-    return basis.view(k).cpu().numpy().copy(), R
+        basis.push(q)
+    return basis.view(k).copy(), R

@@ -190,51 +190,87 @@ class CsrMatrix:
 
 
 class KrylovBasis:
-    """Column store on the device (kernels.py:206-253).
+    """Column store of the Krylov basis (kernels.py:206-253).
 
-    Storage is a (capacity, ld) float64 CUDA tensor, so each Krylov column is
-    contiguous exactly as in the reference's Fortran-order array; ld is
-    padded to 32 doubles (256 B) so every column is 128-bit aligned.
-    ``columns`` / ``view`` / ``column`` return aliasing CUDA views.
-    """
+    Two storage modes:
+      * default (``device=None``): the reference's own storage -- a
+        Fortran-order numpy array; ``view`` / ``column`` / ``columns`` alias
+        it (the reference tests mutate columns through them,
+        test_gram_schmidt.py:375-383).  The lagged kernels stage it into a
+        device copy, run there and write the columns they change back
+        (gram_schmidt._lagged): reference semantics at the API level.
+      * ``device="cuda"``: HBM, (capacity, ld) with column j contiguous at
+        ptr(j) = base + 8*ld*j, ld a multiple of 32 doubles; views are CUDA
+        tensors and the kernels work in place (the solver engine keeps its
+        own basis the same way)."""
 
-    def __init__(self, n, capacity, ld=None):
+    def __init__(self, n, capacity, ld=None, device=None):
         if capacity < 1:
             raise ValueError("capacity must be at least 1")
-        dev = D.require_cuda()
         self.n = int(n)
         self.capacity = int(capacity)
-        self.ld = int(ld) if ld else D.round_up(max(self.n, 2), 32)
-        self.store = torch.zeros((self.capacity, self.ld), dtype=D.F64, device=dev)
+        self.host = device is None
         self.n_cols = 0
         self.lag = 0
+        if self.host:
+            self.ld = self.n
+            self.store = np.zeros((self.n, self.capacity), order="F")
+            return
+        dev = D.require_cuda()
+        self.ld = int(ld) if ld else D.round_up(max(self.n, 2), 32)
+        self.store = torch.zeros((self.capacity, self.ld), dtype=D.F64,
+                                 device=dev if device in (True, "cuda") else device)
 
     @property
     def columns(self):
+        if self.host:
+            return self.store
         return self.store[:, : self.n].t()
 
     def ptr(self, j=0):
+        if self.host:
+            raise TypeError("host-mode KrylovBasis has no device pointer (see device_copy)")
         return self.store.data_ptr() + 8 * self.ld * j
+
+    def device_copy(self):
+        """Device-mode copy of a host-mode basis (same columns and lag)."""
+        V = KrylovBasis(self.n, self.capacity, device="cuda")
+        if self.n_cols:
+            V.store[: self.n_cols, : self.n].copy_(torch.from_numpy(
+                np.ascontiguousarray(self.store[:, : self.n_cols].T)))
+        V.n_cols, V.lag = self.n_cols, self.lag
+        return V
 
     def push(self, vec):
         if self.n_cols >= self.capacity:
             raise ValueError("basis is at capacity")
-        v = vec if isinstance(vec, torch.Tensor) else torch.as_tensor(
-            np.asarray(vec, dtype=np.float64))
-        if v.dim() != 1 or v.shape[0] != self.n:
-            raise DimensionError(f"expected length {self.n}, got {tuple(v.shape)}")
-        self.store[self.n_cols, : self.n].copy_(v)
+        if self.host:
+            v = vec.detach().cpu().numpy() if isinstance(vec, torch.Tensor) else np.asarray(
+                vec, dtype=np.float64)
+            if v.ndim != 1 or v.shape[0] != self.n:
+                raise DimensionError(f"expected length {self.n}, got {tuple(v.shape)}")
+            self.store[:, self.n_cols] = v
+        else:
+            v = vec if isinstance(vec, torch.Tensor) else torch.as_tensor(
+                np.asarray(vec, dtype=np.float64))
+            if v.dim() != 1 or v.shape[0] != self.n:
+                raise DimensionError(f"expected length {self.n}, got {tuple(v.shape)}")
+            self.store[self.n_cols, : self.n].copy_(v)
         self.n_cols += 1
         return self.n_cols - 1
 
     def view(self, p):
         if p < 0 or p > self.n_cols:
             raise ValueError(f"cannot view {p} of {self.n_cols} columns")
+        if self.host:
+            return self.store[:, :p]
         return self.store[:p, : self.n].t()
 
     def column(self, j):
         if j < 0 or j >= self.n_cols:
             raise IndexError(f"column {j} of {self.n_cols}")
+        if self.host:
+            return self.store[:, j]
         return self.store[j, : self.n]
 
     def reset(self):
@@ -242,14 +278,14 @@ class KrylovBasis:
         self.lag = 0
 
     def check_normalized(self):
+        """Columns up to n_cols - lag have unit norm within 4 eps sqrt(n)
+        (kernels.py:246-253); the norms come from the device norm kernel."""
         tol = 4.0 * EPS * np.sqrt(self.n)
         k = self.n_cols - self.lag
-        if k <= 0:
-            return True
-        norms = torch.linalg.vector_norm(self.store[:k, : self.n], dim=1).cpu().numpy()
-        for j, nrm in enumerate(norms):
-            if abs(float(nrm) - 1.0) > tol:
-                raise ValueError(f"column {j} has norm {float(nrm)!r}, outside unit tolerance")
+        for j in range(max(k, 0)):
+            nrm = float(_device_norm(D.to_device_vector(self.column(j))).item())
+            if abs(nrm - 1.0) > tol:
+                raise ValueError(f"column {j} has norm {nrm!r}, outside unit tolerance")
         return True
 
 

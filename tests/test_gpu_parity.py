@@ -261,7 +261,7 @@ def test_mdot_pair_mass_maxpy_norm_dot(P, K, tag):
 
 def test_mdot_on_device_views_large(P):
     n, p = 3 * 1024 * 1024 + 7, 51
-    V = P.KrylovBasis(n, p + 1)
+    V = P.KrylovBasis(n, p + 1, device="cuda")
     g = torch.Generator(device="cuda").manual_seed(0)
     V.store[:, :n] = torch.randn((p + 1, n), generator=g, device="cuda", dtype=torch.float64)
     V.n_cols = p + 1
@@ -324,11 +324,12 @@ def test_givens_special_rotations(P):
 
 
 # ------------------------------------------------------------------ orthogonalizers
-def test_mgs_lvl2_hand_case(P):
-    V = P.KrylovBasis(3, 2)
+@pytest.mark.parametrize("mode", [None, "cuda"], ids=["numpy", "device"])
+def test_mgs_lvl2_hand_case(P, mode):
+    V = P.KrylovBasis(3, 2, device=mode)
     V.push([0.0, 2.0, 0.0])
     V.push([1.0, 1.0, 0.0])
-    st = P.FactorState(2)
+    st = P.FactorState(2, device=mode)
     led = P.ReductionLedger()
     P.mgs_lvl2(V, st, 2, led)
     assert np.array_equal(_np(V.column(0)), [0.0, 1.0, 0.0])
@@ -338,11 +339,12 @@ def test_mgs_lvl2_hand_case(P):
     assert len(led) == 1 and led.events[0].kind == "fused_mdot_norm"
 
 
-def test_lagged_breakdown_one_call_late(P):
-    V = P.KrylovBasis(4, 3)
+@pytest.mark.parametrize("mode", [None, "cuda"], ids=["numpy", "device"])
+def test_lagged_breakdown_one_call_late(P, mode):
+    V = P.KrylovBasis(4, 3, device=mode)
     V.push([2.0, 0.0, 0.0, 0.0])
     V.push([3.0, 0.0, 0.0, 0.0])
-    st = P.FactorState(3)
+    st = P.FactorState(3, device=mode)
     led = P.ReductionLedger()
     P.mgs_lvl2(V, st, 2, led)
     V.push([0.0, 1.0, 0.0, 0.0])
@@ -350,12 +352,13 @@ def test_lagged_breakdown_one_call_late(P):
         P.mgs_lvl2(V, st, 3, led)
 
 
-def test_cgs2_lvl2_fixed_point(P):
+@pytest.mark.parametrize("mode", [None, "cuda"], ids=["numpy", "device"])
+def test_cgs2_lvl2_fixed_point(P, mode):
     Q, _ = np.linalg.qr(np.random.default_rng(11).standard_normal((12, 4)))
-    V = P.KrylovBasis(12, 4)
+    V = P.KrylovBasis(12, 4, device=mode)
     for k in range(4):
         V.push(Q[:, k])
-    st = P.FactorState(4)
+    st = P.FactorState(4, device=mode)
     before = _np(V.column(3)).copy()
     led = P.ReductionLedger()
     P.cgs2_lvl2(V, st, 4, led)
@@ -1060,3 +1063,25 @@ def test_repeated_solves_reuse_the_engine(P):
     assert h3.cycle_starts == h1.cycle_starts and np.array_equal(x3, x1)
     assert basis1 is not None and np.array_equal(h3.basis, basis1)
     gm.clear_engine_cache()
+
+
+def test_numpy_mode_views_alias_the_basis(P):
+    """The default KrylovBasis / FactorState / GivensState are the
+    reference's numpy storage: views alias it (test_gram_schmidt.py:375-383
+    mutates a column through column()), the kernels see those edits and
+    write their results back into it."""
+    V = P.KrylovBasis(4, 3)
+    assert isinstance(V.columns, np.ndarray) and V.columns.flags["F_CONTIGUOUS"]
+    V.push([0.0, 2.0, 0.0, 0.0])
+    V.push([1.0, 1.0, 0.0, 0.0])
+    u = V.column(0)
+    u *= 0.5                        # through the view: (0, 1, 0, 0)
+    st = P.FactorState(3)
+    st.T[0, 0] = 1.0
+    P.mgs_lvl2(V, st, 2, P.ReductionLedger())
+    assert isinstance(st.R, np.ndarray) and st.R[0, 0] == 1.0 and st.R[0, 1] == 1.0
+    assert np.array_equal(V.column(1), [1.0, 0.0, 0.0, 0.0])
+    gs = P.GivensState(2, beta=1.0)
+    gs.tri[:2, :2] = [[2.0, 1.0], [0.0, 3.0]]
+    gs.g[:2] = [3.0, 3.0]
+    assert np.array_equal(P.solve_least_squares(gs, 2), [1.0, 1.0])
