@@ -253,7 +253,8 @@ def _make_comm(args, rank):
     """Host communicator over NCCL, and the peer-memory exchange on top of it
     (falls back to NCCL collectives if peer mappings are unavailable)."""
     from paper_1809_05805_b200.parallel import Comm, PeerComm, PeerUnavailable
-    host = Comm.init()
+    # NCCL refuses two ranks on one device: --shared-gpu validation uses gloo
+    host = Comm.init("gloo" if args.shared_gpu else None)
     if args.comm == "nccl":
         return host, "nccl"
     try:
@@ -275,10 +276,13 @@ def run_gpu(args):
     if args.emulate_ranks <= 1 and world != args.gpus:
         sys.stderr.write(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}\n")
         sys.exit(2)
-    if torch.cuda.device_count() < (args.gpus if args.emulate_ranks <= 1 else 1):
+    need = 1 if (args.emulate_ranks > 1 or args.shared_gpu) else args.gpus
+    if torch.cuda.device_count() < need:
         sys.stderr.write(f"bench: --gpus {args.gpus} but only {torch.cuda.device_count()} "
                          "CUDA devices are visible\n")
         sys.exit(2)
+    if args.shared_gpu:
+        local = 0    # validation: every rank process on GPU 0 (gloo host comm, IPC peers)
     torch.cuda.set_device(local)
     if args.emulate_ranks > 1:
         # P ranks as threads on this one GPU (parallel.run_threads, peer
@@ -295,6 +299,8 @@ def run_gpu(args):
     if world > 1:
         comm, kind = _make_comm(args, rank)
     result = _bench_core(args, comm, world, rank, local, kind)
+    if args.shared_gpu:
+        result["shared_gpu_validation"] = "all ranks on GPU 0: NOT a scaling result"
     if rank == 0:
         print(json.dumps(result), flush=True)
     if comm is not None:
@@ -491,6 +497,9 @@ def main():
                     help="cpu_baseline: windows of 3 iterations after the 23-iteration prefix")
     ap.add_argument("--strong", action="store_true",
                     help="config 4 as stated: the 512^3 solve split over N GPUs (strong scaling)")
+    ap.add_argument("--shared-gpu", action="store_true",
+                    help="validation only: run the N rank processes on GPU 0 (gloo host comm, "
+                         "CUDA IPC peer exchange); not a scaling result")
     ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
                     help="N > 1: exchange transport (peer-memory kernels, or NCCL collectives)")
     ap.add_argument("--slab", type=int, default=N_SLAB, help="per-GPU cube edge (256 = config 2)")
