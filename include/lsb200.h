@@ -416,6 +416,12 @@ int lsb_peer_allgather(const lsb_peer* P, const double* local, int32_t count, do
  * neighbours' planes have landed here. */
 int lsb_peer_halo(const lsb_peer* P, const double* lo_src, double* lo_dst, const double* hi_src,
                   double* hi_dst, int64_t plane, lsb_flags* flags, void* stream);
+/* out[e] = sum_q parts[q*stride + e] over the nparts rank partials, in
+ * rank order (e < count): completes an all-gathered reduction, e.g. a
+ * diagnostics Gram row (diagnostics.py:47-69) on the row-partitioned
+ * solve.  Gated like the cycle kernels. */
+int lsb_sum_parts(const double* parts, int32_t nparts, int32_t stride, int32_t count,
+                  double* out, const lsb_flags* flags, int32_t it, void* stream);
 /* CUDA IPC of an arbitrary device pointer: handle (64 bytes) of the
  * allocation that contains ptr, and ptr's offset inside it. */
 int lsb_ipc_export(const void* ptr, void* handle64, int64_t* offset);

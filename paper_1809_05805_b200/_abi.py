@@ -149,6 +149,7 @@ _SIGS = {
     "lsb_ipc_open": ([_P, _P], C.c_int),
     "lsb_ipc_close": ([_P], C.c_int),
     "lsb_preload": ([], C.c_int),
+    "lsb_sum_parts": ([_P, _I32, _I32, _I32, _P, _P, _I32, _P], C.c_int),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -87,6 +87,7 @@ int launch_settle(const lsb_arnoldi&, int, int, cudaStream_t);
 int launch_trial_combine(const lsb_arnoldi&, int, const double*, const double*, double*,
                          const double*, cudaStream_t);
 int launch_back_substitute(const double*, const double*, int, int, double*, int*, cudaStream_t);
+int launch_sum_parts(const double*, int, int, int, double*, const lsb_flags*, int, cudaStream_t);
 int launch_peer_allgather(const lsb_peer*, const double*, int, double*, int, lsb_flags*,
                           cudaStream_t);
 int launch_peer_halo(const lsb_peer*, const double*, double*, const double*, double*, int64_t,
@@ -450,6 +451,12 @@ int lsb_ipc_open(const void* handle64, void** base) {
 int lsb_ipc_close(void* base) {
   if (!base) return LSB_EINVAL;
   return cuda_status(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle");
+}
+
+int lsb_sum_parts(const double* parts, int32_t nparts, int32_t stride, int32_t count,
+                  double* out, const lsb_flags* flags, int32_t it, void* stream) {
+  if (!parts || !out || nparts < 1 || stride < count) return LSB_EINVAL;
+  return launch_sum_parts(parts, nparts, stride, count, out, flags, it, S_(stream));
 }
 
 int lsb_preload(void) {

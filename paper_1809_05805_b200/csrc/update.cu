@@ -448,6 +448,28 @@ scale_div_kernel(const double* __restrict__ x, int64_t n, const double* s, doubl
     out[r] = __ddiv_rn(x[r], d);
 }
 
+// out[e] = sum over ranks q (in rank order) of parts[q*stride + e]: the
+// multi-rank completion of a reduction whose partials were all-gathered
+// (the same fixed order as the small-state kernels' sums, small_body.cuh).
+__global__ void sum_parts_kernel(const double* __restrict__ parts, int nparts, int stride,
+                                 int count, double* __restrict__ out, const lsb_flags* gate,
+                                 int it) {
+  if (gated_off(gate, it)) return;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x) {
+    double v = parts[e];
+    for (int q = 1; q < nparts; ++q) v += parts[(int64_t)q * stride + e];
+    out[e] = v;
+  }
+}
+
+int launch_sum_parts(const double* parts, int nparts, int stride, int count, double* out,
+                     const lsb_flags* gate, int it, cudaStream_t st) {
+  if (count <= 0) return LSB_OK;
+  sum_parts_kernel<<<(count + 255) / 256, 256, 0, st>>>(parts, nparts, stride, count, out, gate,
+                                                        it);
+  return check_launch("sum_parts");
+}
+
 int launch_scale_div(const double* x, int64_t n, const double* s, double* out,
                      const lsb_flags* gate, int it, int skip_if_broke, cudaStream_t st) {
   if (n <= 0) return LSB_OK;

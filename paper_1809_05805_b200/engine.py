@@ -397,13 +397,27 @@ class Engine:
                 self._call("lsb_cgs2_lvl2_small_b", S, i, p, st)
                 self._call("lsb_lagged_correct", S, i, p, st)
             if self.diagnostics:
-                self._call("lsb_gram_row", S, i, i, i + 1, D.ptr(self.gram), self.cap, st)
+                self._gram_row(i, i, i + 1, st)
             if self.true_residual and i >= 1:
                 self._trial(i, st)
         if defer:   # join: the least squares needs every fold
             main.wait_event(self._ev_settled[m])
             if m >= 2:
                 main.wait_event(self._ev_settled[m - 1])
+
+    def _gram_row(self, it, row, ncols, st):
+        """gram[row, :ncols] = Q^T q_row (diagnostics.py:47-69); on several
+        ranks the local partial rows are all-gathered and summed in rank
+        order (lsb_sum_parts), so every rank holds the same global Gram."""
+        if self.comm is None:
+            self._call("lsb_gram_row", self.Sref, it, row, ncols, D.ptr(self.gram), self.cap, st)
+            return
+        self._call("lsb_mdot", self.col_ptr(0), self.ld, self.n, ncols, self.col_ptr(row), None,
+                   D.ptr(self.Gloc), self.ws.ref(), D.ptr(self.flags), it, st)
+        self._gather(ncols)
+        self._call("lsb_sum_parts", D.ptr(self.G), self.S.g_parts, self.S.g_stride, ncols,
+                   C.c_void_p(self.gram.data_ptr() + 8 * row * self.cap), D.ptr(self.flags), it,
+                   st)
 
     def _trial(self, i, st):
         """||b - A (x + Mi V_i y_i)|| of iteration i into true_res[i]
@@ -472,7 +486,7 @@ class Engine:
     def _direct_body(self, st):
         S, m = self.Sref, self.m
         if self.diagnostics:
-            self._call("lsb_gram_row", S, 0, 0, 1, D.ptr(self.gram), self.cap, st)
+            self._gram_row(0, 0, 1, st)
         for i in range(1, m + 1):
             p = i
             self._op_col(i - 1, i, i)                        # z = A v_{i-1}, in place in V[:, i]
@@ -488,7 +502,7 @@ class Engine:
                 self._call("lsb_cgs_project", S, i, i, p, 0, st)
                 self._call("lsb_direct_normalize", S, i, i, st)
                 if self.diagnostics:
-                    self._call("lsb_gram_row", S, i, i, i + 1, D.ptr(self.gram), self.cap, st)
+                    self._gram_row(i, i, i + 1, st)
                 if self.true_residual:
                     self._trial(i, st)
                 continue
@@ -516,7 +530,7 @@ class Engine:
             self._call("lsb_direct_small", S, i, i, p, st)
             self._call("lsb_direct_normalize", S, i, i, st)
             if self.diagnostics:
-                self._call("lsb_gram_row", S, i, i, i + 1, D.ptr(self.gram), self.cap, st)
+                self._gram_row(i, i, i + 1, st)
             if self.true_residual:
                 self._trial(i, st)
 

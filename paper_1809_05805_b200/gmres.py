@@ -71,14 +71,19 @@ class GmresConfig:
 class Preconditioner:
     """Right preconditioner: identity or Jacobi (gmres.py:106-118)."""
 
-    def __init__(self, kind, A=None):
+    def __init__(self, kind, A=None, comm=None):
         if kind not in ("none", "jacobi"):
             raise ValueError("precond must be 'none' or 'jacobi'")
         self.kind = kind
         self.inv_diag = None
         if kind == "jacobi":
+            # row-partitioned: this rank's rows; the zero test is global
+            # (every rank raises together)
             d = np.asarray(A.diagonal_values(), dtype=np.float64)
-            if np.any(d == 0.0):
+            zero = bool(np.any(d == 0.0))
+            if comm is not None:
+                zero = comm.max_scalar(1.0 if zero else 0.0) > 0.0
+            if zero:
                 raise ValueError("jacobi preconditioner requires a zero-free diagonal")
             self.inv_diag = 1.0 / d
 
@@ -294,9 +299,7 @@ class _DeviceSolve:
         self.x0 = None if x0 is None else D.to_device_vector(x0, self.n)
         self.config = config
         self.ledger = ledger if ledger is not None else ReductionLedger()
-        if comm is not None and config.precond != "none":
-            raise NotImplementedError("jacobi preconditioning on the multi-rank path")
-        self.pc = Preconditioner(config.precond, A)
+        self.pc = Preconditioner(config.precond, A, comm=comm)
         self.m = min(config.restart_m, self.n_global)
         self.diag_every = diagnostics_every
         self.history = ConvergenceHistory()
@@ -628,12 +631,13 @@ def solve(A, b, x0=None, config=None, ledger=None, diagnostics_every=1, true_res
 
 def solve_distributed(op, b_local, comm, n_global, x0_local=None, config=None, ledger=None,
                       diagnostics_every=0):
-    """Row-partitioned solve (one rank per GPU): `op` is this rank's slab
-    operator (parallel.slab_problem), b_local/x0_local its rows.  Every rank
+    """Row-partitioned solve (one rank per GPU): `op` is this rank's row
+    block -- a stencil z-slab (parallel.slab_problem) or a CSR row block
+    (parallel.csr_row_block) -- and b_local/x0_local its rows.  Every rank
     runs the same host restart shell on bit-identical device reports, so
-    histories and ledgers agree across ranks; returns (x_local, history)."""
+    histories, ledgers and diagnostics agree across ranks (the Gram rows of
+    the diagnostics are all-gathered like the solver's reductions);
+    returns (x_local, history)."""
     config = config if config is not None else GmresConfig()
-    if diagnostics_every:
-        raise NotImplementedError("per-iteration diagnostics on the multi-rank path")
     return _DeviceSolve(op, b_local, x0_local, config, ledger, diagnostics_every, 0,
                         use_graph=True, comm=comm, n_global=n_global).run()

@@ -37,6 +37,42 @@ class CsrOperator:
                           col_scale.data_ptr() if col_scale is not None else None, 0, 0)
         self._dictionary()
 
+    @classmethod
+    def row_block(cls, row_ptr, col_idx, values, row0, halo):
+        """Rows [row0, row0 + n) of a global CSR matrix (row_ptr rebased to
+        0, GLOBAL column indices): x is the owned rows with `halo` ghost rows
+        on either side, the kernel indexes it by (col - row0), so ghost
+        columns land in the padding the halo exchange fills."""
+        from types import SimpleNamespace
+        n = len(row_ptr) - 1
+        A = SimpleNamespace(n_rows=n, n_cols=n, nnz=int(len(values)), row_ptr=np.asarray(row_ptr),
+                            col_idx=np.asarray(col_idx), values=np.asarray(values, np.float64))
+        op = object.__new__(cls)
+        dev = D.require_cuda()
+        op.n_rows = op.n_cols = n
+        op.row_ptr = torch.as_tensor(A.row_ptr.astype(np.int32), device=dev)
+        op.col_idx = torch.as_tensor(A.col_idx.astype(np.int32), device=dev)
+        op.values = torch.as_tensor(A.values, device=dev)
+        op.col_scale = None
+        op.halo = int(halo)
+        op.row0 = int(row0)
+        op._diag = None
+        rows = np.repeat(np.arange(n), np.diff(A.row_ptr)) + row0
+        hit = A.col_idx == rows
+        d = np.zeros(n)
+        d[rows[hit] - row0] = A.values[hit]
+        op._diag = d
+        op.c = _abi.Csr(n, n, A.nnz, op.row_ptr.data_ptr(), op.col_idx.data_ptr(),
+                        op.values.data_ptr(), None, int(row0), int(row0))
+        op._dictionary()
+        return op
+
+    def diagonal_values(self):
+        d = getattr(self, "_diag", None)
+        if d is None:
+            raise AttributeError("diagonal_values of a device-only CSR operator")
+        return d
+
     # nnz from which the dictionary form pays for its one-time build
     DICT_MIN_NNZ = 1 << 20
 
@@ -63,6 +99,7 @@ class CsrOperator:
             return
         counts = self.row_ptr[1:].to(torch.int64) - self.row_ptr[:-1].to(torch.int64)
         rows = torch.repeat_interleave(torch.arange(self.n_rows, device=bits.device), counts)
+        rows += int(self.c.row0)          # row-block partition: offsets from global rows
         ot, oi = torch.unique(self.col_idx.to(torch.int64) - rows, return_inverse=True)
         del rows
         if ot.numel() > 256 or ot.abs().max() >= 2 ** 31:
@@ -106,7 +143,7 @@ class CsrOperator:
         op.col_scale = col_scale
         op.c = _abi.Csr(self.c.n_rows, self.c.n_cols, self.c.nnz, self.c.row_ptr, self.c.col_idx,
                         self.c.values, col_scale.data_ptr() if col_scale is not None else None,
-                        0, 0)
+                        self.c.row0, self.c.x_lo)
         if self.cd is not None:
             op.cd = self._dict_struct(col_scale)
         return op
@@ -310,6 +347,11 @@ class StencilOperator:
         c.col_scale = col_scale.data_ptr() if col_scale is not None else None
         self.c = c
         self.h2d_bytes = 0
+
+    def diagonal_values(self):
+        """This slab's rows of the diagonal (the centre coefficient)."""
+        c = [v for (o, v) in self.stencil.offsets if o == (0, 0, 0)]
+        return np.full(self.n_rows, c[0] if c else 0.0)
 
     def with_scale(self, col_scale):
         op = object.__new__(StencilOperator)

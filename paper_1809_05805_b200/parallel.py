@@ -424,3 +424,31 @@ def local_rhs(dims, comm, seed):
     z0, nzl = slab_bounds(nz, comm.size, comm.rank)
     plane = nx * ny
     return np.ascontiguousarray(b[z0 * plane:(z0 + nzl) * plane])
+
+
+def csr_row_block(A, comm):
+    """This rank's contiguous row block of a global CSR matrix (SURVEY
+    §8(e): CSR SpMV partitions by rows) -> (operator,
+    n_global, row0).  Ghost columns are the `halo` rows just below and above
+    the block -- halo = the farthest any rank's columns reach outside its own
+    block, agreed by all ranks -- which the engine's halo exchange copies
+    from the neighbouring blocks (banded matrices: stencils in CSR form,
+    their 27-point convection-diffusion of config 5).  Raises ValueError on
+    every rank if the band reaches past a neighbouring block."""
+    from .operators import CsrOperator
+    n = int(A.n_rows)
+    r0, nl = slab_bounds(n, comm.size, comm.rank)
+    rp = np.asarray(A.row_ptr, dtype=np.int64)
+    lo, hi = int(rp[r0]), int(rp[r0 + nl])
+    cols = np.asarray(A.col_idx[lo:hi], dtype=np.int64)
+    reach = 0
+    if cols.size:
+        reach = max(0, r0 - int(cols.min()), int(cols.max()) - (r0 + nl - 1))
+    halo = int(comm.max_scalar(float(reach)))
+    smallest = -comm.max_scalar(-float(nl))
+    if comm.size > 1 and halo > smallest:
+        raise ValueError(f"matrix band ({halo} rows) reaches past a neighbouring row block "
+                         f"({int(smallest)} rows): use fewer ranks")
+    op = CsrOperator.row_block(rp[r0:r0 + nl + 1] - lo, cols, np.asarray(A.values[lo:hi]), r0,
+                               halo if comm.size > 1 else 0)
+    return op, n, r0
