@@ -164,6 +164,7 @@ typedef struct lsb_arnoldi {
 #define LSB_TUNE_FUSED_PIPE 9     /* fused K1+SpMV pipelined stencil: 0 auto (2-4 items/warp), 1 up to 8, 2 off */
 #define LSB_TUNE_CSR_DICT 10      /* dictionary-coded CSR: 0 thread per row, 1 warp-staged index bytes */
 #define LSB_TUNE_PDL 11           /* programmatic dependent launch of the per-iteration chains (one-sync K1/K5/K2, two-sync K5a/K3/K5b/K4 while p <= 32, lsb_mdot): 0 auto (n < 2^23), 1 on, 2 off */
+#define LSB_TUNE_PERSIST_TIMEOUT_S 12  /* persistent cycle: a cluster handoff waits at most this many seconds (0: 30, < 0: unbounded), then marks the mapped report -1.0 and aborts */
 #define LSB_TUNE_COUNT 16
 /* Set / read a kernel-variant knob (performance only; results unchanged up
  * to the reduction tree of the affected kernel). Returns the old value. */

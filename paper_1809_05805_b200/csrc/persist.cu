@@ -87,11 +87,30 @@ __device__ __forceinline__ void st_async_v2(uint32_t dst, double a, double b, ui
       "d"(a), "d"(b), "r"(bar)
       : "memory");
 }
-// Consumer side of a handoff.  A handoff that never completes is a bug;
-// trap (a loud launch failure) after ~1 s instead of hanging the device.
-__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, unsigned parity) {
+// Consumer side of a handoff.  A handoff that never completes is a protocol
+// bug (every byte pushed is counted on the consumer's barrier).  The wait is
+// bounded in WALL time -- LSB_TUNE_PERSIST_TIMEOUT_S seconds (0: 30 s; < 0:
+// unbounded), read through the launch -- so slowness (compute-sanitizer,
+// time slicing, a debugger stepping) cannot trip it: a handoff takes ~1 us.
+// On expiry the kernel writes -1.0 into the report marker of the mapped log
+// (the host's poll raises a clear error from it) and aborts the grid.  It
+// cannot return cooperatively: the other CTAs sit at hardware cluster
+// barriers, which have no timeout, and a CTA that skipped its part would
+// leave them waiting forever.
+struct PersistAbort {
+  double* marker;       // the current report's marker slot (mapped log), or null
+  long long limit_ns;   // <= 0: unbounded
+};
+__device__ __forceinline__ unsigned long long persist_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, unsigned parity,
+                                                      const PersistAbort& ab) {
   unsigned done = 0;
-  long long spins = 0;
+  unsigned spins = 0;
+  unsigned long long t0 = 0;
   while (!done) {
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
@@ -99,7 +118,15 @@ __device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, unsigned pa
         : "=r"(done)
         : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity)
         : "memory");
-    if (++spins > (1LL << 24)) __trap();
+    if (done || ab.limit_ns <= 0) continue;
+    if (++spins == 1024u) t0 = persist_ns();
+    if (spins > 1024u && (spins & 1023u) == 0u && (long long)(persist_ns() - t0) > ab.limit_ns) {
+      if (ab.marker) {
+        *reinterpret_cast<volatile double*>(ab.marker) = -1.0;
+        __threadfence_system();
+      }
+      __trap();
+    }
   }
 }
 
@@ -284,6 +311,7 @@ struct PersistSolve {
   const double* b;    // local rows of b
   double* log;        // max_cycles reports of kLogStride(m) doubles
   int max_cycles;
+  long long timeout_ns;   // handoff wait limit (PersistAbort)
 };
 __host__ __device__ inline int log_stride(int m) { return 4 + (m + 1) + LSB_S_COUNT + 1; }
 
@@ -393,7 +421,9 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
   unsigned ph1 = 0, ph2 = 0;   // completed phases of mb1 / mb2 (parity of the next wait)
   cluster_barrier();
 
+  PersistAbort ab{nullptr, PS.timeout_ns};
   for (int cyc = 0; cyc < (multi ? PS.max_cycles : 1); ++cyc) {
+  if (multi) ab.marker = PS.log + (int64_t)cyc * log_stride(m) + 4 + (m + 1) + LSB_S_COUNT;
   produced = 1;
   for (int i = 0; i <= m; ++i) {
     const int p = i + 1;
@@ -451,7 +481,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
       // (1) every row CTA's partials have landed (always waited: no st.async
       // may still be in flight into this CTA when the cycle ends)
       if (tid == 0) mbar_arrive_tx(&mb1, (unsigned)(16 * p * (csize - 1)));
-      mbar_wait_acq_cluster(&mb1, ph1++ & 1u);
+      mbar_wait_acq_cluster(&mb1, ph1++ & 1u, ab);
       if (!s_stop) {
         for (int e = tid; e < 2 * p; e += kPT) {
           double acc = 0.0;
@@ -494,7 +524,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
     if (tc0) { const long long t = clock64(); tr[11] += t - c0a; c0a = t; }
     const double* pub0 = s_pub;
     if (crank != 0) {
-      mbar_wait_acq_cluster(&mb2, ph2++ & 1u);
+      mbar_wait_acq_cluster(&mb2, ph2++ & 1u, ab);
       pub0 = s_pubr;
     }
     if (tw) { const long long t = clock64(); tr[2] += t - tc; tc = t; }
@@ -581,7 +611,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
         st_async_v2(mapa_u32(s_ctl, c), (double)kk, (double)stt, bar);
     }
   } else {
-    mbar_wait_acq_cluster(&mb2, ph2++ & 1u);
+    mbar_wait_acq_cluster(&mb2, ph2++ & 1u, ab);
     // (E3) x += M^-1 V_k y on the own rows (extract_kernel's expression)
     const int kk = (int)s_ctl[0], stt = (int)s_ctl[1];
     if (kk >= 1 && stt != LSB_SINGULAR)
@@ -630,7 +660,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
   // exact power-of-two rescale pass when max|r| leaves [2^-450, 2^450]
   __shared__ double s_nrm[3];   // rnorm, rescale flag, scale
   if (crank == 0) {
-    mbar_wait_acq_cluster(&mb1, ph1++ & 1u);
+    mbar_wait_acq_cluster(&mb1, ph1++ & 1u, ab);
     if (tid == 0) {
       double amax = allp[1 * 2 * cap], ssq = allp[1 * 2 * cap + 1];
       int nf = allp[1 * 2 * cap + 2] != 0.0;
@@ -663,7 +693,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
     for (int c = 1 + tid; c < csize; c += kPT)
       st_async_v2(mapa_u32(s_ctl + 2, c), s_nrm[1], s_nrm[2], mapa_u32(&mb2, c));
     if (s_nrm[1] != 0.0) {
-      mbar_wait_acq_cluster(&mb1, ph1++ & 1u);
+      mbar_wait_acq_cluster(&mb1, ph1++ & 1u, ab);
       if (tid == 0) {
         double q = allp[1 * 2 * cap];
         for (int c = 2; c < csize; ++c) q += allp[c * 2 * cap];
@@ -705,7 +735,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
       }
     }
   } else {
-    mbar_wait_acq_cluster(&mb2, ph2++ & 1u);         // rescale decision
+    mbar_wait_acq_cluster(&mb2, ph2++ & 1u, ab);         // rescale decision
     if (tid == 0) mbar_arrive_tx(&mb2, 16u);          // next: continue + rnorm
     __syncthreads();
     if (s_ctl[2] != 0.0) {                             // rescaled sum of squares
@@ -729,7 +759,7 @@ persist_cycle_kernel(lsb_arnoldi S, lsb_csr A, int rows, FastDiv rdiv, int ks, i
         st_async_v2(allp0, a, 0.0, mb1_0);
       }
     }
-    mbar_wait_acq_cluster(&mb2, ph2++ & 1u);         // continue + rnorm
+    mbar_wait_acq_cluster(&mb2, ph2++ & 1u, ab);         // continue + rnorm
   }
   __syncthreads();
   const bool cont = (crank == 0 ? s_nrm[1] : s_ctl[0]) != 0.0;
@@ -867,10 +897,12 @@ int launch_cycle_persistent(const lsb_arnoldi& S, const lsb_csr* A, int ks, cuda
   cfg.numAttrs = 1;
   const lsb_csr Av = *A;
   const bool trace = tuning(LSB_TUNE_PERSIST_TRACE) == 1;
-  const PersistSolve ps{x, b, log, x ? max_cycles : 1};
-  cudaLaunchKernelEx(&cfg, persist_cycle_kernel, S, Av, rows, FastDiv::make((uint32_t)rows), ks,
-                     stage, trace, ps);
-  return check_launch("cycle_persistent");
+  const int tmo = tuning(LSB_TUNE_PERSIST_TIMEOUT_S);
+  const long long limit = tmo < 0 ? 0LL : (long long)(tmo ? tmo : 30) * 1000000000LL;
+  const PersistSolve ps{x, b, log, x ? max_cycles : 1, limit};
+  const cudaError_t le = cudaLaunchKernelEx(&cfg, persist_cycle_kernel, S, Av, rows,
+                                            FastDiv::make((uint32_t)rows), ks, stage, trace, ps);
+  return check_launch("cycle_persistent", le);
 }
 
 // lsb_preload: one kernel of this translation unit (its module)

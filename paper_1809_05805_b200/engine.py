@@ -605,6 +605,9 @@ class Engine:
                 spins += 1
                 if spins % 256 == 0 and done.query() and host[mark] == 0.0:
                     raise RuntimeError("lsb_solve_persistent ended without report %d" % c)
+            if host[mark] < 0.0:
+                raise _abi.LsbError("persistent cycle: a cluster handoff exceeded its wait limit "
+                                    "(LSB_TUNE_PERSIST_TIMEOUT_S); the kernel aborted")
             rec = host[c * stride:(c + 1) * stride].copy()
             self.cycles_run += 1
             yield CycleReport(rec[:4].view(np.int32).tolist(), rec[4:5 + self.m],
