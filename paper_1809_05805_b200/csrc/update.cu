@@ -180,6 +180,7 @@ __device__ __forceinline__ double sum_parts(const lsb_arnoldi& S, int e) {
 
 __global__ void __launch_bounds__(kThreads)
 mgs1_pass_kernel(lsb_arnoldi S, int it, int col, int k, int p) {
+  pdl_enter();
   if (gated_off(S.flags, it)) return;
   const int64_t ld = S.ld, n = S.n;
   double* __restrict__ z = S.V + (int64_t)col * ld;
@@ -241,8 +242,13 @@ mgs1_pass_kernel(lsb_arnoldi S, int it, int col, int k, int p) {
 
 int launch_mgs1_pass(const lsb_arnoldi& S, int it, int col, int k, int p, cudaStream_t st) {
   static const int occ_ = wave(mgs1_pass_kernel, 0);
-  mgs1_pass_kernel<<<row_grid(S.n / 2 + 1, occ_), kThreads, 0, st>>>(S, it, col, k, p);
-  return check_launch("mgs1_pass");
+  // consecutive passes chain through programmatic dependent launch at every
+  // n: pass k+1's CTAs become resident during pass k's reduction tail
+  // (LSB_TUNE_PDL = 2 turns it off)
+  const cudaError_t le = launch_chain(tuning(LSB_TUNE_PDL) != 2, mgs1_pass_kernel,
+                                      dim3((unsigned)row_grid(S.n / 2 + 1, occ_)), dim3(kThreads),
+                                      0, st, S, it, col, k, p);
+  return check_launch("mgs1_pass", le);
 }
 
 // z <- z - Q coef2 (cgs_iterated pass, gram_schmidt.py:136-138), optional
@@ -448,6 +454,25 @@ scale_div_kernel(const double* __restrict__ x, int64_t n, const double* s, doubl
     out[r] = __ddiv_rn(x[r], d);
 }
 
+// 16-byte aligned x/out: row pairs, two pairs per thread per step (four
+// 128-bit loads in flight; the scalar loop ran at ~0.69 of HBM)
+__global__ void __launch_bounds__(kThreads)
+scale_div2_kernel(const double* __restrict__ x, int64_t n, const double* s, double* out,
+                  const lsb_flags* gate, int it, int skip_if_broke) {
+  if (gated_off(gate, it)) return;
+  if (skip_if_broke && gate && gate->broke_iter == it) return;
+  const double d = *s;
+  const int64_t npair = n / 2, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair; j += 2 * stride) {
+    const int64_t j2 = j + stride;
+    const double2 a = ld2(x + 2 * j);
+    const double2 b = j2 < npair ? ld2(x + 2 * j2) : make_double2(0.0, 0.0);
+    st2(out + 2 * j, make_double2(__ddiv_rn(a.x, d), __ddiv_rn(a.y, d)));
+    if (j2 < npair) st2(out + 2 * j2, make_double2(__ddiv_rn(b.x, d), __ddiv_rn(b.y, d)));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) out[n - 1] = __ddiv_rn(x[n - 1], d);
+}
+
 // out[e] = sum over ranks q (in rank order) of parts[q*stride + e]: the
 // multi-rank completion of a reduction whose partials were all-gathered
 // (the same fixed order as the small-state kernels' sums, small_body.cuh).
@@ -473,6 +498,12 @@ int launch_sum_parts(const double* parts, int nparts, int stride, int count, dou
 int launch_scale_div(const double* x, int64_t n, const double* s, double* out,
                      const lsb_flags* gate, int it, int skip_if_broke, cudaStream_t st) {
   if (n <= 0) return LSB_OK;
+  if ((uintptr_t)x % 16 == 0 && (uintptr_t)out % 16 == 0) {
+    static const int occ2 = wave(scale_div2_kernel, 0);
+    scale_div2_kernel<<<row_grid(n / 2 + 1, occ2), kThreads, 0, st>>>(x, n, s, out, gate, it,
+                                                                       skip_if_broke);
+    return check_launch("scale_div2");
+  }
   static const int occ_ = wave(scale_div_kernel, 2048);
   scale_div_kernel<<<row_grid(2 * n, occ_), kThreads, 0, st>>>(x, n, s, out, gate, it, skip_if_broke);
   return check_launch("scale_div");

@@ -874,6 +874,26 @@ def test_c2_256cube_one_sync_full_solve_matches_reference(P):
     assert h.iterations == 1749
 
 
+@pytest.mark.parametrize("meth", ["two_sync_cgs2", "cgs2", "mgs_l1"])
+def test_c2_256cube_other_variants_full_solve_match_reference(P, meth):
+    """Config 2's other variants (BASELINE.json: one-reduce MGS-CWY vs CGS2 vs
+    classical MGS) at full size to convergence against the reference's own
+    runs (tests/golden/laplace3d256_<method>.npz, make_golden.py c2m; 90-150
+    min each on one host core): two-sync CGS2 (gram_schmidt.py:248-280),
+    classical CGS2 (cgs_iterated, 118-141) and level-1 MGS (144-160) through
+    _cycle_lagged / _cycle_direct (gmres.py:309-466) -- identical iteration
+    count and ledger, curve within 1e-10 at every iteration."""
+    name = f"laplace3d256_{meth}.npz"
+    if not os.path.exists(os.path.join(GOLD, name)):
+        pytest.skip(f"{name} not generated yet (make_golden.py c2m {meth})")
+    G = _load(name)
+    A = P.gen_laplace3d(256)
+    b = P.gen_rhs("random", A, 42)
+    x, h, led = _solve(P, A, b, meth, 50, 100, 1e-6)
+    _check(h, led, G, meth)
+    assert h.iterations == len(G[meth + "__curve"])
+
+
 # ------------------------------------------------------------------ full-size properties
 def test_c2_scale_one_cycle_properties(P):
     """n = 16.7M (256^3), one GMRES(50) cycle: the basis stays orthonormal,
