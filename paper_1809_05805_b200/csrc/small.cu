@@ -49,11 +49,13 @@ int launch_settle(const lsb_arnoldi& S, int it, int gc, cudaStream_t st) {
 
 // ------------------------------------------------------------------ cgs2_lvl2
 __global__ void __launch_bounds__(kSmall)
-cgs2_small_a_kernel(lsb_arnoldi S, int it, int p, int ks, int gc) {
+cgs2_small_a_kernel(lsb_arnoldi S, int it, int p, int ks, int gc, bool use_smem) {
   pdl_enter();
   if (gated_off(S.flags, it)) return;
   __shared__ SmallShared sh;
+  extern __shared__ double sL[];   // L[:p-1, :p-1] (row stride p) when use_smem
   const int t = threadIdx.x, cap = S.cap;
+  if (use_smem) stage_block(sL, p, S.L, cap, p - 1, p - 1);   // in flight during the front
   const bool broke = lagged_front(S, sh, it, p, gc);
   if (broke) {
     if (gc > 0) settle_block(S, sh, it, gc, true);
@@ -61,15 +63,23 @@ cgs2_small_a_kernel(lsb_arnoldi S, int it, int p, int ks, int gc) {
   }
   const double beta = sh.beta;
   // L[p-1, :p-1] = G[:p-1, 0] / beta  (gram_schmidt.py:266-267)
-  for (int e = t; e < p - 1; e += blockDim.x)
-    S.L[(int64_t)(p - 1) * cap + e] = __ddiv_rn(sh.a[e], beta);
+  for (int e = t; e < p - 1; e += blockDim.x) {
+    const double v = __ddiv_rn(sh.a[e], beta);
+    S.L[(int64_t)(p - 1) * cap + e] = v;
+    if (use_smem) sL[(p - 1) * p + e] = v;
+  }
   if (t == 0) sh.y[p - 1] = __ddiv_rn(sh.y[p - 1], beta);
   __syncthreads();
   // r = y - Ls y - Ls^T y  (/beta)   (gram_schmidt.py:270-274)
   for (int j = t; j < p; j += blockDim.x) {
     double a = 0.0, b = 0.0;
-    for (int l = 0; l < j; ++l) a = fma(S.L[(int64_t)j * cap + l], sh.y[l], a);
-    for (int l = j + 1; l < p; ++l) b = fma(S.L[(int64_t)l * cap + j], sh.y[l], b);
+    if (use_smem) {
+      for (int l = 0; l < j; ++l) a = fma(sL[j * p + l], sh.y[l], a);
+      for (int l = j + 1; l < p; ++l) b = fma(sL[l * p + j], sh.y[l], b);
+    } else {
+      for (int l = 0; l < j; ++l) a = fma(S.L[(int64_t)j * cap + l], sh.y[l], a);
+      for (int l = j + 1; l < p; ++l) b = fma(S.L[(int64_t)l * cap + j], sh.y[l], b);
+    }
     double r = (sh.y[j] - a) - b;
     if (ks) r = __ddiv_rn(r, beta);
     S.coef[j] = r;
@@ -287,7 +297,17 @@ int launch_mgs_lvl2_small(const lsb_arnoldi& S, int it, int p, int ks, int gc, c
 }
 int launch_cgs2_small_a(const lsb_arnoldi& S, int it, int p, int ks, int gc, cudaStream_t st) {
   if (p < 1 || S.cap > kSmall || p >= S.cap) return LSB_ERANGE;
-  const cudaError_t le = launch_chain(use_pdl(S.n) && p <= 32, cgs2_small_a_kernel, dim3(1), dim3(kSmall), 0, st, S, it, p, ks, gc);
+  constexpr size_t kMaxL = 160 * 1024;   // L block staged in smem up to p = 143
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(cgs2_small_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kMaxL);
+    attr = true;
+  }
+  const size_t need = sizeof(double) * (size_t)p * p;
+  const bool use = need <= kMaxL;
+  const cudaError_t le = launch_chain(use_pdl(S.n) && p <= 32, cgs2_small_a_kernel, dim3(1),
+                                      dim3(kSmall), use ? need : 0, st, S, it, p, ks, gc, use);
   return check_launch("cgs2_small_a", le);
 }
 int launch_cgs2_small_b(const lsb_arnoldi& S, int it, int p, cudaStream_t st) {

@@ -17,6 +17,36 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
+// Copy an r x c block of a row-major global matrix (row stride src_ld)
+// into shared memory (row stride dst_ld) with every thread keeping U loads
+// in flight: a load-then-store loop leaves each thread one L2 round trip
+// per element (ncu: the K5 kernel at p = 100 spent most of its 30 us on the
+// T block copy).  All threads call it; no trailing barrier.
+template <int U = 8>
+__device__ __forceinline__ void stage_block(double* dst, int dst_ld, const double* src,
+                                            int64_t src_ld, int r, int c) {
+  const int tot = r * c;
+  for (int base = threadIdx.x; base < tot; base += U * blockDim.x) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = base + u * blockDim.x;
+      if (e < tot) {
+        const int j = e / c, l = e - j * c;
+        v[u] = src[(int64_t)j * src_ld + l];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = base + u * blockDim.x;
+      if (e < tot) {
+        const int j = e / c, l = e - j * c;
+        dst[j * dst_ld + l] = v[u];
+      }
+    }
+  }
+}
+
 struct SmallShared {
   double a[kSmall];     // G[:,0] / scaled
   double y[kSmall];     // G[:,1] / y
@@ -114,12 +144,7 @@ __device__ inline void mgs_small_body(const lsb_arnoldi& S, SmallShared& sh, dou
   // the scalars, rotations and g that the breakdown test and the Givens
   // fold read later.
   const bool st = use_smem;
-  if (st) {
-    for (int e = t; e < (p - 1) * (p - 1); e += blockDim.x) {
-      const int j = e / (p - 1), l = e - j * (p - 1);
-      sT[j * p + l] = S.T[(int64_t)j * cap + l];
-    }
-  }
+  if (st) stage_block(sT, p, S.T, cap, p - 1, p - 1);
   if (t == 0) {
     prefetch_l1(S.scal);
     if (gc > 0) prefetch_l1(S.g + gc - 1);

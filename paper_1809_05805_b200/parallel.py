@@ -178,6 +178,18 @@ def run_threads(size, fn, *args, peer=False):
         import warnings
         warnings.warn("run_threads(peer=True) on one device wants CUDA_DEVICE_MAX_CONNECTIONS >= "
                       "2 x ranks set before CUDA initialises; exchanges may time out")
+    if peer and torch.cuda.is_available():
+        # ranks sharing the device must not hit a device-wide synchronisation
+        # while a peer's exchange kernel spins: cudaFree (the caching
+        # allocator releasing cached segments to satisfy a new allocation) is
+        # one.  Start from an empty cache so the ranks' allocations are fresh
+        # cudaMallocs, and drop a cached single-rank solver engine.
+        import gc
+        from . import gmres as _gm
+        _gm.clear_engine_cache()
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
     import threading
     grp = ThreadGroup(size)
     out = [None] * size
