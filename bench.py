@@ -459,6 +459,10 @@ def _bench_core(args, comm, world, rank, local, comm_kind=None):
         assert h.iterations == M and isinstance(x, np.ndarray)
         h.release()
 
+    # two untimed calls: the first builds the solver engine, the second
+    # captures its cycle graph (one-time costs of a (operator, config) that
+    # every later call on the same operator reuses -- gmres._ENGINE_CACHE)
+    e2e_once()
     e2e_once()
     torch.cuda.synchronize()
     if comm is not None:
@@ -474,7 +478,9 @@ def _bench_core(args, comm, world, rank, local, comm_kind=None):
                      "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                      "steps": e2e_steps,
                      "what": "solve(A, b_host) -> x_host (per rank: solve_distributed), "
-                             "GmresConfig(50, 1 cycle); bytes per rank"}
+                             "GmresConfig(50, 1 cycle); bytes per rank; after 2 untimed calls "
+                             "(engine build, cycle-graph capture: reused by every later call "
+                             "on the same operator)"}
     if world == 1 and not args.no_cpu and rank == 0 and not args.strong:
         secs, thr = cpu_windows(args.cpu_windows)
         v = PER_WINDOW * len(secs) / sum(secs)

@@ -389,7 +389,8 @@ class _DeviceSolve:
             # exchange kernel can spin on them
             self.comm.barrier()
         # the host result buffer is faulted in while the device iterates
-        self._xhost = D.HostBuffer(eng.n) if self.host and eng.n >= D._STAGE_MIN else None
+        self._xhost = D.HostBuffer(eng.n) if (self.host and eng.n >= D._STAGE_MIN
+                                              and not D._PINNED_RESULTS) else None
         led.iteration = 0
         rep = eng.prologue()
         self._mark("prologue")
