@@ -293,6 +293,15 @@ int lsb_solve_persistent(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_
 /* 1 if an n-row, cap-column cycle fits one cluster's shared memory
  * (n * cap <= ~450K doubles, cap <= 128), else 0.  No device needed. */
 int lsb_cycle_persistent_fits(int64_t n, int32_t cap);
+/* Iterations 0..m of a one-sync cycle (as lsb_cycle_persistent) in one
+ * cooperative launch over every SM, for bases too large for one cluster but
+ * small enough that the per-iteration kernels are latency-bound
+ * (lsb_cycle_grid_fits: n * cap <= 2^23 doubles): SpMV, partial dots,
+ * their fixed-order sum, K5 on CTA 0 and K2 separated by grid barriers.
+ * part: reduction scratch of part_len >= 2 * cap * (2 * SMs) doubles. */
+int lsb_cycle_grid(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_scale, double* part,
+                   int64_t part_len, void* stream);
+int lsb_cycle_grid_fits(int64_t n, int32_t cap);
 /* Diagnostics: the last traced persistent cycle's phase timestamps (6 per
  * iteration, globaltimer ns; LSB_TUNE_PERSIST_TRACE = 1 to record). */
 int lsb_persist_trace(int64_t* out, int32_t count);

@@ -87,6 +87,8 @@ int launch_settle(const lsb_arnoldi&, int, int, cudaStream_t);
 int launch_trial_combine(const lsb_arnoldi&, int, const double*, const double*, double*,
                          const double*, cudaStream_t);
 int launch_back_substitute(const double*, const double*, int, int, double*, int*, cudaStream_t);
+int launch_cycle_grid(const lsb_arnoldi&, const lsb_csr*, int, double*, int64_t, cudaStream_t);
+int grid_fits(int64_t, int);
 int launch_sum_parts(const double*, int, int, int, double*, const lsb_flags*, int, cudaStream_t);
 int launch_peer_allgather(const lsb_peer*, const double*, int, double*, int, lsb_flags*,
                           cudaStream_t);
@@ -115,6 +117,7 @@ const void* tu_anchor_peer();
 const void* tu_anchor_persist();
 const void* tu_anchor_small();
 const void* tu_anchor_update();
+const void* tu_anchor_gridcycle();
 
 template <class F>
 static F driver_fn(const char* name) {
@@ -459,6 +462,14 @@ int lsb_sum_parts(const double* parts, int32_t nparts, int32_t stride, int32_t c
   return launch_sum_parts(parts, nparts, stride, count, out, flags, it, S_(stream));
 }
 
+int lsb_cycle_grid(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_scale, double* part,
+                   int64_t part_len, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_cycle_grid(*S, A, krylov_scale, part, part_len, S_(stream));
+}
+
+int lsb_cycle_grid_fits(int64_t n, int32_t cap) { return grid_fits(n, cap); }
+
 int lsb_preload(void) {
   // Load every kernel of every module of the library now.  Under CUDA's
   // lazy loading a kernel's first launch loads it, and loading waits for
@@ -479,7 +490,7 @@ int lsb_preload(void) {
   }
   const void* anchors[] = {tu_anchor_fused(), tu_anchor_mdot(), tu_anchor_project(),
                            tu_anchor_spmv(), tu_anchor_peer(), tu_anchor_persist(),
-                           tu_anchor_small(), tu_anchor_update()};
+                           tu_anchor_small(), tu_anchor_update(), tu_anchor_gridcycle()};
   int loaded = 0;
   for (const void* a : anchors) {
     cudaFunction_t f;

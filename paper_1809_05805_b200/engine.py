@@ -202,6 +202,16 @@ class Engine:
                 and self.lib.lsb_cycle_persistent_fits(self.n, self.cap):
             self.pcsr = self._persist_csr(base_op)
         self.persistent = self.pcsr is not None
+        # above one cluster, while the basis still sits in L2: the whole
+        # cycle's iterations as one cooperative launch over every SM
+        # (lsb_cycle_grid; LSB_GRID_CYCLE=0 or LSB_PERSISTENT=0 disables)
+        self.gcsr = None
+        if not self.persistent and want is not False and method in PERSIST_METHODS \
+                and comm is None and not diagnostics and not self.true_residual \
+                and os.environ.get("LSB_GRID_CYCLE", "1") != "0" \
+                and self.lib.lsb_cycle_grid_fits(self.n, self.cap):
+            self.gcsr = self._persist_csr(base_op)
+        self.grid_cycle = self.gcsr is not None
 
     def reset(self, rel_tol, btf):
         """Fresh small state for another solve on the same operator (the
@@ -334,6 +344,9 @@ class Engine:
         self._call("lsb_cycle_begin", S, st)
         if self.persistent:       # iterations 0..m in one cluster launch
             self._call("lsb_cycle_persistent", S, C.byref(self.pcsr.c), 1, st)
+        elif self.grid_cycle:     # iterations 0..m in one cooperative grid launch
+            self._call("lsb_cycle_grid", S, C.byref(self.gcsr.c), 1, D.ptr(self.ws.partial),
+                       int(self.ws.partial.numel()), st)
         elif self.lagged:
             self._lagged_body(st)
         else:

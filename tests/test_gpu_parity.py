@@ -1129,3 +1129,47 @@ def test_c1_deviation_pinned_per_execution_mode(P, monkeypatch, mode):
     pin = {"whole_solve": 9.5e-11, "cluster_cycle": 8.0e-11, "per_iteration": 3.0e-11}
     key = {("1", "1"): "whole_solve", ("1", "0"): "cluster_cycle", ("0", "0"): "per_iteration"}[mode]
     assert dev <= pin[key], (key, dev)
+
+
+@pytest.mark.parametrize("meth", ["one_sync_mgs", "pipeline2"])
+@pytest.mark.parametrize("grid", ["1", "0"], ids=["grid_cycle", "per_iteration"])
+def test_grid_cycle_3d32_matches_reference(P, monkeypatch, meth, grid):
+    """3D 7-point 32^3 GMRES(50): too large for one cluster, latency-bound
+    for the per-iteration kernels -- the cooperative grid cycle
+    (lsb_cycle_grid) is auto-selected and must reproduce the reference's
+    golden history (count, ledger, curve <= 1e-10) like the per-iteration
+    path does."""
+    from paper_1809_05805_b200 import gmres as gm
+    monkeypatch.setenv("LSB_GRID_CYCLE", grid)
+    gm.clear_engine_cache()
+    G = _load("laplace3d32.npz")
+    A = P.gen_laplace3d(32)
+    b = P.gen_rhs("random", A, 42)
+    x, h, led = _solve(P, A, b, meth, 50, 50, 1e-6)
+    _check(h, led, G, meth)
+    assert h._stash[0].grid_cycle == (grid == "1")
+    xr = G[meth + "__x"]
+    assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+    gm.clear_engine_cache()
+
+
+def test_grid_cycle_breakdown_and_jacobi(P, monkeypatch):
+    """The grid cycle's exits: a happy breakdown inside the cycle (the Krylov
+    space of a 40-row operator with 6 distinct eigenvalues closes) and the
+    right-Jacobi column scaling -- same counts, outcomes and curves as the
+    per-iteration kernels."""
+    rng = np.random.default_rng(3)
+    ev = np.repeat([1.0, 2.0, 3.0, 5.0, 8.0, 13.0], 7)[:40]
+    Aj = P.CsrMatrix.diagonal(ev * (1.0 + 0.0 * rng.standard_normal(40)))
+    b = rng.standard_normal(40)
+    out = {}
+    for grid in ("1", "0"):
+        monkeypatch.setenv("LSB_GRID_CYCLE", grid)
+        monkeypatch.setenv("LSB_PERSISTENT", "1" if grid == "1" else "0")
+        cfg = P.GmresConfig(restart_m=20, max_restarts=5, rel_tol=1e-14, method="one_sync_mgs",
+                            precond="jacobi")
+        x, h = P.solve(Aj, b, config=cfg, diagnostics_every=0)
+        out[grid] = (h.implicit_curve(), h.outcome, h.cycle_starts, x)
+    c1, c0 = out["1"][0], out["0"][0]
+    assert len(c1) == len(c0) and out["1"][1] == out["0"][1] and out["1"][2] == out["0"][2]
+    assert np.max(np.abs(c1 - c0) / np.maximum(c0, 1e-300)) <= 1e-8
