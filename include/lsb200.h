@@ -426,6 +426,36 @@ int lsb_peer_allgather(const lsb_peer* P, const double* local, int32_t count, do
  * neighbours' planes have landed here. */
 int lsb_peer_halo(const lsb_peer* P, const double* lo_src, double* lo_dst, const double* hi_src,
                   double* hi_dst, int64_t plane, lsb_flags* flags, void* stream);
+/* Ghost exchange fused into the kernels on either side of it (one-sync
+ * fused 7-point path): the K2 that finishes column p also stores its first
+ * / last `plane` rows straight into the neighbours' ghost rows of the same
+ * column and, from its last CTA, releases the neighbours' halo signals with
+ * this rank's next halo epoch; the next fused K1+SpMV processes its interior
+ * tiles first and waits for its own signals only before the tiles that read
+ * ghost rows.  NULL neighbour pointers = no neighbour on that side. */
+typedef struct lsb_halo_push {
+  double* lo_dst;        /* rank-1's ghost rows above its block (peer-mapped) */
+  double* hi_dst;        /* rank+1's ghost rows below its block (peer-mapped) */
+  int64_t plane;         /* ghost rows per side (even)                        */
+  int64_t* sig_lo;       /* rank-1's "from above" signal word (peer-mapped)   */
+  int64_t* sig_hi;       /* rank+1's "from below" signal word (peer-mapped)   */
+  int64_t* epoch;        /* this rank's halo epoch (lsb_peer.epoch + 1)       */
+  uint32_t* counter;     /* this rank's grid counter (lsb_peer.counter)       */
+} lsb_halo_push;
+typedef struct lsb_halo_wait {
+  const int64_t* sig_lo; /* own "from below" word, NULL without a lower rank   */
+  const int64_t* sig_hi; /* own "from above" word, NULL without an upper rank  */
+  const int64_t* epoch;  /* own halo epoch                                     */
+  int64_t timeout_ns;    /* <= 0: 60 s                                         */
+  lsb_flags* flags;      /* comm_error on timeout                              */
+} lsb_halo_wait;
+/* lsb_lagged_update + the halo push of column p (see lsb_halo_push). */
+int lsb_lagged_update_push(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
+                           const lsb_halo_push* hp, void* stream);
+/* lsb_lagged_reduce_spmv7 on a slab whose ghost rows arrive by push:
+ * interior tiles first, boundary tiles after the neighbours' signals. */
+int lsb_lagged_reduce_spmv7_halo(const lsb_arnoldi* S, const lsb_stencil* A, int32_t it,
+                                 int32_t p, const lsb_halo_wait* hw, void* stream);
 /* out[e] = sum_q parts[q*stride + e] over the nparts rank partials, in
  * rank order (e < count): completes an all-gathered reduction, e.g. a
  * diagnostics Gram row (diagnostics.py:47-69) on the row-partitioned

@@ -94,6 +94,17 @@ class Peer(C.Structure):
                 ("sig", C.c_void_p * PEER_MAX), ("epoch", C.c_void_p), ("counter", C.c_void_p)]
 
 
+class HaloPush(C.Structure):
+    _fields_ = [("lo_dst", C.c_void_p), ("hi_dst", C.c_void_p), ("plane", C.c_int64),
+                ("sig_lo", C.c_void_p), ("sig_hi", C.c_void_p), ("epoch", C.c_void_p),
+                ("counter", C.c_void_p)]
+
+
+class HaloWait(C.Structure):
+    _fields_ = [("sig_lo", C.c_void_p), ("sig_hi", C.c_void_p), ("epoch", C.c_void_p),
+                ("timeout_ns", C.c_int64), ("flags", C.c_void_p)]
+
+
 _P = C.c_void_p
 _I32 = C.c_int32
 _I64 = C.c_int64
@@ -153,6 +164,8 @@ _SIGS = {
     "lsb_ipc_close": ([_P], C.c_int),
     "lsb_preload": ([], C.c_int),
     "lsb_sum_parts": ([_P, _I32, _I32, _I32, _P, _P, _I32, _P], C.c_int),
+    "lsb_lagged_update_push": ([_P, _I32, _I32, _I32, _P, _P], C.c_int),
+    "lsb_lagged_reduce_spmv7_halo": ([_P, _P, _I32, _I32, _P, _P], C.c_int),
 }
 
 EXPORTS = tuple(_SIGS)

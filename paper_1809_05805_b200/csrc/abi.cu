@@ -45,7 +45,8 @@ int launch_mdot(const double*, int64_t, int64_t, int, const double*, const doubl
                 const lsb_workspace*, const lsb_flags*, int, cudaStream_t);
 int launch_maxpy(const double*, const double*, int64_t, int64_t, int, const double*, int, double*,
                  const lsb_flags*, int, cudaStream_t);
-int launch_lagged_update(const lsb_arnoldi&, int, int, int, cudaStream_t);
+int launch_lagged_update(const lsb_arnoldi&, int, int, int, cudaStream_t,
+                         const lsb_halo_push* = nullptr);
 int launch_lagged_correct(const lsb_arnoldi&, int, int, cudaStream_t);
 int launch_lagged_update_reduce(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int k3_tile_rows(int);
@@ -80,7 +81,8 @@ int launch_cycle_begin(const lsb_arnoldi&, cudaStream_t);
 int launch_cycle_lsq(const lsb_arnoldi&, cudaStream_t);
 int launch_restart_check(const lsb_arnoldi&, int, cudaStream_t);
 int launch_givens_update(double*, double*, double*, int, const double*, int, double*, cudaStream_t);
-int launch_lagged_reduce_spmv7(const lsb_arnoldi&, const lsb_stencil*, int, int, cudaStream_t);
+int launch_lagged_reduce_spmv7(const lsb_arnoldi&, const lsb_stencil*, int, int, cudaStream_t,
+                               const lsb_halo_wait* = nullptr);
 int launch_trial_lsq(const lsb_arnoldi&, int, double*, cudaStream_t);
 int launch_ghysels_small(const lsb_arnoldi&, int, int, int, cudaStream_t);
 int launch_settle(const lsb_arnoldi&, int, int, cudaStream_t);
@@ -469,6 +471,20 @@ int lsb_cycle_grid(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_scale,
 }
 
 int lsb_cycle_grid_fits(int64_t n, int32_t cap) { return grid_fits(n, cap); }
+
+int lsb_lagged_update_push(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
+                           const lsb_halo_push* hp, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (!hp) return LSB_EINVAL;
+  return launch_lagged_update(*S, it, p, krylov_scale, S_(stream), hp);
+}
+
+int lsb_lagged_reduce_spmv7_halo(const lsb_arnoldi* S, const lsb_stencil* A, int32_t it,
+                                 int32_t p, const lsb_halo_wait* hw, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (!hw || !hw->epoch) return LSB_EINVAL;
+  return launch_lagged_reduce_spmv7(*S, A, it, p, S_(stream), hw);
+}
 
 int lsb_preload(void) {
   // Load every kernel of every module of the library now.  Under CUDA's

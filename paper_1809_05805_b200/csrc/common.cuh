@@ -308,6 +308,33 @@ __device__ inline double givens_fold(double* h, double* rot, double* g, int i) {
   return fabs(g[i]);
 }
 
+// ---------------------------------------------------------------- peer signals
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int64_t ld_acquire_sys64(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys64(int64_t* p, int64_t v) {
+  asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// spin until *sig >= e (acquire); false after timeout_ns (<= 0: 60 s)
+__device__ inline bool spin_signal(const int64_t* sig, int64_t e, int64_t timeout_ns) {
+  if (ld_acquire_sys64(sig) >= e) return true;
+  const long long lim = timeout_ns > 0 ? timeout_ns : 60000000000LL;
+  const unsigned long long t0 = gtimer_ns();
+  unsigned k = 0;
+  while (ld_acquire_sys64(sig) < e) {
+    if ((++k & 255u) == 0 && (long long)(gtimer_ns() - t0) > lim) return false;
+    __nanosleep(32);
+  }
+  return true;
+}
+
 // ---------------------------------------------------------------- launch helpers
 int sm_count();
 int check_launch(const char* what);

@@ -20,6 +20,32 @@ struct Stencil7 {
   double c0, c1, c2, c3, c4, c5, c6;
   FastDiv fx, fy;
   int64_t lo_valid, hi_valid;  // u rows that exist in memory (ghost planes included)
+  // ghost rows arriving by push (lsb_halo_wait): tiles are visited in the
+  // order t -> (t + shift) mod ntiles, so the tiles reading ghost rows come
+  // last; the staging of any tile >= wait_from waits for the signals first
+  int64_t shift, wait_from;
+  const int64_t* sig_lo;
+  const int64_t* sig_hi;
+  const int64_t* epoch;
+  int64_t timeout_ns;
+  lsb_flags* wflags;
+  __device__ __forceinline__ int64_t row0(int64_t t, int64_t ntiles) const {
+    int64_t v = t + shift;
+    if (v >= ntiles) v -= ntiles;
+    return v * kTile;
+  }
+  // leader thread, before staging tile t (t in visiting order)
+  __device__ __forceinline__ void wait_ghosts(int64_t t, bool& waited) const {
+    if (waited || t < wait_from || !(sig_lo || sig_hi)) return;
+    waited = true;
+    const int64_t e = *epoch;
+    bool ok = true;
+    if (sig_lo) ok = spin_signal(sig_lo, e, timeout_ns) && ok;
+    if (sig_hi) ok = spin_signal(sig_hi, e, timeout_ns) && ok;
+    if (!ok && wflags) wflags->comm_error = LSB_COMM_TIMEOUT;
+    // the remote stores are read by the bulk-copy (async) proxy next
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
 };
 
 // One row pair (lr, lr+1) of w = A u from the staged tile (numpy order:
@@ -97,11 +123,14 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
     mbar_fence_init();
   }
   __syncthreads();
+  const int64_t ntiles = (n + kTile - 1) / kTile;
+  bool waited = false;
   auto stage_all = [&](int b, int64_t t) {
     double* base = smem + b * stage;
-    const int64_t r0 = t * kTile;
+    const int64_t r0 = K.row0(t, ntiles);
     unsigned tx = 0;
     const bool leader = threadIdx.x == 0;
+    if (leader) K.wait_ghosts(t, waited);
     stage_bulk(base, u, r0 - H, span, K.lo_valid, K.hi_valid, &bars[b], leader, &tx);
     stage_bulk(base + span, u, r0 - K.plane, kTile, K.lo_valid, K.hi_valid, &bars[b], leader, &tx);
     stage_bulk(base + span + kTile, u, r0 + K.plane, kTile, K.lo_valid, K.hi_valid, &bars[b],
@@ -109,7 +138,6 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
     if (leader) mbar_arrive_tx(&bars[b], tx);
   };
 
-  const int64_t ntiles = (n + kTile - 1) / kTile;
   int64_t t = blockIdx.x;
   int buf = 0;
   unsigned phase = 0;
@@ -122,7 +150,7 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
     __syncthreads();
     const int64_t tn = t + gridDim.x;
     if (tn < ntiles) stage_all(buf ^ 1, tn);
-    const int64_t r0 = t * kTile;
+    const int64_t r0 = K.row0(t, ntiles);
     const double* ut = smem + buf * stage + H;   // ut[lr] = u[r0 + lr], lr in [-H, kTile+H)
     const double* zt = smem + buf * stage + span;
     const double* pt = zt + kTile;
@@ -258,18 +286,20 @@ mdot_spmv7_pipe_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int 
     mbar_fence_init();
   }
   __syncthreads();
+  const int64_t ntiles = (n + kTile - 1) / kTile;
+  bool waited = false;
   auto stage_all = [&](int b, int64_t t) {
     double* base = smem + b * stage;
-    const int64_t r0 = t * kTile;
+    const int64_t r0 = K.row0(t, ntiles);
     unsigned tx = 0;
     const bool leader = threadIdx.x == 0;
+    if (leader) K.wait_ghosts(t, waited);
     stage_bulk(base, u, r0 - H, span, K.lo_valid, K.hi_valid, &bars[b], leader, &tx);
     stage_bulk(base + span, u, r0 - K.plane, kTile, K.lo_valid, K.hi_valid, &bars[b], leader, &tx);
     stage_bulk(base + span + kTile, u, r0 + K.plane, kTile, K.lo_valid, K.hi_valid, &bars[b],
                leader, &tx);
     if (leader) mbar_arrive_tx(&bars[b], tx);
   };
-  const int64_t ntiles = (n + kTile - 1) / kTile;
   int64_t t = blockIdx.x;
   int buf = 0;
   unsigned phase = 0;
@@ -279,21 +309,22 @@ mdot_spmv7_pipe_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int 
     phase ^= 1u;
     const double* ut = smem + H;
     const double* zt = smem + span;
+    const int64_t rp0 = K.row0(t, ntiles);
     for (int j = threadIdx.x; j < kTile / 2; j += kThreads)
-      s7_tile_pair(K, ut, zt, zt + kTile, 2 * j, t * kTile + 2 * j, n, swb, wout, bad);
+      s7_tile_pair(K, ut, zt, zt + kTile, 2 * j, rp0 + 2 * j, n, swb, wout, bad);
   }
   for (; t < ntiles; t += gridDim.x) {
     __syncthreads();           // w of tile t complete; tile t-1 fully consumed
     const int64_t tn = t + gridDim.x;
     const bool nxt = tn < ntiles;
     if (nxt) stage_all(buf ^ 1, tn);
-    const int64_t r0 = t * kTile;
+    const int64_t r0 = K.row0(t, ntiles);
     const double* ut = smem + buf * stage + H;
     const double* sw = swb + buf * kTile;
     const double* utn = smem + (buf ^ 1) * stage + H;
     const double* ztn = smem + (buf ^ 1) * stage + span;
     double* swn = swb + (buf ^ 1) * kTile;
-    const int64_t rn0 = tn * kTile;
+    const int64_t rn0 = nxt ? K.row0(tn, ntiles) : 0;
     const bool full = r0 + kTile <= n;
     const int rbase = part * kRows;
     bool ready = false;
@@ -458,7 +489,7 @@ static int launch_r(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cuda
 }
 
 int launch_lagged_reduce_spmv7(const lsb_arnoldi& S, const lsb_stencil* A, int it, int p,
-                               cudaStream_t st) {
+                               cudaStream_t st, const lsb_halo_wait* hw) {
   if (!canonical7(A) || A->nx > kTile) return LSB_EINVAL;
   if ((int64_t)A->nx * A->ny * A->nz != S.n || (S.n & 1) || p < 1 || p > 128 || p + 1 > S.cap)
     return LSB_ERANGE;
@@ -472,6 +503,36 @@ int launch_lagged_reduce_spmv7(const lsb_arnoldi& S, const lsb_stencil* A, int i
   K.fy = FastDiv::make((uint32_t)A->ny);
   K.lo_valid = A->halo_lo ? -(int64_t)K.plane : 0;
   K.hi_valid = S.n + (A->halo_hi ? K.plane : 0);
+  K.shift = 0;
+  K.wait_from = INT64_MAX;
+  K.sig_lo = K.sig_hi = K.epoch = nullptr;
+  K.timeout_ns = 0;
+  K.wflags = nullptr;
+  if (hw && ((A->halo_lo && hw->sig_lo) || (A->halo_hi && hw->sig_hi))) {
+    // tiles that stage ghost rows: the z-1 tile or the row halo below row 0
+    // (r0 < plane + nx), the z+1 tile or the row halo past n - 1
+    const int64_t ntiles = (S.n + kTile - 1) / kTile;
+    const int64_t reach = (int64_t)K.plane + K.nx;
+    const int64_t nb_lo = A->halo_lo ? (reach + kTile - 1) / kTile : 0;
+    int64_t first_hi = ntiles;
+    if (A->halo_hi) {
+      first_hi = (S.n - reach - kTile) / kTile;   // conservative: one tile early
+      if (S.n - reach - kTile < 0) first_hi = 0;
+    }
+    const int64_t nb_hi = ntiles - first_hi;
+    if (nb_lo + nb_hi >= ntiles) {
+      K.shift = 0;
+      K.wait_from = 0;           // every tile touches a ghost row: wait up front
+    } else {
+      K.shift = nb_lo;           // visiting order: interior, upper boundary, lower boundary
+      K.wait_from = ntiles - nb_lo - nb_hi;
+    }
+    K.sig_lo = A->halo_lo ? hw->sig_lo : nullptr;
+    K.sig_hi = A->halo_hi ? hw->sig_hi : nullptr;
+    K.epoch = hw->epoch;
+    K.timeout_ns = hw->timeout_ns;
+    K.wflags = hw->flags;
+  }
   switch (occ3(p) ? choose_parts(p, 8) : choose_parts(p)) {
     case 8: return launch_r<8>(S, K, p, it, st);
     case 4: return launch_r<4>(S, K, p, it, st);

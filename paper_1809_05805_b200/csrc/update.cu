@@ -72,10 +72,11 @@ int launch_maxpy(const double* y, const double* X, int64_t ld, int64_t n, int p,
 // with Q's last column already the normalised u.  One pass: reads Q and w,
 // writes u and w.
 __global__ void __launch_bounds__(kThreads)
-lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks) {
+lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks, lsb_halo_push hp) {
   pdl_enter();
   if (gated_off(S.flags, it)) return;
   if (S.flags && S.flags->broke_iter == it) return;
+  const bool push = hp.lo_dst || hp.hi_dst;
   extern __shared__ double sc[];
   for (int k = threadIdx.x; k < p; k += blockDim.x) sc[k] = S.coef[k];
   __syncthreads();
@@ -103,7 +104,12 @@ lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks) {
     acc.y = fma(cu, uu.y, acc.y);
     double2 ww = ld2(w + r);
     if (ks) { ww.x = __ddiv_rn(ww.x, beta); ww.y = __ddiv_rn(ww.y, beta); }
-    st2(w + r, make_double2(ww.x - acc.x, ww.y - acc.y));
+    const double2 out = make_double2(ww.x - acc.x, ww.y - acc.y);
+    st2(w + r, out);
+    if (push) {   // boundary rows of the new column into the neighbours' ghost rows
+      if (hp.lo_dst && r < hp.plane) st2(hp.lo_dst + r, out);
+      if (hp.hi_dst && r >= n - hp.plane) st2(hp.hi_dst + (r - (n - hp.plane)), out);
+    }
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t r = n - 1;
@@ -116,13 +122,38 @@ lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks) {
     if (ks) ww = __ddiv_rn(ww, beta);
     w[r] = ww - acc;
   }
+  if (push) {
+    // every CTA's remote stores are visible system-wide before the last CTA
+    // releases the neighbours' signals with this rank's next halo epoch
+    __threadfence_system();
+    __syncthreads();
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) s_last = atomicAdd(hp.counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      __threadfence_system();
+      const int64_t e = *hp.epoch + 1;
+      if (hp.sig_lo) st_release_sys64(hp.sig_lo, e);
+      if (hp.sig_hi) st_release_sys64(hp.sig_hi, e);
+      *hp.epoch = e;
+      *hp.counter = 0u;
+    }
+  }
 }
 
-int launch_lagged_update(const lsb_arnoldi& S, int it, int p, int ks, cudaStream_t st) {
+int launch_lagged_update(const lsb_arnoldi& S, int it, int p, int ks, cudaStream_t st,
+                         const lsb_halo_push* hp) {
   if (p < 1) return LSB_OK;
+  lsb_halo_push h = {};
+  if (hp) {
+    if (!hp->epoch || !hp->counter || hp->plane < 0 || (hp->plane & 1) || hp->plane > S.n ||
+        (hp->lo_dst && !hp->sig_lo) || (hp->hi_dst && !hp->sig_hi))
+      return LSB_EINVAL;
+    h = *hp;
+  }
   static const int occ_ = wave(lagged_update_kernel, 2048);
   const cudaError_t le = launch_chain(use_pdl(S.n), lagged_update_kernel, dim3((unsigned)row_grid(S.n, occ_)), dim3(kThreads),
-               coef_smem(p), st, S, it, p, ks);
+               coef_smem(p), st, S, it, p, ks, h);
   return check_launch("lagged_update", le);
 }
 

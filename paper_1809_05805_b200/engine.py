@@ -212,6 +212,14 @@ class Engine:
                 and self.lib.lsb_cycle_grid_fits(self.n, self.cap):
             self.gcsr = self._persist_csr(base_op)
         self.grid_cycle = self.gcsr is not None
+        # multi-rank fused path: the ghost exchange rides on K2 (push) and the
+        # fused K1+SpMV (interior tiles first, wait before boundary tiles)
+        self.push_halo = bool(self._peer and self.halo and self.fused7
+                              and method in ("one_sync_mgs", "pipeline2")
+                              and not self.true_residual
+                              and os.environ.get("LSB_HALO_PUSH", "1") != "0")
+        self._keep = []
+        self._hwait = comm.halo_wait() if self.push_halo else None
 
     def reset(self, rel_tol, btf):
         """Fresh small state for another solve on the same operator (the
@@ -338,6 +346,7 @@ class Engine:
         st = D.stream()
         S = self.Sref
         self._count = 0
+        self._keep = []     # launch arguments are copied at launch / capture
         # V[:,0] = r / beta (gmres.py:396 / 313), fresh small state (392-395)
         self._call("lsb_scale_div", D.ptr(self.rbuf), self.n,
                    C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_RNORM), self.col_ptr(0), None, -1, st)
@@ -381,9 +390,15 @@ class Engine:
             if defer and i >= 3:
                 main.wait_event(self._ev_settled[i - 2])
             if self.fused7:                                  # w = A u and [Q^T u, Q^T w], one pass
-                if self.comm is not None and self.halo:
-                    self.comm.halo(self.Vstore[i], self.off, self.n, self.halo)
-                self._call("lsb_lagged_reduce_spmv7", S, C.byref(self.op.c), i, p, st)
+                if self.push_halo and i >= 1:
+                    # column i's ghost rows were pushed by K2 of iteration
+                    # i-1; interior tiles run before the wait on the signals
+                    self._call("lsb_lagged_reduce_spmv7_halo", S, C.byref(self.op.c), i, p,
+                               C.byref(self._hwait), st)
+                else:
+                    if self.comm is not None and self.halo:
+                        self.comm.halo(self.Vstore[i], self.off, self.n, self.halo)
+                    self._call("lsb_lagged_reduce_spmv7", S, C.byref(self.op.c), i, p, st)
             else:
                 self._op_col(i, i + 1, i)                    # V.push(A v_i)
                 self._call("lsb_lagged_reduce", S, i, p, st)  # one pass: [Q^T u, Q^T w]
@@ -394,10 +409,10 @@ class Engine:
                 side.wait_event(self._ev_front[i])
                 self._call("lsb_settle", S, i, i, side_ptr)
                 self._ev_settled[i].record(side)
-                self._call("lsb_lagged_update", S, i, p, 1, st)
+                self._k2(i, p, st)
             elif not two:
                 self._call("lsb_mgs_lvl2_small", S, i, p, 1, i, st)
-                self._call("lsb_lagged_update", S, i, p, 1, st)
+                self._k2(i, p, st)
             else:
                 self._call("lsb_cgs2_lvl2_small_a", S, i, p, 1, i, st)
                 if self.fuse_k3 and p + 1 <= K3_MAX_COLS:   # K2 + 2nd mdot, Q read once
@@ -431,6 +446,16 @@ class Engine:
         self._call("lsb_sum_parts", D.ptr(self.G), self.S.g_parts, self.S.g_stride, ncols,
                    C.c_void_p(self.gram.data_ptr() + 8 * row * self.cap), D.ptr(self.flags), it,
                    st)
+
+    def _k2(self, i, p, st):
+        """K2; with the fused ghost exchange it also pushes the boundary rows
+        of the column it finishes (the next SpMV's input) to the neighbours."""
+        if self.push_halo and i < self.m:
+            hp = self.comm.halo_push(self.Vstore[p], self.off, self.n, self.halo)
+            self._keep.append(hp)       # the struct outlives graph capture
+            self._call("lsb_lagged_update_push", self.Sref, i, p, 1, C.byref(hp), st)
+        else:
+            self._call("lsb_lagged_update", self.Sref, i, p, 1, st)
 
     def _trial(self, i, st):
         """||b - A (x + Mi V_i y_i)|| of iteration i into true_res[i]

@@ -382,6 +382,40 @@ class PeerComm:
             from . import _abi
             _abi.check(rc, "lsb_peer_halo")
 
+    # ---- the ghost exchange fused into K2 / the fused K1+SpMV (one-sync)
+    def halo_push(self, vec, off, n, plane):
+        """lsb_halo_push for the column/vector `vec` (registered): the K2 that
+        finishes it stores its first/last `plane` rows straight into the
+        neighbours' ghost rows and signals them."""
+        from . import _abi
+        r, j = self._find(vec.data_ptr())
+        q = self.rank
+        hp = _abi.HaloPush()
+        hp.plane = int(plane)
+        if q > 0:
+            hp.lo_dst = r.ptrs[q - 1] + 8 * (j * r.ld[q - 1] + r.off[q - 1] + r.n[q - 1])
+            hp.sig_lo = self.P.sig[q - 1] + 8 * (self.size + 1)
+        if q < self.size - 1:
+            hp.hi_dst = r.ptrs[q + 1] + 8 * (j * r.ld[q + 1] + r.off[q + 1] - plane)
+            hp.sig_hi = self.P.sig[q + 1] + 8 * self.size
+        hp.epoch = self.ctr.data_ptr() + 8
+        hp.counter = self.counter.data_ptr()
+        return hp
+
+    def halo_wait(self):
+        """lsb_halo_wait: this rank's own halo signal words and epoch."""
+        from . import _abi
+        hw = _abi.HaloWait()
+        base = self.sig.data_ptr()
+        if self.rank > 0:
+            hw.sig_lo = base + 8 * self.size
+        if self.rank < self.size - 1:
+            hw.sig_hi = base + 8 * (self.size + 1)
+        hw.epoch = self.ctr.data_ptr() + 8
+        hw.timeout_ns = self.P.timeout_ns
+        hw.flags = self.flags.value if self.flags is not None else None
+        return hw
+
     def check(self):
         """Raise if an exchange kernel timed out (a peer died or diverged)."""
         if int(self.ctr[2].item()):
