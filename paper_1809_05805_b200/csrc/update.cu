@@ -74,9 +74,19 @@ int launch_maxpy(const double* y, const double* X, int64_t ld, int64_t n, int p,
 __global__ void __launch_bounds__(kThreads)
 lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks, lsb_halo_push hp) {
   pdl_enter();
-  if (gated_off(S.flags, it)) return;
-  if (S.flags && S.flags->broke_iter == it) return;
-  const bool push = hp.lo_dst || hp.hi_dst;
+  const bool push = hp.epoch != nullptr;
+  // a gated-off or broken-down iteration does no row work; with the fused
+  // halo push it still advances this rank's halo epoch and signals the
+  // neighbours, so every rank issues the same epochs whatever moment its own
+  // flags were set (pipeline2 settles on a side stream, so the gate can
+  // close at different points of the kernel sequence on different ranks)
+  __shared__ int s_skip;   // one decision per CTA (the flags may change under a side-stream settle)
+  if (threadIdx.x == 0)
+    s_skip = gated_off(S.flags, it) || (S.flags && S.flags->broke_iter == it);
+  __syncthreads();
+  const bool skip = s_skip != 0;
+  if (skip && !push) return;
+  if (!skip) {
   extern __shared__ double sc[];
   for (int k = threadIdx.x; k < p; k += blockDim.x) sc[k] = S.coef[k];
   __syncthreads();
@@ -106,7 +116,7 @@ lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks, lsb_halo_push hp) {
     if (ks) { ww.x = __ddiv_rn(ww.x, beta); ww.y = __ddiv_rn(ww.y, beta); }
     const double2 out = make_double2(ww.x - acc.x, ww.y - acc.y);
     st2(w + r, out);
-    if (push) {   // boundary rows of the new column into the neighbours' ghost rows
+    if (hp.lo_dst || hp.hi_dst) {   // boundary rows of the new column into the neighbours' ghost rows
       if (hp.lo_dst && r < hp.plane) st2(hp.lo_dst + r, out);
       if (hp.hi_dst && r >= n - hp.plane) st2(hp.hi_dst + (r - (n - hp.plane)), out);
     }
@@ -122,6 +132,7 @@ lagged_update_kernel(lsb_arnoldi S, int it, int p, int ks, lsb_halo_push hp) {
     if (ks) ww = __ddiv_rn(ww, beta);
     w[r] = ww - acc;
   }
+  }   // !skip
   if (push) {
     // every CTA's remote stores are visible system-wide before the last CTA
     // releases the neighbours' signals with this rank's next halo epoch

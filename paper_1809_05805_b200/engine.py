@@ -214,8 +214,11 @@ class Engine:
         self.grid_cycle = self.gcsr is not None
         # multi-rank fused path: the ghost exchange rides on K2 (push) and the
         # fused K1+SpMV (interior tiles first, wait before boundary tiles)
+        # (one_sync_mgs only: with pipeline2's side-stream settle the gate of
+        # an iteration closes at a different point of the kernel sequence on
+        # each rank; the separate halo kernel, never gated, keeps it simple)
         self.push_halo = bool(self._peer and self.halo and self.fused7
-                              and method in ("one_sync_mgs", "pipeline2")
+                              and method == "one_sync_mgs"
                               and not self.true_residual
                               and os.environ.get("LSB_HALO_PUSH", "1") != "0")
         self._keep = []

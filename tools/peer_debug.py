@@ -22,7 +22,8 @@ def body(comm, N, kind, meth, m):
         x, h = P.gmres.solve_distributed(op, b, comm, ng, config=cfg)
         res = ("ok", h.iterations, h.outcome)
     except Exception as e:
-        res = ("err", repr(e))
+        import traceback
+        res = ("err", repr(e), traceback.format_exc()[-1500:])
     torch.cuda.synchronize()
     return res, comm.ctr.cpu().tolist(), comm.sig.cpu().tolist()
 
