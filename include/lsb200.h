@@ -165,6 +165,8 @@ typedef struct lsb_arnoldi {
 #define LSB_TUNE_CSR_DICT 10      /* dictionary-coded CSR: 0 thread per row, 1 warp-staged index bytes */
 #define LSB_TUNE_PDL 11           /* programmatic dependent launch of the per-iteration chains (one-sync K1/K5/K2, two-sync K5a/K3/K5b/K4 while p <= 32, lsb_mdot): 0 auto (n < 2^23), 1 on, 2 off */
 #define LSB_TUNE_PERSIST_TIMEOUT_S 12  /* persistent cycle: a cluster handoff waits at most this many seconds (0: 30, < 0: unbounded), then marks the mapped report -1.0 and aborts */
+#define LSB_TUNE_GRID_OCC 13       /* grid cycle CTAs per SM (0: 1) */
+#define LSB_TUNE_GRID_TRACE 14     /* 1: lsb_cycle_grid accumulates per-phase ns (lsb_grid_trace) */
 #define LSB_TUNE_COUNT 16
 /* Set / read a kernel-variant knob (performance only; results unchanged up
  * to the reduction tree of the affected kernel). Returns the old value. */
@@ -302,6 +304,10 @@ int lsb_cycle_persistent_fits(int64_t n, int32_t cap);
 int lsb_cycle_grid(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_scale, double* part,
                    int64_t part_len, void* stream);
 int lsb_cycle_grid_fits(int64_t n, int32_t cap);
+/* Diagnostics: ns per phase summed over traced grid-cycle iterations
+ * (SpMV, barrier, dots, barrier + sums, K5, barrier, K2, barrier); reads and
+ * clears (LSB_TUNE_GRID_TRACE = 1 to record). */
+int lsb_grid_trace(int64_t* out, int32_t count);
 /* Diagnostics: the last traced persistent cycle's phase timestamps (6 per
  * iteration, globaltimer ns; LSB_TUNE_PERSIST_TRACE = 1 to record). */
 int lsb_persist_trace(int64_t* out, int32_t count);

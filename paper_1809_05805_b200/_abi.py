@@ -147,6 +147,7 @@ _SIGS = {
     "lsb_cycle_persistent_fits": ([C.c_int64, _I32], C.c_int),
     "lsb_cycle_grid": ([_P, _P, _I32, _P, _I64, _P], C.c_int),
     "lsb_cycle_grid_fits": ([C.c_int64, _I32], C.c_int),
+    "lsb_grid_trace": ([_P, _I32], C.c_int),
     "lsb_persist_trace": ([_P, _I32], C.c_int),
     "lsb_cycle_begin": ([_P, _P], C.c_int),
     "lsb_cycle_lsq": ([_P, _P], C.c_int),

@@ -91,6 +91,7 @@ int launch_trial_combine(const lsb_arnoldi&, int, const double*, const double*, 
 int launch_back_substitute(const double*, const double*, int, int, double*, int*, cudaStream_t);
 int launch_cycle_grid(const lsb_arnoldi&, const lsb_csr*, int, double*, int64_t, cudaStream_t);
 int grid_fits(int64_t, int);
+int grid_trace(long long*, int);
 int launch_sum_parts(const double*, int, int, int, double*, const lsb_flags*, int, cudaStream_t);
 int launch_peer_allgather(const lsb_peer*, const double*, int, double*, int, lsb_flags*,
                           cudaStream_t);
@@ -471,6 +472,10 @@ int lsb_cycle_grid(const lsb_arnoldi* S, const lsb_csr* A, int32_t krylov_scale,
 }
 
 int lsb_cycle_grid_fits(int64_t n, int32_t cap) { return grid_fits(n, cap); }
+
+int lsb_grid_trace(int64_t* out, int32_t count) {
+  return out ? grid_trace(reinterpret_cast<long long*>(out), count) : LSB_EINVAL;
+}
 
 int lsb_lagged_update_push(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,
                            const lsb_halo_push* hp, void* stream) {

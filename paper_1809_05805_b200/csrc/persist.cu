@@ -186,30 +186,6 @@ struct CsrRowAccCluster {
 // the K5 code touches, copied in at launch and out at the end, so no global
 // store is outstanding at a cluster barrier (each barrier.cluster.arrive
 // .release would otherwise wait for them to reach L2).
-struct StateLayout {
-  int R, T, tri, rot, g, res, coef, G, scal, flags, total;   // offsets (doubles)
-  __host__ __device__ static StateLayout make(int cap, int m) {
-    StateLayout L{};
-    int o = 0;
-    L.R = o; o += cap * cap;
-    L.T = o; o += cap * cap;
-    L.tri = o; o += (m + 1) * m;
-    L.rot = o; o += 2 * m;
-    L.g = o; o += m + 1;
-    L.res = o; o += m + 1;
-    L.coef = o; o += cap;
-    L.G = o; o += 2 * cap;
-    L.scal = o; o += LSB_S_COUNT;
-    L.flags = o; o += (int)(sizeof(lsb_flags) / sizeof(double));
-    L.total = o;
-    return L;
-  }
-};
-
-__device__ __forceinline__ void copy_d(double* dst, const double* src, int n) {
-  for (int e = threadIdx.x; e < n; e += blockDim.x) dst[e] = src[e];
-}
-
 // K5 of the control CTA (gram_schmidt.py:226-245 with krylov_scale; the
 // Givens fold is deferred), arranged for latency: warp 0 runs the breakdown
 // test (beta, ||R[:p-1,p-1]||, CPython hypot -- gram_schmidt.py:96-106)

@@ -216,25 +216,38 @@ cycle_begin_kernel(lsb_arnoldi S) {
 
 // solve_least_squares (gmres.py:184-192) on the rotated k x k triangle:
 // row-oriented back substitution, one warp per row dot (fixed lane order).
-__global__ void __launch_bounds__(32)
-cycle_lsq_kernel(lsb_arnoldi S) {
+__global__ void __launch_bounds__(kSmall)
+cycle_lsq_kernel(lsb_arnoldi S, int staged) {
   __shared__ double sy[kSmall];
-  const int lane = threadIdx.x;
+  __shared__ double sg[kSmall];
+  extern __shared__ double stri[];          // tri[:k, :k], row stride m (staged)
+  const int t = threadIdx.x, lane = t & 31;
   const int stop = S.flags->stop_iter;
   // a cgs1_ghysels cancellation check leaves the extract to the host
   const int k = S.flags->status == LSB_GHYSELS_CHECK ? 0 : (stop == LSB_NO_STOP ? S.m : stop);
-  if (lane == 0) S.flags->k = k;
   const int m = S.m;
+  // the triangle and g into shared memory by the whole CTA, every thread with
+  // 8 loads in flight (a warp reading them row by row from L2 inside the
+  // serial solve took ~64 us per cycle); the solve itself is unchanged
+  const double* tri = S.tri;
+  if (staged) {
+    stage_block(stri, m, S.tri, m, k, k);
+    tri = stri;
+  }
+  for (int j = t; j < k; j += blockDim.x) sg[j] = S.g[j];
+  __syncthreads();
+  if (t >= 32) return;
+  if (lane == 0) S.flags->k = k;
   for (int i = k - 1; i >= 0; --i) {
-    const double d = S.tri[(int64_t)i * m + i];
+    const double d = tri[(int64_t)i * m + i];
     if (d == 0.0) {
       if (lane == 0) { S.flags->status = LSB_SINGULAR; S.flags->k = i; }
       return;
     }
     double acc = 0.0;
-    for (int j = i + 1 + lane; j < k; j += 32) acc = fma(S.tri[(int64_t)i * m + j], sy[j], acc);
+    for (int j = i + 1 + lane; j < k; j += 32) acc = fma(tri[(int64_t)i * m + j], sy[j], acc);
     acc = warp_sum(acc);
-    if (lane == 0) sy[i] = __ddiv_rn(S.g[i] - acc, d);
+    if (lane == 0) sy[i] = __ddiv_rn(sg[i] - acc, d);
     __syncwarp();
   }
   for (int j = lane; j < k; j += 32) S.coef2[j] = sy[j];
@@ -329,7 +342,16 @@ int launch_cycle_begin(const lsb_arnoldi& S, cudaStream_t st) {
   return check_launch("cycle_begin");
 }
 int launch_cycle_lsq(const lsb_arnoldi& S, cudaStream_t st) {
-  cycle_lsq_kernel<<<1, 32, 0, st>>>(S);
+  constexpr size_t kMaxTri = 160 * 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(cycle_lsq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kMaxTri);
+    attr = true;
+  }
+  const size_t need = sizeof(double) * (size_t)S.m * S.m;
+  const int staged = need <= kMaxTri;
+  cycle_lsq_kernel<<<1, kSmall, staged ? need : 0, st>>>(S, staged);
   return check_launch("cycle_lsq");
 }
 int launch_restart_check(const lsb_arnoldi& S, int first, cudaStream_t st) {

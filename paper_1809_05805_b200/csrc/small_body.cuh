@@ -47,6 +47,33 @@ __device__ __forceinline__ void stage_block(double* dst, int dst_ld, const doubl
   }
 }
 
+// The cycle's small state laid out in one CTA's shared memory (the
+// persistent cycles keep it resident there across iterations): offsets of
+// the lsb_arnoldi arrays the K5 code touches.
+struct StateLayout {
+  int R, T, tri, rot, g, res, coef, G, scal, flags, total;   // offsets (doubles)
+  __host__ __device__ static StateLayout make(int cap, int m) {
+    StateLayout L{};
+    int o = 0;
+    L.R = o; o += cap * cap;
+    L.T = o; o += cap * cap;
+    L.tri = o; o += (m + 1) * m;
+    L.rot = o; o += 2 * m;
+    L.g = o; o += m + 1;
+    L.res = o; o += m + 1;
+    L.coef = o; o += cap;
+    L.G = o; o += 2 * cap;
+    L.scal = o; o += LSB_S_COUNT;
+    L.flags = o; o += (int)(sizeof(lsb_flags) / sizeof(double));
+    L.total = o;
+    return L;
+  }
+};
+
+__device__ __forceinline__ void copy_d(double* dst, const double* src, int n) {
+  for (int e = threadIdx.x; e < n; e += blockDim.x) dst[e] = src[e];
+}
+
 struct SmallShared {
   double a[kSmall];     // G[:,0] / scaled
   double y[kSmall];     // G[:,1] / y
@@ -136,7 +163,8 @@ __device__ inline bool lagged_front(const lsb_arnoldi& S, SmallShared& sh, int i
 // CTA, every thread calls it.  sT: p*p doubles of shared memory when
 // use_smem (the T block), else unused.
 __device__ inline void mgs_small_body(const lsb_arnoldi& S, SmallShared& sh, double* sT, int it,
-                                      int p, int ks, int gc, bool use_smem) {
+                                      int p, int ks, int gc, bool use_smem,
+                                      bool resident = false) {
   const int t = threadIdx.x, cap = S.cap;
   // The kernel is a chain of dependent L2 round trips, not work (ncu: ~2K
   // warp instructions in ~20K cycles): issue every independent load up
@@ -145,11 +173,13 @@ __device__ inline void mgs_small_body(const lsb_arnoldi& S, SmallShared& sh, dou
   // fold read later.
   const bool st = use_smem;
   if (st) stage_block(sT, p, S.T, cap, p - 1, p - 1);
-  if (t == 0) {
-    prefetch_l1(S.scal);
-    if (gc > 0) prefetch_l1(S.g + gc - 1);
+  if (!resident) {   // (resident: the state is in shared memory already)
+    if (t == 0) {
+      prefetch_l1(S.scal);
+      if (gc > 0) prefetch_l1(S.g + gc - 1);
+    }
+    if (gc > 1 && 16 * t < 2 * (gc - 1)) prefetch_l1(S.rot + 16 * t);
   }
-  if (gc > 1 && 16 * t < 2 * (gc - 1)) prefetch_l1(S.rot + 16 * t);
   const bool broke = lagged_front(S, sh, it, p, gc);
   if (broke) {
     if (gc > 0) settle_block(S, sh, it, gc, true);

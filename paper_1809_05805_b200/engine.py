@@ -581,6 +581,12 @@ class Engine:
         return self.report()
 
     def cycle(self):
+        self.launch_cycle()
+        return self.report()
+
+    def launch_cycle(self):
+        """Enqueue one restart cycle (graph replay from the second on) without
+        waiting for it; report() collects it."""
         if self.use_graph and self.cycles_run >= 1:
             if self.graph is None:
                 self.graph = torch.cuda.CUDAGraph()
@@ -605,7 +611,6 @@ class Engine:
         else:
             self.enqueue_cycle()
         self.cycles_run += 1
-        return self.report()
 
     def report(self):
         self.h_flags.copy_(self.flags, non_blocking=True)

@@ -415,10 +415,24 @@ class _DeviceSolve:
         whole = eng.persistent and cfg.max_restarts >= 1 \
             and os.environ.get("LSB_PERSISTENT_SOLVE", "1") != "0"
         device_reports = eng.solve_cycles(cfg.max_restarts) if whole else None
+        # the next cycle is launched as soon as a report says the restart
+        # shell will continue -- before this cycle's ledger/history
+        # bookkeeping, which then overlaps the device (not for Ghysels, whose
+        # arbitration is host-driven, nor with diagnostics, read from the
+        # device state the next cycle overwrites)
+        ahead = cfg.method != "cgs1_ghysels" and not self.diag_every
+        pending = False
         for _cycle in range(cfg.max_restarts):
             hist.cycle_starts.append(self.global_it)
             if device_reports is None:
-                rep = eng.cycle()
+                rep = eng.report() if pending else eng.cycle()
+                pending = False
+                if ahead and _cycle + 1 < cfg.max_restarts and not rep.nonfinite \
+                        and not rep.comm_error and rep.status == _abi.RUNNING \
+                        and rep.stop_iter == _abi.NO_STOP \
+                        and not float(rep.scal[_abi.S_RNORM]) <= target:
+                    eng.launch_cycle()
+                    pending = True
             else:
                 rep = next(device_reports, None)
                 if rep is None:
