@@ -199,6 +199,100 @@ stencil27_pair_kernel(const StencilK K, FastDiv fint, const double* __restrict__
   if (bad && flags) flags->nonfinite = 1;
 }
 
+// z-marching variant (2.5D blocking in registers): a thread owns one row
+// pair position (ix, iy) and walks a chunk of consecutive planes.  The nine
+// (dz, dy) lines of a pair overlap those of the next plane's pair in six
+// lines, which stay in registers (v[l] for dz = 0, +1 become dz = -1, 0);
+// each step loads only the three dz = +1 lines -- 9 loads per row pair
+// instead of 27.  Products, plans and summation order are the pair
+// kernel's (box27_pair), so y is bitwise the same.
+constexpr int kS27MarchZ = 16;   // planes per work item
+
+__device__ __forceinline__ void load27_lines(const double* __restrict__ x, int64_t r, int64_t nx,
+                                             int sy, bool pres_z, bool xm, bool xp,
+                                             double (&v)[9][4], int l0) {
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy) {
+    const int l = l0 + dy + 1;
+    const bool pres = pres_z && (dy < 0 ? (sy & 1) : dy > 0 ? (sy & 2) : 1);
+    const double* base = x + r + dy * nx;
+    double2 c2 = make_double2(0.0, 0.0);
+    v[l][0] = v[l][3] = 0.0;
+    if (pres) {
+      c2 = __ldg(reinterpret_cast<const double2*>(base));
+      if (xm) v[l][0] = __ldg(base - 1);
+      if (xp) v[l][3] = __ldg(base + 2);
+    }
+    v[l][1] = c2.x;
+    v[l][2] = c2.y;
+  }
+}
+
+__global__ void __launch_bounds__(kS27Threads)
+stencil27_march_kernel(const StencilK K, FastDiv fint, const double* __restrict__ x,
+                       const double* __restrict__ b, double* __restrict__ y, lsb_flags* flags,
+                       int it, int nzc) {
+  if (gated_off(flags, it)) return;
+  // work items: (z chunk, line in plane, pair slot); interior pairs of the
+  // line first (one shared plan), then the two x-edge pairs -- as the pair
+  // kernel, so warps do not diverge on the x edges
+  const uint32_t nint = K.nx >= 6 ? (uint32_t)(K.nx / 2 - 2) : 0u;
+  const uint32_t per_line = nint + 2u;
+  const uint32_t lines = (uint32_t)K.ny;                 // lines of one plane
+  const uint32_t items_int = (uint32_t)nzc * lines * nint;
+  const uint32_t items = items_int + 2u * (uint32_t)nzc * lines;
+  const int64_t nx = K.nx, plane = (int64_t)K.nx * K.ny;
+  auto cf = [&](int o) { return K.val[o]; };
+  bool bad = false;
+  (void)per_line;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < items; i += gridDim.x * blockDim.x) {
+    uint32_t zc, iy;
+    int ix;
+    if (i < items_int) {
+      const uint32_t q = fint.div(i);               // (zc, iy) index
+      ix = 2 + 2 * (int)(i - q * nint);
+      zc = q / lines;
+      iy = q - zc * lines;
+    } else {
+      const uint32_t e = i - items_int;
+      const uint32_t q = e >> 1;
+      ix = (e & 1) ? K.nx - 2 : 0;
+      zc = q / lines;
+      iy = q - zc * lines;
+    }
+    const int z0 = (int)zc * kS27MarchZ;
+    const int z1 = min(K.nz, z0 + kS27MarchZ);
+    const int sy = ((int)iy >= 1) | (((int)iy + 1 < K.ny) << 1);
+    const bool xm = ix >= 1, xp = ix + 2 < K.nx;
+    double v[9][4];
+    const int64_t r00 = (int64_t)iy * nx + ix;       // row of (ix, iy) in plane 0
+    // lines of planes z0-1 (dz = -1) and z0 (dz = 0)
+    load27_lines(x, r00 + (int64_t)(z0 - 1) * plane, nx, sy, z0 - 1 >= K.zlo, xm, xp, v, 0);
+    load27_lines(x, r00 + (int64_t)z0 * plane, nx, sy, true, xm, xp, v, 3);
+    for (int iz = z0; iz < z1; ++iz) {
+      const int64_t r = r00 + (int64_t)iz * plane;
+      load27_lines(x, r + plane, nx, sy, iz + 1 <= K.zhi, xm, xp, v, 6);
+      const int sz = (iz - 1 >= K.zlo) | ((iz + 1 <= K.zhi) << 1);
+      double y0, y1;
+      box27_pair(v, sy, sz, xm, xp, cf, y0, y1);
+      if (!isfinite(y0) || !isfinite(y1)) bad = true;
+      double2 out;
+      if (b) {
+        const double2 bb = *reinterpret_cast<const double2*>(b + r);
+        out = make_double2(__dsub_rn(bb.x, y0), __dsub_rn(bb.y, y1));
+      } else {
+        out = make_double2(y0, y1);
+      }
+      *reinterpret_cast<double2*>(y + r) = out;
+#pragma unroll
+      for (int l = 0; l < 6; ++l)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[l][c] = v[l + 3][c];
+    }
+  }
+  if (bad && flags) flags->nonfinite = 1;
+}
+
 static bool canonical27(const lsb_stencil* S) {
   if (S->noff != 27) return false;
   for (int o = 0; o < 27; ++o)
@@ -328,6 +422,21 @@ int launch_stencil(const lsb_stencil* S, const double* x, const double* b, doubl
     if (gp > (int64_t)sm_count() * occ27p) gp = (int64_t)sm_count() * occ27p;
     if (gp < 1) gp = 1;
     const FastDiv fint = FastDiv::make(S->nx >= 6 ? (uint32_t)(S->nx / 2 - 2) : 1u);
+    if (S->nz >= 2 * kS27MarchZ && tuning(LSB_TUNE_S27_MARCH) != 2) {
+      static const int occm = [] {
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, stencil27_march_kernel, kS27Threads, 0);
+        return o > 0 ? o : 1;
+      }();
+      const int nzc = (S->nz + kS27MarchZ - 1) / kS27MarchZ;
+      const int64_t items = (int64_t)nzc * S->ny * (S->nx / 2);
+      int64_t gm = (items + kS27Threads - 1) / kS27Threads;
+      if (gm > (int64_t)sm_count() * occm) gm = (int64_t)sm_count() * occm;
+      if (gm < 1) gm = 1;
+      stencil27_march_kernel<<<(unsigned)gm, kS27Threads, 0, st>>>(K, fint, x, b, y, flags, it,
+                                                                   nzc);
+      return check_launch("stencil27_march");
+    }
     stencil27_pair_kernel<<<(unsigned)gp, kS27Threads, 0, st>>>(K, fint, x, b, y, flags, it);
     return check_launch("stencil27_pair");
   }

@@ -208,11 +208,14 @@ def test_solve_csr_dict_identical(P, monkeypatch):
     assert out[0][2] == out[1][2]
 
 
-@pytest.mark.parametrize("dims", [(4, 3, 7), (6, 5, 4), (8, 8, 8), (12, 7, 5), (9, 4, 4), (10, 3, 3)])
+@pytest.mark.parametrize("dims", [(4, 3, 7), (6, 5, 4), (8, 8, 8), (12, 7, 5), (9, 4, 4), (10, 3, 3),
+                                  (8, 6, 40), (4, 5, 33), (10, 3, 64), (16, 16, 48)])
 def test_spmv_box27_bitwise_shapes(P, dims):
     """27-point operator on boxes that exercise every edge class of the
-    row-pair kernel (nx = 4 has no interior pairs) and the odd-nx fallback;
-    y = Ax and y = b - Ax, bitwise against the reference SpMV order."""
+    row-pair kernel (nx = 4 has no interior pairs), the z-marching kernel
+    (nz >= 32: chunks of 16 planes, a ragged last chunk) and the odd-nx
+    fallback; y = Ax and y = b - Ax, bitwise against the reference SpMV
+    order."""
     from paper_1809_05805_b200.operators import convdiff27
     S, O = convdiff27(0, dims=dims), orc.convdiff27(0, dims=dims)
     n = O.n_rows
@@ -1173,3 +1176,48 @@ def test_grid_cycle_breakdown_and_jacobi(P, monkeypatch):
     c1, c0 = out["1"][0], out["0"][0]
     assert len(c1) == len(c0) and out["1"][1] == out["0"][1] and out["1"][2] == out["0"][2]
     assert np.max(np.abs(c1 - c0) / np.maximum(c0, 1e-300)) <= 1e-8
+
+
+@pytest.mark.parametrize("halo", [(1, 0), (0, 1), (1, 1)])
+def test_spmv27_march_on_slabs_bitwise(P, halo):
+    """The z-marching 27-point kernel on a z-slab with ghost planes (the
+    first chunk reads the lower ghost plane, the last the upper one):
+    bitwise the row-pair kernel's y (LSB_TUNE_S27_MARCH = 2)."""
+    from paper_1809_05805_b200 import _abi
+    from paper_1809_05805_b200.operators import StencilOperator, convdiff27
+    nx, ny, nz = 12, 10, 70
+    S = convdiff27(0, dims=(nx, ny, nz))
+    z0 = 8 if halo[0] else 0
+    nzl = 40 if halo[1] else nz - z0
+    op = StencilOperator(S, z0=z0, nz_local=nzl)
+    plane = nx * ny
+    n = plane * nzl
+    rng = np.random.default_rng(5)
+    xpad = torch.as_tensor(rng.standard_normal(n + 2 * plane + 2)).cuda()
+    xs = xpad[plane:plane + n]           # ghost planes either side
+    outs = []
+    lib = _abi.load()
+    for knob in (0, 2):
+        lib.lsb_set_tuning(_abi.TUNE_S27_MARCH, knob)
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        op.apply(xs, y)
+        outs.append(_np(y))
+    lib.lsb_set_tuning(_abi.TUNE_S27_MARCH, 0)
+    assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("persist", ["1", "0"])
+def test_zero_restarts_stalls_like_reference(P, monkeypatch, persist):
+    """GmresConfig(max_restarts=0) is legal in the reference (gmres.py:87-103):
+    the restart loop never runs and solve() reports stalled_maxiter with
+    x = x0 -- also on the launch-bound whole-solve path."""
+    monkeypatch.setenv("LSB_PERSISTENT", persist)
+    A = P.gen_laplace2d(64)
+    b = P.gen_rhs("random", A, 42)
+    led = P.ReductionLedger()
+    x, h = P.solve(A, b, config=P.GmresConfig(restart_m=30, max_restarts=0), ledger=led,
+                   diagnostics_every=0)
+    assert h.outcome == "stalled_maxiter" and h.iterations == 0
+    assert np.array_equal(x, np.zeros(A.n_rows))
+    assert abs(h.final_true_rel_res - 1.0) <= 1e-12
+    assert [e.kind for e in led.events] == ["norm", "norm"]
