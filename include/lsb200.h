@@ -345,6 +345,11 @@ int lsb_mgs1_pass(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t k, int3
  * coef2 = s) -- the r_col bookkeeping of cgs_iterated. */
 int lsb_collect_coef(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t accumulate,
                      void* stream);
+/* lsb_collect_coef (accumulate 0) from the odd entries of an interleaved
+ * [Q^T u, Q^T w] reduction: the direct methods' first pass when the SpMV
+ * z = A v_{i-1} is fused into it (lsb_lagged_reduce_spmv7 with u = v_{i-1},
+ * the last column of Q = V[:, :i]). */
+int lsb_collect_coef_pairs(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream);
 /* z <- z + Q (-coef2) and, when want_norm, Gloc[0..1] = (max|z|, sum z^2). */
 int lsb_cgs_project(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p,
                     int32_t want_norm, void* stream);

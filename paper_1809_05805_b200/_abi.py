@@ -137,6 +137,7 @@ _SIGS = {
     "lsb_lagged_correct": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_mgs1_pass": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
     "lsb_collect_coef": ([_P, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_collect_coef_pairs": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_cgs_project": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
     "lsb_cgs_project_reduce": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_direct_small": ([_P, _I32, _I32, _I32, _P], C.c_int),

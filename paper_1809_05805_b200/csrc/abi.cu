@@ -75,7 +75,7 @@ int persist_fits(int64_t, int);
 int persist_trace(long long*, int);
 int launch_cgs2_small_a(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int launch_cgs2_small_b(const lsb_arnoldi&, int, int, cudaStream_t);
-int launch_collect_coef(const lsb_arnoldi&, int, int, int, cudaStream_t);
+int launch_collect_coef(const lsb_arnoldi&, int, int, int, cudaStream_t, int = 1, int = 0);
 int launch_direct_small(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int launch_cycle_begin(const lsb_arnoldi&, cudaStream_t);
 int launch_cycle_lsq(const lsb_arnoldi&, cudaStream_t);
@@ -489,6 +489,11 @@ int lsb_lagged_reduce_spmv7_halo(const lsb_arnoldi* S, const lsb_stencil* A, int
   if (int rc = check_arnoldi(S)) return rc;
   if (!hw || !hw->epoch) return LSB_EINVAL;
   return launch_lagged_reduce_spmv7(*S, A, it, p, S_(stream), hw);
+}
+
+int lsb_collect_coef_pairs(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_collect_coef(*S, it, p, 0, S_(stream), 2, 1);
 }
 
 int lsb_preload(void) {

@@ -103,10 +103,10 @@ cgs2_small_b_kernel(lsb_arnoldi S, int it, int p) {
 // ------------------------------------------------------------------ direct kernels
 // coef = s (or coef += s) and coef2 = s from the gathered products.
 __global__ void __launch_bounds__(kSmall)
-collect_coef_kernel(lsb_arnoldi S, int it, int p, int accumulate) {
+collect_coef_kernel(lsb_arnoldi S, int it, int p, int accumulate, int stride, int offset) {
   if (gated_off(S.flags, it)) return;
   for (int j = threadIdx.x; j < p; j += blockDim.x) {
-    const double s = gsum(S, j);
+    const double s = gsum(S, stride * j + offset);
     S.coef2[j] = s;
     S.coef[j] = accumulate ? S.coef[j] + s : s;
   }
@@ -327,8 +327,9 @@ int launch_cgs2_small_b(const lsb_arnoldi& S, int it, int p, cudaStream_t st) {
   const cudaError_t le = launch_chain(use_pdl(S.n) && p <= 32, cgs2_small_b_kernel, dim3(1), dim3(kSmall), 0, st, S, it, p);
   return check_launch("cgs2_small_b", le);
 }
-int launch_collect_coef(const lsb_arnoldi& S, int it, int p, int acc, cudaStream_t st) {
-  collect_coef_kernel<<<1, kSmall, 0, st>>>(S, it, p, acc);
+int launch_collect_coef(const lsb_arnoldi& S, int it, int p, int acc, cudaStream_t st,
+                        int stride, int offset) {
+  collect_coef_kernel<<<1, kSmall, 0, st>>>(S, it, p, acc, stride, offset);
   return check_launch("collect_coef");
 }
 int launch_direct_small(const lsb_arnoldi& S, int it, int col, int p, int gc, cudaStream_t st) {

@@ -110,8 +110,11 @@ class Engine:
                 comm.register(self.inv_diag, self.off, self.n)
             self.inv_diag_view().copy_(torch.as_tensor(np.asarray(inv_diag), **f64)
                                        if not isinstance(inv_diag, torch.Tensor) else inv_diag)
-            if comm is not None and self.halo:
-                comm.halo(self.inv_diag, self.off, self.n, self.halo)
+            # the ghost entries of the scaling are exchanged by setup_exchange(),
+            # once every rank's engine exists (no rank may spin on an exchange
+            # while a peer still allocates: allocation can synchronise a
+            # device the ranks share)
+            self._setup_halo = comm is not None and self.halo
             self.op = base_op.with_scale(self.inv_diag[self.off:])
         else:
             self.op = base_op
@@ -191,6 +194,11 @@ class Engine:
         # fuse the 7-point SpMV into K1 when the operator allows it
         self.fused7 = bool(fuse) and self.lagged and _canonical7(self.op) and self.n % 2 == 0 \
             and self.cap - 1 <= 128
+        # classical CGS2: z = A v_{i-1} and the first pass's Q^T z in one pass
+        # (the lagged kernel with u = v_{i-1}, the last column of Q = V[:, :i])
+        self.fused7_direct = bool(fuse) and method == "cgs2" and _canonical7(self.op) \
+            and self.n % 2 == 0 and self.cap <= 128 \
+            and os.environ.get("LSB_FUSE_DIRECT", "1") != "0"
         # two-sync: fuse the first projection with the second reduction (K3)
         self.fuse_k3 = bool(fuse)
         # launch-bound sizes: the whole lagged cycle as one cluster launch
@@ -233,6 +241,14 @@ class Engine:
         self.scal[_abi.S_BTF] = float(btf)
         if self._peer:
             self.comm.flags = C.c_void_p(self.flags.data_ptr())
+
+    def setup_exchange(self):
+        """Exchanges the engine needs before its first cycle (multi-rank:
+        the ghost entries of the Jacobi scaling); call on every rank after
+        all ranks have built their engines."""
+        if getattr(self, "_setup_halo", False):
+            self.comm.halo(self.inv_diag, self.off, self.n, self.halo)
+            self._setup_halo = False
 
     def _persist_csr(self, base_op):
         """The operator as device CSR (bitwise the same SpMV), column-scaled
@@ -530,6 +546,27 @@ class Engine:
             self._gram_row(0, 0, 1, st)
         for i in range(1, m + 1):
             p = i
+            if self.fused7_direct:
+                # z = A v_{i-1} into V[:, i] and [Q^T v_{i-1}, Q^T z] in one pass;
+                # the first CGS pass takes the Q^T z half (odd entries)
+                if self.comm is not None and self.halo:
+                    self.comm.halo(self.Vstore[i - 1], self.off, self.n, self.halo)
+                self._call("lsb_lagged_reduce_spmv7", S, C.byref(self.op.c), i, p, st)
+                self._gather(2 * p)
+                self._call("lsb_collect_coef_pairs", S, i, p, st)
+                fused = p + 1 <= K3_MAX_COLS
+                if fused:   # z -= Q s and the 2nd pass's Q^T z in one read of Q
+                    self._call("lsb_cgs_project_reduce", S, i, i, p, st)
+                else:
+                    self._call("lsb_cgs_project", S, i, i, p, 0, st)
+                    self._call("lsb_mdot", self.col_ptr(0), self.ld, self.n, p, self.col_ptr(i),
+                               None, D.ptr(self.Gloc), self.ws.ref(), D.ptr(self.flags), i, st)
+                self._gather(p)
+                self._call("lsb_collect_coef", S, i, p, 1, st)
+                self._call("lsb_cgs_project", S, i, i, p, 1, st)
+                self._gather(2)
+                self._finish_direct(i, p, st)
+                continue
             self._op_col(i - 1, i, i)                        # z = A v_{i-1}, in place in V[:, i]
             if self.method == "cgs1_ghysels":
                 # one fused reduction: [Q^T z, max|z|, sum z^2] (fused_mdot_norm)
@@ -565,15 +602,21 @@ class Engine:
                     else:
                         self._call("lsb_cgs_project", S, i, i, p, accumulate, st)
                 self._gather(2)
-            self._call("lsb_norm_finish", D.ptr(self.G), self.S.g_parts, self.S.g_stride, self.col_ptr(i), self.n,
-                       C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_BETA), self.ws.ref(),
-                       D.ptr(self.flags), i, st)
-            self._call("lsb_direct_small", S, i, i, p, st)
-            self._call("lsb_direct_normalize", S, i, i, st)
-            if self.diagnostics:
-                self._gram_row(i, i, i + 1, st)
-            if self.true_residual:
-                self._trial(i, st)
+            self._finish_direct(i, p, st)
+
+    def _finish_direct(self, i, p, st):
+        """r_diag = ||z|| from the gathered (max, ssq) pair, K5d (breakdown,
+        Hessenberg column, Givens fold), q = z / r_diag, diagnostics."""
+        S = self.Sref
+        self._call("lsb_norm_finish", D.ptr(self.G), self.S.g_parts, self.S.g_stride,
+                   self.col_ptr(i), self.n, C.c_void_p(self.scal.data_ptr() + 8 * _abi.S_BETA),
+                   self.ws.ref(), D.ptr(self.flags), i, st)
+        self._call("lsb_direct_small", S, i, i, p, st)
+        self._call("lsb_direct_normalize", S, i, i, st)
+        if self.diagnostics:
+            self._gram_row(i, i, i + 1, st)
+        if self.true_residual:
+            self._trial(i, st)
 
     # ---------------------------------------------------------------- driving
     def prologue(self):

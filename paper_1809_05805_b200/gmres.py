@@ -388,6 +388,7 @@ class _DeviceSolve:
             # every rank's buffers exist (and are registered) before any
             # exchange kernel can spin on them
             self.comm.barrier()
+            eng.setup_exchange()
         # the host result buffer is faulted in while the device iterates
         self._xhost = D.HostBuffer(eng.n) if (self.host and eng.n >= D._STAGE_MIN
                                               and not D._PINNED_RESULTS) else None
@@ -420,7 +421,8 @@ class _DeviceSolve:
         # bookkeeping, which then overlaps the device (not for Ghysels, whose
         # arbitration is host-driven, nor with diagnostics, read from the
         # device state the next cycle overwrites)
-        ahead = cfg.method != "cgs1_ghysels" and not self.diag_every
+        ahead = cfg.method != "cgs1_ghysels" and not self.diag_every \
+            and os.environ.get("LSB_CYCLE_AHEAD", "1") != "0"
         pending = False
         for _cycle in range(cfg.max_restarts):
             hist.cycle_starts.append(self.global_it)

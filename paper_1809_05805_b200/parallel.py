@@ -207,6 +207,11 @@ def run_threads(size, fn, *args, peer=False):
                     c.close()
             s.synchronize()
         except BaseException as e:  # pragma: no cover
+            if os.environ.get("LSB_RANK_ERRORS"):
+                import sys
+                import traceback
+                sys.stderr.write(f"rank {r}: " + traceback.format_exc())
+                sys.stderr.flush()
             err.append(e)
             grp.barrier.abort()
 
