@@ -297,6 +297,9 @@ def run_gpu(args):
         return
     comm, kind = None, None
     if world > 1:
+        # communicator creation logged (ranks per NCCL communicator), also
+        # when the driver launches torchrun itself
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         comm, kind = _make_comm(args, rank)
     result = _bench_core(args, comm, world, rank, local, kind)
     if args.shared_gpu:
