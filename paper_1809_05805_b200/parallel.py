@@ -38,8 +38,19 @@ class Comm:
             dist.init_process_group(backend=backend, **kw)
         return cls()
 
+    def _staged(self):
+        """gloo moves CPU tensors only: CUDA buffers are staged through host
+        copies (validation of this class with the real kernels on one GPU;
+        NCCL takes the device buffers directly)."""
+        return dist.get_backend(self.group) == "gloo"
+
     def allgather(self, local, out):
         """out[q*len(local):(q+1)*len(local)] = rank q's `local` (one collective)."""
+        if self._staged() and local.is_cuda:
+            h = out.cpu()
+            dist.all_gather_into_tensor(h, local.cpu(), group=self.group)
+            out.copy_(h)
+            return
         dist.all_gather_into_tensor(out, local, group=self.group)
 
     def halo(self, vec, off, n, plane):
@@ -48,15 +59,28 @@ class Comm:
         <- first plane of rank+1 (one batched send/recv group)."""
         ops = []
         r, s = self.rank, self.size
+        staged = self._staged() and vec.is_cuda
+        bufs = []
+
+        def sbuf(t):
+            if not staged:
+                return t
+            h = t.cpu()
+            bufs.append((h, t))
+            return h
         if r > 0:
-            ops.append(dist.P2POp(dist.isend, vec[off:off + plane], r - 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, vec[off - plane:off], r - 1, self.group))
+            ops.append(dist.P2POp(dist.isend, sbuf(vec[off:off + plane]), r - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, sbuf(vec[off - plane:off]), r - 1, self.group))
         if r < s - 1:
-            ops.append(dist.P2POp(dist.isend, vec[off + n - plane:off + n], r + 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, vec[off + n:off + n + plane], r + 1, self.group))
+            ops.append(dist.P2POp(dist.isend, sbuf(vec[off + n - plane:off + n]), r + 1,
+                                  self.group))
+            ops.append(dist.P2POp(dist.irecv, sbuf(vec[off + n:off + n + plane]), r + 1,
+                                  self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        for h, t in bufs:
+            t.copy_(h)
 
     def exchange(self, obj):
         """Host-side all-gather of a picklable object (setup only)."""

@@ -166,7 +166,7 @@ def test_peer_cycle_is_graph_captured(P):
         assert np.array_equal(a, b)
 
 
-def _ipc_worker(rank, size, port, q):
+def _ipc_worker(rank, size, port, q, peer=True):
     import torch.distributed as dist
     os.environ.setdefault("LSB_QUIET", "1")
     torch.cuda.set_device(0)
@@ -174,7 +174,7 @@ def _ipc_worker(rank, size, port, q):
                             world_size=size)
     try:
         from paper_1809_05805_b200.parallel import Comm, PeerComm
-        comm = PeerComm(Comm(), ipc=True)
+        comm = PeerComm(Comm(), ipc=True) if peer else Comm()
         res = _rank(comm, (32, 32, 32), "one_sync_mgs", 50, 50, 1e-6)
         comm.close()
         q.put((rank, res[0], res[1], res[2], res[3], res[5]))
@@ -185,10 +185,12 @@ def _ipc_worker(rank, size, port, q):
         dist.destroy_process_group()
 
 
-def test_peer_ipc_two_processes(P):
-    """Two processes (as torchrun would start them) exchange through CUDA
-    IPC mappings of each other's buffers -- the multi-GPU transport -- here
-    both on the one GPU.  Same history as the reference golden."""
+@pytest.mark.parametrize("peer", [True, False], ids=["peer_ipc", "collective_comm"])
+def test_two_processes(P, peer):
+    """Two processes (as torchrun would start them) on the one GPU: through
+    CUDA IPC mappings of each other's buffers (the multi-GPU transport), or
+    through the collective communicator class (NCCL's code path; here gloo
+    with host staging).  Same history as the reference golden."""
     import socket
     import torch.multiprocessing as mp
     with socket.socket() as s_:
@@ -196,7 +198,7 @@ def test_peer_ipc_two_processes(P):
         port = s_.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q, peer)) for r in range(2)]
     for p_ in ps:
         p_.start()
     res = {}
