@@ -168,7 +168,8 @@ typedef struct lsb_arnoldi {
 #define LSB_TUNE_GRID_OCC 13       /* grid cycle CTAs per SM (0: 1) */
 #define LSB_TUNE_GRID_TRACE 14     /* 1: lsb_cycle_grid accumulates per-phase ns (lsb_grid_trace) */
 #define LSB_TUNE_S27_MARCH 15      /* 27-point stencil: 0 z-marching kernel when nz >= 32 (auto), 2 row-pair kernel */
-#define LSB_TUNE_COUNT 16
+#define LSB_TUNE_MGS1_GRID 16     /* lsb_mgs1_passes: 0 cooperative single launch when it fits, 2 per-pass launches */
+#define LSB_TUNE_COUNT 17
 /* Set / read a kernel-variant knob (performance only; results unchanged up
  * to the reduction tree of the affected kernel). Returns the old value. */
 int lsb_set_tuning(int32_t key, int32_t value);
@@ -341,6 +342,12 @@ int lsb_lagged_correct(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream
  * Gloc[0..1] = (max|z|, sum z^2).  One pass over z. */
 int lsb_mgs1_pass(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t k, int32_t p,
                   void* stream);
+/* All passes k = 0..p of lsb_mgs1_pass for one rank alone (g_parts == 1 and
+ * G == Gloc, else LSB_EINVAL): the whole level-1 MGS of column col
+ * (gram_schmidt.py:154-158) as one cooperative launch with a grid barrier
+ * between passes (bitwise the per-pass results), or p + 1 chained per-pass
+ * launches when the grid cannot be co-resident. */
+int lsb_mgs1_passes(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, void* stream);
 /* Sum the p rank partials in G into coef (accumulate != 0: coef += s, and
  * coef2 = s) -- the r_col bookkeeping of cgs_iterated. */
 int lsb_collect_coef(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t accumulate,

@@ -27,7 +27,7 @@ TUNE_FUSED_OCC3, TUNE_FORCE_PARTS, TUNE_ROW_CTAS_PER_SM = 1, 2, 3
 TUNE_K3_ROWS, TUNE_K3_STAGES, TUNE_CSR_THREAD_ROW = 4, 5, 6
 TUNE_PERSIST_TRACE, TUNE_PERSIST_CTAS, TUNE_FUSED_PIPE, TUNE_CSR_DICT, TUNE_PDL = 7, 8, 9, 10, 11
 TUNE_PERSIST_TIMEOUT_S = 12
-TUNE_GRID_OCC, TUNE_GRID_TRACE, TUNE_S27_MARCH = 13, 14, 15
+TUNE_GRID_OCC, TUNE_GRID_TRACE, TUNE_S27_MARCH, TUNE_MGS1_GRID = 13, 14, 15, 16
 
 
 class LsbUnavailable(RuntimeError):
@@ -136,6 +136,7 @@ _SIGS = {
     "lsb_lagged_update_reduce": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_lagged_correct": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_mgs1_pass": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_mgs1_passes": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_collect_coef": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_collect_coef_pairs": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_cgs_project": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),

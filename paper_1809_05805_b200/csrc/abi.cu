@@ -51,6 +51,7 @@ int launch_lagged_correct(const lsb_arnoldi&, int, int, cudaStream_t);
 int launch_lagged_update_reduce(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int k3_tile_rows(int);
 int launch_mgs1_pass(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
+int launch_mgs1_passes(const lsb_arnoldi&, int, int, int, cudaStream_t);
 int launch_cgs_project(const lsb_arnoldi&, int, int, int, int, cudaStream_t);
 int launch_norm_partial(const double*, int64_t, double*, const lsb_workspace*, const lsb_flags*,
                         int, cudaStream_t);
@@ -319,6 +320,12 @@ int lsb_mgs1_pass(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t k, int3
   if (int rc = check_arnoldi(S)) return rc;
   if (k < 0 || k > p || col < p || col >= S->cap) return LSB_ERANGE;
   return launch_mgs1_pass(*S, it, col, k, p, S_(stream));
+}
+
+int lsb_mgs1_passes(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (p < 0 || col < p || col >= S->cap) return LSB_ERANGE;
+  return launch_mgs1_passes(*S, it, col, p, S_(stream));
 }
 
 int lsb_collect_coef(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t accumulate,

@@ -4,6 +4,8 @@
 // from shared memory, grid-stride persistent CTAs.
 #include "tile.cuh"
 
+#include <cooperative_groups.h>
+
 namespace lsb {
 
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
@@ -220,21 +222,15 @@ __device__ __forceinline__ double sum_parts(const lsb_arnoldi& S, int e) {
   return v;
 }
 
-__global__ void __launch_bounds__(kThreads)
-mgs1_pass_kernel(lsb_arnoldi S, int it, int col, int k, int p) {
-  pdl_enter();
-  if (gated_off(S.flags, it)) return;
+// The rows of pass k: z -= h q_{k-1} (k > 0), then a0 = q_k . z (k < p) or
+// (a0, a1) = (max|z|, sum z^2) (k == p).  Shared by the per-pass kernel and
+// the cooperative all-passes kernel, so both produce the same partials.
+__device__ __forceinline__ void mgs1_rows(const lsb_arnoldi& S, int col, int k, int p, double h,
+                                          double& a0, double& a1) {
   const int64_t ld = S.ld, n = S.n;
   double* __restrict__ z = S.V + (int64_t)col * ld;
-  double h = 0.0;
-  const double* qm = nullptr;
-  if (k > 0) {
-    h = sum_parts(S, 0);
-    qm = S.V + (int64_t)(k - 1) * ld;
-    if (blockIdx.x == 0 && threadIdx.x == 0) S.coef[k - 1] = h;
-  }
+  const double* qm = k > 0 ? S.V + (int64_t)(k - 1) * ld : nullptr;
   const double* qk = k < p ? S.V + (int64_t)k * ld : nullptr;
-  double a0 = 0.0, a1 = 0.0;  // dot  or  (amax, ssq)
   auto row = [&](double zz, double qmv, double qkv) -> double {
     if (qm) zz = __dsub_rn(zz, __dmul_rn(h, qmv));
     if (qk) a0 = fma(qkv, zz, a0);
@@ -271,7 +267,20 @@ mgs1_pass_kernel(lsb_arnoldi S, int it, int col, int k, int p) {
     const double zz = row(z[r], qm ? qm[r] : 0.0, qk ? qk[r] : 0.0);
     if (qm) z[r] = zz;
   }
-  if (qk) {
+}
+
+__global__ void __launch_bounds__(kThreads)
+mgs1_pass_kernel(lsb_arnoldi S, int it, int col, int k, int p) {
+  pdl_enter();
+  if (gated_off(S.flags, it)) return;
+  double h = 0.0;
+  if (k > 0) {
+    h = sum_parts(S, 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) S.coef[k - 1] = h;
+  }
+  double a0 = 0.0, a1 = 0.0;  // dot  or  (amax, ssq)
+  mgs1_rows(S, col, k, p, h, a0, a1);
+  if (k < p) {
     const double v[1] = {a0};
     const int op[1] = {0};
     grid_reduce<1>(v, op, S.ws.partial, S.ws.counter, S.Gloc);
@@ -279,6 +288,63 @@ mgs1_pass_kernel(lsb_arnoldi S, int it, int col, int k, int p) {
     const double v[2] = {a0, a1};
     const int op[2] = {1, 0};
     grid_reduce<2>(v, op, S.ws.partial, S.ws.counter, S.Gloc);
+  }
+}
+
+// All p + 1 passes of one column in ONE cooperative launch (single rank:
+// the reduction of pass k feeds pass k + 1 without a host all-gather).  Each
+// pass ends with a grid barrier instead of a kernel boundary; the pass-k dot
+// is then summed redundantly by every CTA in exactly grid_reduce's order
+// over the same per-CTA partials (same grid, same rows per CTA as the
+// per-pass kernel), so h, coef and z are bitwise the per-pass results.
+// Partials alternate between two halves of the workspace (a fast CTA writes
+// pass k+1's partial while a slow one still reads pass k's); the final
+// (max, ssq) reduction uses the next 2G entries (lsb_partial_len >= 4 *
+// 8 * SMs >= 4G).
+__global__ void __launch_bounds__(kThreads)
+mgs1_grid_kernel(lsb_arnoldi S, int it, int col, int p) {
+  if (gated_off(S.flags, it)) return;      // grid-uniform: no CTA reaches a barrier
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  __shared__ double red[kWarps];
+  __shared__ double s_h;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  double h = 0.0;
+  for (int k = 0; k <= p; ++k) {
+    if (k > 0 && blockIdx.x == 0 && threadIdx.x == 0) S.coef[k - 1] = h;
+    double a0 = 0.0, a1 = 0.0;
+    mgs1_rows(S, col, k, p, h, a0, a1);
+    if (k == p) {   // (max, ssq) past both halves: slow CTAs may still read pass p-1's
+      const double v[2] = {a0, a1};
+      const int op[2] = {1, 0};
+      grid_reduce<2>(v, op, S.ws.partial + 2 * (size_t)G, S.ws.counter, S.Gloc);
+      break;
+    }
+    double* part = S.ws.partial + (size_t)(k & 1) * G;
+    const double x = warp_sum(a0);
+    if (lane == 0) red[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double y = red[0];
+      for (int w = 1; w < kWarps; ++w) y = y + red[w];
+      part[blockIdx.x] = y;
+    }
+    grid.sync();
+    if (warp == 0) {
+      double y = 0.0;
+      bool first = true;
+      for (int c = lane; c < G; c += 32) {
+        const double t = __ldcg(part + c);
+        if (first) { y = t; first = false; } else { y = y + t; }
+      }
+      if (first) y = 0.0;
+      y = warp_sum(y);
+      if (lane == 0) s_h = y;
+    }
+    __syncthreads();
+    h = s_h;
+    if (blockIdx.x == 0 && threadIdx.x == 0) S.Gloc[0] = h;
+    __syncthreads();                       // s_h is rewritten after the next barrier only
   }
 }
 
@@ -291,6 +357,35 @@ int launch_mgs1_pass(const lsb_arnoldi& S, int it, int col, int k, int p, cudaSt
                                       dim3((unsigned)row_grid(S.n / 2 + 1, occ_)), dim3(kThreads),
                                       0, st, S, it, col, k, p);
   return check_launch("mgs1_pass", le);
+}
+
+// lsb_mgs1_passes: passes 0..p of column col.  Cooperative single launch
+// when the rank is alone (g_parts == 1, G aliases Gloc) and the per-pass
+// grid is co-resident for the cooperative kernel; else p + 1 chained
+// per-pass launches (identical results either way).
+int launch_mgs1_passes(const lsb_arnoldi& S, int it, int col, int p, cudaStream_t st) {
+  if (S.g_parts != 1 || S.G != S.Gloc) return LSB_EINVAL;
+  static const int occ_pass = wave(mgs1_pass_kernel, 0);
+  static const int occ_grid = wave(mgs1_grid_kernel, 0);
+  const int G = row_grid(S.n / 2 + 1, occ_pass);
+  if (tuning(LSB_TUNE_MGS1_GRID) != 2 && (int64_t)G <= (int64_t)sm_count() * occ_grid) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return check_launch("mgs1_grid", cudaLaunchKernelEx(&cfg, mgs1_grid_kernel, S, it, col, p));
+  }
+  for (int k = 0; k <= p; ++k) {
+    const int rc = launch_mgs1_pass(S, it, col, k, p, st);
+    if (rc) return rc;
+  }
+  return LSB_OK;
 }
 
 // z <- z - Q coef2 (cgs_iterated pass, gram_schmidt.py:136-138), optional

@@ -585,9 +585,12 @@ class Engine:
                     self._trial(i, st)
                 continue
             if self.method == "mgs_l1":
-                for k in range(p + 1):
-                    self._call("lsb_mgs1_pass", S, i, i, k, p, st)
-                    self._gather(2)
+                if self.comm is None:     # all passes in one cooperative launch
+                    self._call("lsb_mgs1_passes", S, i, i, p, st)
+                else:
+                    for k in range(p + 1):
+                        self._call("lsb_mgs1_pass", S, i, i, k, p, st)
+                        self._gather(2)
             else:
                 fused = self.fuse_k3 and p + 1 <= K3_MAX_COLS
                 for accumulate in (0, 1):

@@ -215,10 +215,9 @@ def _direct(Q, a, ledger, btf, passes):
     from .kernels import DOT, MDOT, NORM
     zp = C.c_void_p(store.data_ptr() + 8 * ld * p)
     if passes == 0:  # level-1 MGS: p fused axpy+dot passes, then the norm pass
-        for k in range(p + 1):
-            if k < p:
-                ledger.record(DOT, 1)
-            _abi.call("lsb_mgs1_pass", ref, 0, p, k, p, st)
+        for k in range(p):
+            ledger.record(DOT, 1)
+        _abi.call("lsb_mgs1_passes", ref, 0, p, p, st)   # one cooperative launch
     else:
         fused_next = False   # Q^T z of this pass already produced by the previous projection
         for ps in range(passes if p else 0):

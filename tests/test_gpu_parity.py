@@ -400,6 +400,29 @@ def test_direct_kernels_events(P):
         P.cgs_iterated(Q[:, :2], Q[:, :2] @ np.ones(2), 2, P.ReductionLedger())
 
 
+@pytest.mark.parametrize("n,p", [(20, 5), (100003, 13), (1 << 20, 40)])
+def test_mgs1_cooperative_bitwise(P, n, p):
+    """The level-1 MGS as one cooperative launch (grid barriers between the
+    passes) is bitwise the p + 1 per-pass launches: q, coefficients, r_diag
+    (odd n: the tail row; n = 2^20: the full co-resident grid)."""
+    from paper_1809_05805_b200 import _abi
+    lib = _abi.load()
+    rng = np.random.default_rng(n + p)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, p)))
+    a = rng.standard_normal(n)
+    outs = []
+    for knob in (0, 2):
+        lib.lsb_set_tuning(_abi.TUNE_MGS1_GRID, knob)
+        try:
+            outs.append(P.mgs_level1(Q, a, P.ReductionLedger()))
+        finally:
+            lib.lsb_set_tuning(_abi.TUNE_MGS1_GRID, 0)
+    (q0, c0, d0), (q1, c1, d1) = outs
+    assert np.array_equal(q0, q1) and np.array_equal(c0, c1) and d0 == d1
+    qo, co, do = orc.level1_mgs(Q, a, orc.Ledger())
+    assert np.allclose(c0, co, atol=1e-12) and abs(d0 - do) <= 1e-12 * do
+
+
 # ------------------------------------------------------------------ GMRES histories
 def _solve(P, A, b, meth, m, restarts, tol, diag=0, **kw):
     led = P.ReductionLedger()

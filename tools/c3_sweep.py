@@ -1,18 +1,24 @@
 """Config C3: orthogonalization-only sweep, n = 2^20 .. 2^27,
 k = 10, 20, 50, 100.  At each (n, k), p = k, one "step" is the per-column
-kernel sequence of a variant:
+kernel sequence of a variant, replayed as a CUDA graph as the engine runs its
+cycles (`--eager`: launched from the host, round 1's protocol):
 
   one_sync  K1 lagged_reduce -> K5 mgs_lvl2_small -> K2 lagged_update
             (algorithmic 8n(2p+4))
   two_sync  K1 -> K5a -> K3 lagged_update_reduce -> K5b -> K4 lagged_correct
             (8n(3p+6); unfused K2 + K1' when p + 1 > 110)
-  mgs_l1    p+1 fused K8 axpy+dot passes -> norm -> K5d -> scale
+  mgs_l1    p+1 fused K8 axpy+dot passes (one cooperative launch, grid
+            barriers between passes) -> norm -> K5d -> scale
             (8n(4p+3))
 
 V (cap k+2, Fortran-like column store) is filled from default_rng(0)-style
 normals (torch generator seed 0) with unit columns, w from seed 1.  L2 is
-flushed (256 MB write) before every timed rep; each rep is bracketed by CUDA
-events on the launching stream.  Output: one JSON object per line.
+flushed before every timed rep by READING a 256 MB buffer, so the step starts
+with none of its data in L2 and no dirty lines to write back (round 1 wrote
+the buffer instead: up to 126 MB of dirty-line write-back then landed inside
+the timed step, ~15-30 us at n <= 2^22; `--dirty-flush` restores that).  Each
+rep is bracketed by CUDA events on the launching stream.  Output: one JSON
+object per line.
 
     python tools/c3_sweep.py [--ns 20,21,...,27] [--ks 10,20,50,100] [--reps 5]
 """
@@ -71,9 +77,17 @@ def main():
     ap.add_argument("--ks", default="10,20,50,100")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--variants", default="one_sync,two_sync,mgs_l1")
+    ap.add_argument("--dirty-flush", action="store_true",
+                    help="round-1 flush: write the 256 MB buffer, leaving L2 full of dirty "
+                         "lines whose write-back lands inside the timed step")
+    ap.add_argument("--eager", action="store_true",
+                    help="issue each step's launches from the host (default: replay the "
+                         "step as a CUDA graph, as the engine runs its cycles)")
     a = ap.parse_args()
-    lib, stream = _abi.load(), D.stream()
-    flush = torch.empty(1 << 25, dtype=torch.float64, device="cuda")   # 256 MB > L2
+    lib = _abi.load()
+    cur = {"s": D.stream()}
+    flush = torch.ones(1 << 25, dtype=torch.float64, device="cuda")   # 256 MB > L2
+    sink = torch.empty((), dtype=torch.float64, device="cuda")
 
     def call(name, *args):
         _abi.check(getattr(lib, name)(*args), name)
@@ -87,11 +101,13 @@ def main():
             col = lambda j: C.c_void_p(V.data_ptr() + 8 * j * ld)  # noqa: E731
 
             def one_sync():
+                stream = cur["s"]
                 call("lsb_lagged_reduce", ref, 0, p, stream)
                 call("lsb_mgs_lvl2_small", ref, 0, p, 1, 0, stream)
                 call("lsb_lagged_update", ref, 0, p, 1, stream)
 
             def two_sync():
+                stream = cur["s"]
                 call("lsb_lagged_reduce", ref, 0, p, stream)
                 call("lsb_cgs2_lvl2_small_a", ref, 0, p, 1, 0, stream)
                 if p + 1 <= 110:
@@ -104,8 +120,8 @@ def main():
                 call("lsb_lagged_correct", ref, 0, p, stream)
 
             def mgs_l1():
-                for kk in range(p + 1):
-                    call("lsb_mgs1_pass", ref, 0, p, kk, p, stream)
+                stream = cur["s"]
+                call("lsb_mgs1_passes", ref, 0, p, p, stream)
                 call("lsb_norm_finish", D.ptr(st["G"]), 1, 2 * (p + 2), col(p), n,
                      C.c_void_p(st["scal"].data_ptr() + 8 * _abi.S_BETA), ws.ref(), None, -1,
                      stream)
@@ -120,9 +136,22 @@ def main():
                 for _ in range(2):
                     fn()
                 torch.cuda.synchronize()
+                if not a.eager:
+                    g = torch.cuda.CUDAGraph()
+                    side = torch.cuda.Stream()
+                    with torch.cuda.graph(g, stream=side):
+                        cur["s"] = C.c_void_p(side.cuda_stream)
+                        fn()
+                    cur["s"] = D.stream()
+                    g.replay()
+                    torch.cuda.synchronize()
+                    fn = g.replay
                 tot = 0.0
                 for _ in range(a.reps):
-                    flush.fill_(1.0)
+                    if a.dirty_flush:
+                        flush.fill_(1.0)
+                    else:
+                        torch.sum(flush, dim=0, out=sink)
                     e0 = torch.cuda.Event(enable_timing=True)
                     e1 = torch.cuda.Event(enable_timing=True)
                     e0.record()
@@ -132,7 +161,9 @@ def main():
                     tot += e0.elapsed_time(e1)
                 ms = tot / a.reps
                 gbs = byts[var] / (ms / 1e3) / 1e9
-                print(json.dumps({"n": n, "k": k, "variant": var, "ms": round(ms, 4),
+                print(json.dumps({"n": n, "k": k, "variant": var, "graph": not a.eager,
+                                  "flush": "write" if a.dirty_flush else "read",
+                                  "ms": round(ms, 4),
                                   "alg_GBps": round(gbs, 1), "frac": round(gbs * 1e9 / PEAK, 3),
                                   "fits_L2": n * (k + 2) * 8 <= 126 * 2 ** 20}), flush=True)
             del V, st, ws, S
