@@ -357,7 +357,9 @@ int lsb_collect_coef(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t accumu
  * z = A v_{i-1} is fused into it (lsb_lagged_reduce_spmv7 with u = v_{i-1},
  * the last column of Q = V[:, :i]). */
 int lsb_collect_coef_pairs(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream);
-/* z <- z + Q (-coef2) and, when want_norm, Gloc[0..1] = (max|z|, sum z^2). */
+/* z <- z + Q (-coef2) and, when want_norm == 1, Gloc[0..1] = (max|z|,
+ * sum z^2); want_norm == 2: then z /= scal[BETA] unless flags->broke_iter ==
+ * it (lsb_direct_normalize fused, bitwise the same). */
 int lsb_cgs_project(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p,
                     int32_t want_norm, void* stream);
 /* cgs_iterated's first projection fused with the second pass's reduction
@@ -374,6 +376,12 @@ int lsb_direct_small(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, v
  * sum z^2] -> y, h = sqrt(||z||^2 - y.y), Hbar column, Givens fold; stops the
  * cycle with LSB_GHYSELS_CHECK when the radicand cancels. */
 int lsb_ghysels_small(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, void* stream);
+/* The same with G = [v.q_0, z.q_0, v.q_1, z.q_1, ..., max|z|, sum z^2] (the
+ * pair layout lsb_lagged_reduce_spmv7 writes with u = v_{col-1}; y_j = G[2j+1],
+ * norm pair at G[2p], G[2p+1]): the SpMV of the Ghysels step fused into its
+ * reduction. */
+int lsb_ghysels_small_pairs(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p,
+                            void* stream);
 /* V[:, col] /= r_diag unless the column broke down. */
 int lsb_direct_normalize(const lsb_arnoldi* S, int32_t it, int32_t col, void* stream);
 

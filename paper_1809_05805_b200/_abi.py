@@ -144,6 +144,7 @@ _SIGS = {
     "lsb_direct_small": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_direct_normalize": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_ghysels_small": ([_P, _I32, _I32, _I32, _P], C.c_int),
+    "lsb_ghysels_small_pairs": ([_P, _I32, _I32, _I32, _P], C.c_int),
     "lsb_settle": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_cycle_persistent": ([_P, _P, _I32, _P], C.c_int),
     "lsb_solve_persistent": ([_P, _P, _I32, _P, _P, _P, _I32, _P], C.c_int),

@@ -85,7 +85,7 @@ int launch_givens_update(double*, double*, double*, int, const double*, int, dou
 int launch_lagged_reduce_spmv7(const lsb_arnoldi&, const lsb_stencil*, int, int, cudaStream_t,
                                const lsb_halo_wait* = nullptr);
 int launch_trial_lsq(const lsb_arnoldi&, int, double*, cudaStream_t);
-int launch_ghysels_small(const lsb_arnoldi&, int, int, int, cudaStream_t);
+int launch_ghysels_small(const lsb_arnoldi&, int, int, int, cudaStream_t, int = 1, int = 0);
 int launch_settle(const lsb_arnoldi&, int, int, cudaStream_t);
 int launch_trial_combine(const lsb_arnoldi&, int, const double*, const double*, double*,
                          const double*, cudaStream_t);
@@ -363,6 +363,12 @@ int lsb_settle(const lsb_arnoldi* S, int32_t it, int32_t col, void* stream) {
 int lsb_ghysels_small(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p, void* stream) {
   if (int rc = check_arnoldi(S)) return rc;
   return launch_ghysels_small(*S, it, col, p, S_(stream));
+}
+
+int lsb_ghysels_small_pairs(const lsb_arnoldi* S, int32_t it, int32_t col, int32_t p,
+                            void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  return launch_ghysels_small(*S, it, col, p, S_(stream), 2, 1);
 }
 
 int lsb_direct_normalize(const lsb_arnoldi* S, int32_t it, int32_t col, void* stream) {

@@ -145,20 +145,22 @@ direct_small_kernel(lsb_arnoldi S, int it, int col, int p, int gc) {
 // the rotation is still folded, and the cycle stops with status
 // LSB_GHYSELS_CHECK so the host can run the true-residual arbitration of
 // gmres.py:338-359 before deciding converged / breakdown / cancellation.
+// Strided form: y_j at G[stride j + offset] and the norm pair after the 2p
+// pair entries of the fused SpMV + reduction (stride 2, offset 1).
 __global__ void __launch_bounds__(kSmall)
-ghysels_small_kernel(lsb_arnoldi S, int it, int col, int p) {
+ghysels_small_kernel(lsb_arnoldi S, int it, int col, int p, int stride, int offset) {
   if (gated_off(S.flags, it)) return;
   __shared__ SmallShared sh;
   const int t = threadIdx.x, cap = S.cap;
   for (int j = t; j < p; j += blockDim.x) {
-    const double y = gsum(S, j);
+    const double y = gsum(S, stride * j + offset);
     sh.col[j] = y;
     S.coef[j] = y;
     S.coef2[j] = y;
   }
   __syncthreads();
   if (t == 0) {
-    const double ssq = gsum(S, p + 1);
+    const double ssq = gsum(S, stride * p + 1);
     const double znorm = sqrt(ssq);
     double yy = 0.0;
     for (int j = 0; j < p; ++j) yy = fma(sh.col[j], sh.col[j], yy);
@@ -187,9 +189,10 @@ ghysels_small_kernel(lsb_arnoldi S, int it, int col, int p) {
   }
 }
 
-int launch_ghysels_small(const lsb_arnoldi& S, int it, int col, int p, cudaStream_t st) {
+int launch_ghysels_small(const lsb_arnoldi& S, int it, int col, int p, cudaStream_t st,
+                         int stride, int offset) {
   if (p + 2 > 2 * S.cap || col < 1) return LSB_ERANGE;
-  ghysels_small_kernel<<<1, kSmall, 0, st>>>(S, it, col, p);
+  ghysels_small_kernel<<<1, kSmall, 0, st>>>(S, it, col, p, stride, offset);
   return check_launch("ghysels_small");
 }
 

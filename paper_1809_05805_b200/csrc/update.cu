@@ -398,6 +398,11 @@ cgs_project_kernel(lsb_arnoldi S, int it, int col, int p, int want_norm) {
   __syncthreads();
   const int64_t ld = S.ld, n = S.n;
   double* __restrict__ z = S.V + (int64_t)col * ld;
+  // want_norm == 2: then q = z / r_diag unless the column broke down
+  // (lsb_direct_normalize fused: the same rounded difference, then the same
+  // division -- bitwise the two-kernel result)
+  const bool divide = want_norm == 2 && !(S.flags && S.flags->broke_iter == it);
+  const double d = want_norm == 2 ? S.scal[LSB_S_BETA] : 1.0;
   double amax = 0.0, ssq = 0.0;
   const int64_t npair = n / 2;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
@@ -413,6 +418,10 @@ cgs_project_kernel(lsb_arnoldi S, int it, int col, int p, int want_norm) {
     double2 zz = ld2(z + r);
     zz.x = zz.x + acc.x;
     zz.y = zz.y + acc.y;
+    if (divide) {
+      zz.x = __ddiv_rn(zz.x, d);
+      zz.y = __ddiv_rn(zz.y, d);
+    }
     st2(z + r, zz);
     amax = fmax(amax, fmax(fabs(zz.x), fabs(zz.y)));
     ssq = fma(zz.x, zz.x, ssq);
@@ -422,12 +431,13 @@ cgs_project_kernel(lsb_arnoldi S, int it, int col, int p, int want_norm) {
     const int64_t r = n - 1;
     double acc = 0.0;
     for (int k = 0; k < p; ++k) acc = fma(-sc[k], S.V[(int64_t)k * ld + r], acc);
-    const double zz = z[r] + acc;
+    double zz = z[r] + acc;
+    if (divide) zz = __ddiv_rn(zz, d);
     z[r] = zz;
     amax = fmax(amax, fabs(zz));
     ssq = fma(zz, zz, ssq);
   }
-  if (want_norm) {
+  if (want_norm == 1) {
     const double v[2] = {amax, ssq};
     const int op[2] = {1, 0};
     grid_reduce<2>(v, op, S.ws.partial, S.ws.counter, S.Gloc);

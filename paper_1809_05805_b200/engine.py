@@ -199,6 +199,10 @@ class Engine:
         self.fused7_direct = bool(fuse) and method == "cgs2" and _canonical7(self.op) \
             and self.n % 2 == 0 and self.cap <= 128 \
             and os.environ.get("LSB_FUSE_DIRECT", "1") != "0"
+        # cgs1_ghysels: z = A v_{i-1} and Q^T z in one pass the same way
+        self.fused7_ghysels = bool(fuse) and method == "cgs1_ghysels" and _canonical7(self.op) \
+            and self.n % 2 == 0 and self.cap <= 128 \
+            and os.environ.get("LSB_FUSE_DIRECT", "1") != "0"
         # two-sync: fuse the first projection with the second reduction (K3)
         self.fuse_k3 = bool(fuse)
         # launch-bound sizes: the whole lagged cycle as one cluster launch
@@ -567,6 +571,23 @@ class Engine:
                 self._gather(2)
                 self._finish_direct(i, p, st)
                 continue
+            if self.fused7_ghysels:
+                # [Q^T v_{i-1}, Q^T z] pairs with z = A v_{i-1} (one pass), then
+                # (max|z|, sum z^2) after them: fused_mdot_norm's reduction
+                if self.comm is not None and self.halo:
+                    self.comm.halo(self.Vstore[i - 1], self.off, self.n, self.halo)
+                self._call("lsb_lagged_reduce_spmv7", S, C.byref(self.op.c), i, p, st)
+                self._call("lsb_norm_partial", self.col_ptr(i), self.n,
+                           C.c_void_p(self.Gloc.data_ptr() + 8 * 2 * p), self.ws.ref(),
+                           D.ptr(self.flags), i, st)
+                self._gather(2 * p + 2)
+                self._call("lsb_ghysels_small_pairs", S, i, i, p, st)
+                self._call("lsb_cgs_project", S, i, i, p, 2, st)   # + q = z / h
+                if self.diagnostics:
+                    self._gram_row(i, i, i + 1, st)
+                if self.true_residual:
+                    self._trial(i, st)
+                continue
             self._op_col(i - 1, i, i)                        # z = A v_{i-1}, in place in V[:, i]
             if self.method == "cgs1_ghysels":
                 # one fused reduction: [Q^T z, max|z|, sum z^2] (fused_mdot_norm)
@@ -577,8 +598,7 @@ class Engine:
                            D.ptr(self.flags), i, st)
                 self._gather(p + 2)
                 self._call("lsb_ghysels_small", S, i, i, p, st)
-                self._call("lsb_cgs_project", S, i, i, p, 0, st)
-                self._call("lsb_direct_normalize", S, i, i, st)
+                self._call("lsb_cgs_project", S, i, i, p, 2, st)   # + q = z / h
                 if self.diagnostics:
                     self._gram_row(i, i, i + 1, st)
                 if self.true_residual:

@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--method", default="two_sync_cgs2")
     ap.add_argument("--cycles", type=int, default=2)
     ap.add_argument("--out", default="")
+    ap.add_argument("--seq", default="",
+                    help="comma-separated kernel names: also record their per-launch "
+                         "durations in launch order (first cycle)")
     a = ap.parse_args()
     A = P.gen_laplace3d(a.N)
     b = np.random.default_rng(42).standard_normal(A.n_rows)
@@ -51,12 +54,17 @@ def main():
     span = (evs[-1].time_range.end - evs[0].time_range.start) if evs else 0
     busy = 0.0
     last_end = None
+    want = set(x for x in a.seq.split(",") if x)
+    seq = collections.defaultdict(list)
     for e in evs:
-        nm = e.name.split("(")[0].replace("void ", "").replace("lsb::", "")
+        nm = e.name.replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
+        nm = nm.split("(")[0].replace("void ", "").replace("lsb::", "")
         nm = nm.split("<")[0]
         d = e.time_range.end - e.time_range.start
         tot[nm] += d
         cnt[nm] += 1
+        if nm in want:
+            seq[nm].append(round(d, 1))
         busy += d
         if last_end is not None and e.time_range.start > last_end:
             gaps[nm] += e.time_range.start - last_end   # idle before this kernel
@@ -67,6 +75,8 @@ def main():
            "kernels": {k: {"n": cnt[k], "total_us": round(tot[k], 1),
                            "avg_us": round(tot[k] / cnt[k], 2),
                            "idle_before_us": round(gaps[k], 1)} for k in tot}}
+    if want:
+        out["seq_us"] = dict(seq)
     print(json.dumps(out, indent=1))
     if a.out:
         with open(a.out, "w") as fh:
