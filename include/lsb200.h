@@ -253,6 +253,11 @@ int lsb_lagged_reduce(const lsb_arnoldi* S, int32_t it, int32_t p, void* stream)
  * gmres.py:411-414.  Ghost planes (multi-rank) must already be in place. */
 int lsb_lagged_reduce_spmv7(const lsb_arnoldi* S, const lsb_stencil* A, int32_t it, int32_t p,
                             void* stream);
+/* The same plus (max|w|, sum w^2) in Gloc[2p], Gloc[2p+1] (norm_partial's
+ * per-row update, fixed-order CTA tree): fused_mdot_norm (kernels.py:315-325)
+ * of the cgs1_ghysels step with its SpMV, u = v_{i-1}. */
+int lsb_lagged_reduce_spmv7_norm(const lsb_arnoldi* S, const lsb_stencil* A, int32_t it, int32_t p,
+                            void* stream);
 
 /* Small-state update of the one-reduce MGS-CWY kernel: beta, breakdown test,
  * R/T columns, c = T^T y (/beta).  givens_col > 0 also folds Hessenberg

@@ -129,6 +129,7 @@ _SIGS = {
     "lsb_scale_div": ([_P, _I64, _P, _P, _P, _I32, _P], C.c_int),
     "lsb_lagged_reduce": ([_P, _I32, _I32, _P], C.c_int),
     "lsb_lagged_reduce_spmv7": ([_P, _P, _I32, _I32, _P], C.c_int),
+    "lsb_lagged_reduce_spmv7_norm": ([_P, _P, _I32, _I32, _P], C.c_int),
     "lsb_mgs_lvl2_small": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
     "lsb_cgs2_lvl2_small_a": ([_P, _I32, _I32, _I32, _I32, _P], C.c_int),
     "lsb_cgs2_lvl2_small_b": ([_P, _I32, _I32, _P], C.c_int),

@@ -83,7 +83,7 @@ int launch_cycle_lsq(const lsb_arnoldi&, cudaStream_t);
 int launch_restart_check(const lsb_arnoldi&, int, cudaStream_t);
 int launch_givens_update(double*, double*, double*, int, const double*, int, double*, cudaStream_t);
 int launch_lagged_reduce_spmv7(const lsb_arnoldi&, const lsb_stencil*, int, int, cudaStream_t,
-                               const lsb_halo_wait* = nullptr);
+                               const lsb_halo_wait* = nullptr, bool = false);
 int launch_trial_lsq(const lsb_arnoldi&, int, double*, cudaStream_t);
 int launch_ghysels_small(const lsb_arnoldi&, int, int, int, cudaStream_t, int = 1, int = 0);
 int launch_settle(const lsb_arnoldi&, int, int, cudaStream_t);
@@ -253,6 +253,13 @@ int lsb_lagged_reduce_spmv7(const lsb_arnoldi* S, const lsb_stencil* A, int32_t 
   if (int rc = check_arnoldi(S)) return rc;
   if (!A) return LSB_EINVAL;
   return launch_lagged_reduce_spmv7(*S, A, it, p, S_(stream));
+}
+
+int lsb_lagged_reduce_spmv7_norm(const lsb_arnoldi* S, const lsb_stencil* A, int32_t it, int32_t p,
+                            void* stream) {
+  if (int rc = check_arnoldi(S)) return rc;
+  if (!A) return LSB_EINVAL;
+  return launch_lagged_reduce_spmv7(*S, A, it, p, S_(stream), nullptr, true);
 }
 
 int lsb_mgs_lvl2_small(const lsb_arnoldi* S, int32_t it, int32_t p, int32_t krylov_scale,

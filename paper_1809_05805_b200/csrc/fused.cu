@@ -51,9 +51,11 @@ struct Stencil7 {
 // One row pair (lr, lr+1) of w = A u from the staged tile (numpy order:
 // first present product + sequential sum of the rest), written to the
 // shared w tile and to HBM.
+template <bool NORM = false>
 __device__ __forceinline__ void s7_tile_pair(const Stencil7& K, const double* ut, const double* zt,
                                              const double* pt, int lr, int64_t r, int64_t n,
-                                             double* sw, double* __restrict__ wout, bool& bad) {
+                                             double* sw, double* __restrict__ wout, bool& bad,
+                                             double (&nrm)[2]) {
   if (r >= n) { sw[lr] = sw[lr + 1] = 0.0; return; }
   const uint32_t line = K.fx.div((uint32_t)r);
   const int ix = (int)((uint32_t)r - line * (uint32_t)K.nx);
@@ -86,12 +88,21 @@ __device__ __forceinline__ void s7_tile_pair(const Stencil7& K, const double* ut
 #undef LSB_T
   const double s0 = __dadd_rn(f0, a0), s1 = __dadd_rn(f1, a1);
   if (!isfinite(s0) || !isfinite(s1)) bad = true;
+  if constexpr (NORM) {   // norm_partial's per-row update (a NaN row poisons max and ssq)
+    nrm[0] = fmax(nrm[0], fabs(s0));
+    if (isnan(s0)) nrm[0] = s0;
+    nrm[1] = fma(s0, s0, nrm[1]);
+    nrm[0] = fmax(nrm[0], fabs(s1));
+    if (isnan(s1)) nrm[0] = s1;
+    nrm[1] = fma(s1, s1, nrm[1]);
+  }
   sw[lr] = s0;
   sw[lr + 1] = s1;
   *reinterpret_cast<double2*>(wout + r) = make_double2(s0, s1);
 }
 
-template <int R, int SLOTS, int MINB>
+// NORM: also (max|w|, sum w^2) as entries 2p, 2p+1 (fused_mdot_norm)
+template <int R, int SLOTS, int MINB, bool NORM = false>
 __global__ void __launch_bounds__(kThreads, MINB)
 mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
                   double* __restrict__ wout, const Stencil7 K, double* __restrict__ out,
@@ -113,6 +124,7 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) acc[s][0] = acc[s][1] = 0.0;
   bool bad = false;
+  double nrm[2] = {0.0, 0.0};
 
   // u tile + halo + z-neighbour tiles arrive by three TMA bulk copies issued
   // by one thread, completion on a per-buffer mbarrier (double-buffered)
@@ -172,7 +184,7 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
     // ---- w = A u for the tile rows (row pairs; nx even keeps pairs in a line)
 #pragma unroll 2
     for (int j = threadIdx.x; j < kTile / 2; j += kThreads)
-      s7_tile_pair(K, ut, zt, pt, 2 * j, r0 + 2 * j, n, sw, wout, bad);
+      s7_tile_pair<NORM>(K, ut, zt, pt, 2 * j, r0 + 2 * j, n, sw, wout, bad, nrm);
     __syncthreads();
     // ---- column sweep: [Q^T u, Q^T w] partials (same item deal as mdot_kernel)
 #pragma unroll
@@ -224,6 +236,11 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
       const double x = warp_sum(acc[s][v]);
       if (lane == 0) red[warp + kWarps * s][v] = x;
     }
+  __shared__ double nred[kWarps][2];
+  if (NORM) {
+    const double m = warp_max(nrm[0]), q = warp_sum(nrm[1]);
+    if (lane == 0) { nred[warp][0] = m; nred[warp][1] = q; }
+  }
   __syncthreads();
   const int G = gridDim.x;
   for (int e = threadIdx.x; e < p * 2; e += kThreads) {
@@ -233,6 +250,12 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
     for (int pr = 1; pr < R; ++pr) x += red[k * R + pr][v];
     partial[(size_t)e * G + blockIdx.x] = x;
   }
+  if (NORM && threadIdx.x < 2) {
+    const int v = threadIdx.x;
+    double x = nred[0][v];
+    for (int w = 1; w < kWarps; ++w) x = v == 0 ? fmax(x, nred[w][v]) : x + nred[w][v];
+    partial[(size_t)(2 * p + v) * G + blockIdx.x] = x;
+  }
   __shared__ bool is_last;
   __threadfence();
   __syncthreads();
@@ -240,10 +263,15 @@ mdot_spmv7_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int p,
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  for (int e = warp; e < 2 * p; e += kWarps) {
+  const int E = 2 * p + (NORM ? 2 : 0);
+  for (int e = warp; e < E; e += kWarps) {
+    const bool mx = NORM && e == 2 * p;
     double x = 0.0;
-    for (int c = lane; c < G; c += 32) x += __ldcg(partial + (size_t)e * G + c);
-    x = warp_sum(x);
+    for (int c = lane; c < G; c += 32) {
+      const double y = __ldcg(partial + (size_t)e * G + c);
+      x = mx ? fmax(x, y) : x + y;
+    }
+    x = mx ? warp_max(x) : warp_sum(x);
     if (lane == 0) out[e] = x;
   }
   if (threadIdx.x == 0) *counter = 0u;
@@ -279,6 +307,7 @@ mdot_spmv7_pipe_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int 
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) acc[s][0] = acc[s][1] = 0.0;
   bool bad = false;
+  double nrm[2];   // unused (no norm in the pipelined variant)
   __shared__ __align__(8) uint64_t bars[2];
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
@@ -311,7 +340,7 @@ mdot_spmv7_pipe_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int 
     const double* zt = smem + span;
     const int64_t rp0 = K.row0(t, ntiles);
     for (int j = threadIdx.x; j < kTile / 2; j += kThreads)
-      s7_tile_pair(K, ut, zt, zt + kTile, 2 * j, rp0 + 2 * j, n, swb, wout, bad);
+      s7_tile_pair(K, ut, zt, zt + kTile, 2 * j, rp0 + 2 * j, n, swb, wout, bad, nrm);
   }
   for (; t < ntiles; t += gridDim.x) {
     __syncthreads();           // w of tile t complete; tile t-1 fully consumed
@@ -338,7 +367,7 @@ mdot_spmv7_pipe_kernel(const double* __restrict__ X, int64_t ld, int64_t n, int 
       const int j0 = SLOTS == 1 ? 0 : c, j1 = SLOTS == 1 ? 2 : c + 1;
       for (int jj = j0; jj < j1; ++jj) {
         const int j = threadIdx.x + jj * kThreads;
-        s7_tile_pair(K, utn, ztn, ztn + kTile, 2 * j, rn0 + 2 * j, n, swn, wout, bad);
+        s7_tile_pair(K, utn, ztn, ztn + kTile, 2 * j, rn0 + 2 * j, n, swn, wout, bad, nrm);
       }
     };
 #pragma unroll
@@ -460,7 +489,12 @@ static int launch_k(Kern kern, bool pipe, int* occ_nx, int* occ, const lsb_arnol
 }
 
 template <int R, int SLOTS, int MINB>
-static int launch_t(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cudaStream_t st) {
+static int launch_t(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cudaStream_t st,
+                    bool norm) {
+  if (norm) {
+    static int nx = -1, occ = 0;
+    return launch_k(mdot_spmv7_kernel<R, SLOTS, 2, true>, false, &nx, &occ, S, K, p, it, st);
+  }
   if constexpr (MINB == 2 && SLOTS <= 8) {
     if (use_pipe(SLOTS)) {
       static int nx = -1, occ = 0;
@@ -472,24 +506,25 @@ static int launch_t(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cuda
 }
 
 template <int R>
-static int launch_r(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cudaStream_t st) {
+static int launch_r(const lsb_arnoldi& S, const Stencil7& K, int p, int it, cudaStream_t st,
+                    bool norm) {
   const int s = slots_for(p, R);
-  if (occ3(p)) {   // 3 CTAs/SM, at most 8 items per warp
-    if (s <= 1) return launch_t<R, 1, 3>(S, K, p, it, st);
-    if (s <= 2) return launch_t<R, 2, 3>(S, K, p, it, st);
-    if (s <= 4) return launch_t<R, 4, 3>(S, K, p, it, st);
-    return launch_t<R, 8, 3>(S, K, p, it, st);
+  if (occ3(p) && !norm) {   // 3 CTAs/SM, at most 8 items per warp
+    if (s <= 1) return launch_t<R, 1, 3>(S, K, p, it, st, norm);
+    if (s <= 2) return launch_t<R, 2, 3>(S, K, p, it, st, norm);
+    if (s <= 4) return launch_t<R, 4, 3>(S, K, p, it, st, norm);
+    return launch_t<R, 8, 3>(S, K, p, it, st, norm);
   }
-  if (s <= 1) return launch_t<R, 1, 2>(S, K, p, it, st);
-  if (s <= 2) return launch_t<R, 2, 2>(S, K, p, it, st);
-  if (s <= 4) return launch_t<R, 4, 2>(S, K, p, it, st);
-  if (s <= 8) return launch_t<R, 8, 2>(S, K, p, it, st);
-  if (s <= 13) return launch_t<R, 13, 2>(S, K, p, it, st);
-  return launch_t<R, 16, 2>(S, K, p, it, st);
+  if (s <= 1) return launch_t<R, 1, 2>(S, K, p, it, st, norm);
+  if (s <= 2) return launch_t<R, 2, 2>(S, K, p, it, st, norm);
+  if (s <= 4) return launch_t<R, 4, 2>(S, K, p, it, st, norm);
+  if (s <= 8) return launch_t<R, 8, 2>(S, K, p, it, st, norm);
+  if (s <= 13) return launch_t<R, 13, 2>(S, K, p, it, st, norm);
+  return launch_t<R, 16, 2>(S, K, p, it, st, norm);
 }
 
 int launch_lagged_reduce_spmv7(const lsb_arnoldi& S, const lsb_stencil* A, int it, int p,
-                               cudaStream_t st, const lsb_halo_wait* hw) {
+                               cudaStream_t st, const lsb_halo_wait* hw, bool norm) {
   if (!canonical7(A) || A->nx > kTile) return LSB_EINVAL;
   if ((int64_t)A->nx * A->ny * A->nz != S.n || (S.n & 1) || p < 1 || p > 128 || p + 1 > S.cap)
     return LSB_ERANGE;
@@ -533,11 +568,11 @@ int launch_lagged_reduce_spmv7(const lsb_arnoldi& S, const lsb_stencil* A, int i
     K.timeout_ns = hw->timeout_ns;
     K.wflags = hw->flags;
   }
-  switch (occ3(p) ? choose_parts(p, 8) : choose_parts(p)) {
-    case 8: return launch_r<8>(S, K, p, it, st);
-    case 4: return launch_r<4>(S, K, p, it, st);
-    case 2: return launch_r<2>(S, K, p, it, st);
-    default: return launch_r<1>(S, K, p, it, st);
+  switch (occ3(p) && !norm ? choose_parts(p, 8) : choose_parts(p)) {
+    case 8: return launch_r<8>(S, K, p, it, st, norm);
+    case 4: return launch_r<4>(S, K, p, it, st, norm);
+    case 2: return launch_r<2>(S, K, p, it, st, norm);
+    default: return launch_r<1>(S, K, p, it, st, norm);
   }
 }
 

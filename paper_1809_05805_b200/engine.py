@@ -576,10 +576,7 @@ class Engine:
                 # (max|z|, sum z^2) after them: fused_mdot_norm's reduction
                 if self.comm is not None and self.halo:
                     self.comm.halo(self.Vstore[i - 1], self.off, self.n, self.halo)
-                self._call("lsb_lagged_reduce_spmv7", S, C.byref(self.op.c), i, p, st)
-                self._call("lsb_norm_partial", self.col_ptr(i), self.n,
-                           C.c_void_p(self.Gloc.data_ptr() + 8 * 2 * p), self.ws.ref(),
-                           D.ptr(self.flags), i, st)
+                self._call("lsb_lagged_reduce_spmv7_norm", S, C.byref(self.op.c), i, p, st)
                 self._gather(2 * p + 2)
                 self._call("lsb_ghysels_small_pairs", S, i, i, p, st)
                 self._call("lsb_cgs_project", S, i, i, p, 2, st)   # + q = z / h
@@ -666,12 +663,17 @@ class Engine:
                         # ranks sharing a device (in-process emulation) spin
                         # on each other's exchange kernels: no device-wide
                         # synchronize (torch.cuda.graph's entry does one), and
-                        # capture errors only for this thread
+                        # capture errors only for this thread.  Every rank
+                        # captures and instantiates between two barriers: the
+                        # instantiation may wait for the device, which must
+                        # not hold a kernel spinning on a rank still capturing
+                        self.comm.barrier()
                         self.graph.capture_begin(capture_error_mode="thread_local")
                         try:
                             self.enqueue_cycle()
                         finally:
                             self.graph.capture_end()
+                        self.comm.barrier()
                 torch.cuda.current_stream().wait_stream(side)
             self.graph.replay()
         else:
