@@ -228,10 +228,68 @@ __device__ __forceinline__ void load27_lines(const double* __restrict__ x, int64
   }
 }
 
-__global__ void __launch_bounds__(kS27Threads)
+// Interior march (both x and y neighbours present, every plane of the chunk
+// has its z-1 and z+1 planes): the same products and order as box27_pair's
+// interior case, with no per-plane dispatch or presence predicates, and the
+// three plane buffers rotated by unrolling the plane loop by three instead of
+// copying six lines of registers per plane (those moves were a fifth of the
+// generic march's instructions).
+template <class Cf>
+__device__ __forceinline__ void march27_interior(const double* __restrict__ x,
+                                                 const double* __restrict__ b,
+                                                 double* __restrict__ y, int64_t r00, int64_t nx,
+                                                 int64_t plane, int z0, int z1, const Cf& cf,
+                                                 bool& bad) {
+  double A[3][4], B[3][4], Q[3][4];
+  auto load = [&](double (&d)[3][4], int64_t r) {
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      const double* base = x + r + dy * nx;
+      const double2 c2 = __ldg(reinterpret_cast<const double2*>(base));
+      d[dy + 1][0] = __ldg(base - 1);
+      d[dy + 1][1] = c2.x;
+      d[dy + 1][2] = c2.y;
+      d[dy + 1][3] = __ldg(base + 2);
+    }
+  };
+  auto step = [&](const double (&m)[3][4], const double (&c)[3][4], double (&p)[3][4], int iz) {
+    const int64_t r = r00 + (int64_t)iz * plane;
+    load(p, r + plane);
+    auto g0 = [&](int o) {
+      const int l = o / 3, k = o % 3;
+      return l < 3 ? m[l][k] : (l < 6 ? c[l - 3][k] : p[l - 6][k]);
+    };
+    auto g1 = [&](int o) {
+      const int l = o / 3, k = o % 3 + 1;
+      return l < 3 ? m[l][k] : (l < 6 ? c[l - 3][k] : p[l - 6][k]);
+    };
+    const double y0 = box27_row<3, 3, 3>(g0, cf);
+    const double y1 = box27_row<3, 3, 3>(g1, cf);
+    if (!isfinite(y0) || !isfinite(y1)) bad = true;
+    double2 out;
+    if (b) {
+      const double2 bb = *reinterpret_cast<const double2*>(b + r);
+      out = make_double2(__dsub_rn(bb.x, y0), __dsub_rn(bb.y, y1));
+    } else {
+      out = make_double2(y0, y1);
+    }
+    *reinterpret_cast<double2*>(y + r) = out;
+  };
+  load(A, r00 + (int64_t)(z0 - 1) * plane);
+  load(B, r00 + (int64_t)z0 * plane);
+  for (int iz = z0; iz < z1; iz += 3) {
+    step(A, B, Q, iz);
+    if (iz + 1 >= z1) break;
+    step(B, Q, A, iz + 1);
+    if (iz + 2 >= z1) break;
+    step(Q, A, B, iz + 2);
+  }
+}
+
+__global__ void __launch_bounds__(kS27Threads, 4)
 stencil27_march_kernel(const StencilK K, FastDiv fint, const double* __restrict__ x,
                        const double* __restrict__ b, double* __restrict__ y, lsb_flags* flags,
-                       int it, int nzc) {
+                       int it, int nzc, int tuning_fast27) {
   if (gated_off(flags, it)) return;
   // work items: (z chunk, line in plane, pair slot); interior pairs of the
   // line first (one shared plan), then the two x-edge pairs -- as the pair
@@ -264,8 +322,12 @@ stencil27_march_kernel(const StencilK K, FastDiv fint, const double* __restrict_
     const int z1 = min(K.nz, z0 + kS27MarchZ);
     const int sy = ((int)iy >= 1) | (((int)iy + 1 < K.ny) << 1);
     const bool xm = ix >= 1, xp = ix + 2 < K.nx;
-    double v[9][4];
     const int64_t r00 = (int64_t)iy * nx + ix;       // row of (ix, iy) in plane 0
+    if (xm && xp && sy == 3 && z0 - 1 >= K.zlo && z1 <= K.zhi && tuning_fast27) {
+      march27_interior(x, b, y, r00, nx, plane, z0, z1, cf, bad);
+      continue;
+    }
+    double v[9][4];
     // lines of planes z0-1 (dz = -1) and z0 (dz = 0)
     load27_lines(x, r00 + (int64_t)(z0 - 1) * plane, nx, sy, z0 - 1 >= K.zlo, xm, xp, v, 0);
     load27_lines(x, r00 + (int64_t)z0 * plane, nx, sy, true, xm, xp, v, 3);
@@ -433,8 +495,8 @@ int launch_stencil(const lsb_stencil* S, const double* x, const double* b, doubl
       int64_t gm = (items + kS27Threads - 1) / kS27Threads;
       if (gm > (int64_t)sm_count() * occm) gm = (int64_t)sm_count() * occm;
       if (gm < 1) gm = 1;
-      stencil27_march_kernel<<<(unsigned)gm, kS27Threads, 0, st>>>(K, fint, x, b, y, flags, it,
-                                                                   nzc);
+      stencil27_march_kernel<<<(unsigned)gm, kS27Threads, 0, st>>>(
+          K, fint, x, b, y, flags, it, nzc, tuning(LSB_TUNE_S27_MARCH) != 3);
       return check_launch("stencil27_march");
     }
     stencil27_pair_kernel<<<(unsigned)gp, kS27Threads, 0, st>>>(K, fint, x, b, y, flags, it);
