@@ -275,12 +275,14 @@ int launch_k3_rows(const lsb_arnoldi& S, int it, int p, int ks, int direct, cuda
 int k3_tile_rows(int p) {
   if (p < 1 || p + 1 > kMaxK3Cols) return 0;
   const int forced = tuning(LSB_TUNE_K3_ROWS);
-  if ((forced == 64 || forced == 128 || forced == 256 ||
+  if ((forced == 64 || forced == 128 || forced == 192 || forced == 256 ||
        ((forced == 512 || forced == 1024) && p <= 32)) &&
       k3_stages(p, forced) >= 2)
     return forced;
-  for (int T = 1024; T >= 128; T /= 2)
+  for (int T = 1024; T >= 128; T /= 2) {
     if ((T <= 256 || p <= 32) && k3_half_fits(p, T)) return T;
+    if (T == 256 && k3_half_fits(p, 192) && tuning(LSB_TUNE_K3_ROWS) != 128) return 192;
+  }
   if (k3_stages(p, 128) >= 2) return 128;
   return k3_stages(p, 64) >= 2 ? 64 : 0;
 }
@@ -294,6 +296,7 @@ int launch_lagged_update_reduce(const lsb_arnoldi& S, int it, int p, int ks, int
     case 1024: return launch_k3_rows<1024>(S, it, p, ks, direct, st);
     case 512: return launch_k3_rows<512>(S, it, p, ks, direct, st);
     case 256: return launch_k3_rows<256>(S, it, p, ks, direct, st);
+    case 192: return launch_k3_rows<192>(S, it, p, ks, direct, st);
     case 128: return launch_k3_rows<128>(S, it, p, ks, direct, st);
     case 64: return launch_k3_rows<64>(S, it, p, ks, direct, st);
     default: return LSB_ERANGE;

@@ -690,11 +690,13 @@ def test_fused_spmv_k1_matches_unfused(P, p):
 
 
 @pytest.mark.parametrize("p,n", [(1, 4096), (2, 70_001), (7, 65_536), (26, 300_001),
-                                 (51, 1 << 20), (60, 99_999), (101, 200_000), (109, 5_000)])
+                                 (30, 250_001), (35, 1 << 20), (51, 1 << 20), (60, 99_999),
+                                 (101, 200_000), (109, 5_000)])
 def test_fused_update_reduce_matches_unfused(P, p, n):
     """K3 (two-sync first projection + second reduction in one pass): u and w
     bit for bit lagged_update's, Q^T w equal to K1's up to the reduction
-    tree -- every tile width (1024..128 rows), ragged and odd n."""
+    tree -- every tile width (1024..128 rows, 192 at 27 <= p <= 35), ragged
+    and odd n."""
     import ctypes as C
     from paper_1809_05805_b200 import _abi
     from paper_1809_05805_b200 import _dev as D
