@@ -17,7 +17,7 @@ eng.Vstore[:, :n].normal_(generator=torch.Generator(device="cuda").manual_seed(0
 eng.flags.copy_(torch.tensor([_abi.NO_STOP, 0, -1, 0, 0, 0, 0, 0], dtype=torch.int32))
 st, S = D.stream(), eng.Sref
 tot = {"pipe": 0.0, "old": 0.0, "k1": 0.0}
-for p in (2, 5, 8, 13, 20, 26, 33, 40, 51):
+for p in [int(v) for v in os.environ.get("KPIPE_PS", "2,5,8,13,20,26,33,40,51").split(",")]:
     res = {}
     for name, knob in (("pipe", 1), ("old", 2)):
         lib.lsb_set_tuning(_abi.TUNE_FUSED_PIPE, knob)
