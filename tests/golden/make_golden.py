@@ -199,6 +199,17 @@ def ghysels():
     _save("ghysels.npz", **out)
 
 
+def ghysels3d():
+    """cgs1_ghysels on the 3D 7-point N=32 problem of laplace3d32.npz
+    (GMRES(50), tol 1e-6): the case where the device fuses the Ghysels
+    step's SpMV and norm into its reduction (7-point stencil)."""
+    A = _ref_csr(orc.laplace3d(32))
+    b = ls.gen_rhs("random", A, 42)
+    r = _run(A, b, "cgs1_ghysels", 50, 50, 1e-6)
+    print("L3D32 cgs1_ghysels", len(r["curve"]), r["outcome"])
+    _save("laplace3d32_ghysels.npz", **{f"cgs1_ghysels__{k}": v for k, v in r.items()})
+
+
 def extras():
     """true_residual_every probes (gmres.py:273-283)."""
     out = {}
@@ -288,6 +299,8 @@ if __name__ == "__main__":
         extras()
     elif what == "ghysels":
         ghysels()
+    elif what == "ghysels3d":
+        ghysels3d()
     elif what == "c2":
         big_c2(int(sys.argv[2]) if len(sys.argv) > 2 else 256)
     elif what == "l3d64":

@@ -41,11 +41,13 @@ def _rank(comm, dims, meth, m, restarts, tol):
 
 @pytest.mark.parametrize("ranks,meth", [(2, "one_sync_mgs"), (4, "one_sync_mgs"),
                                         (2, "two_sync_cgs2"), (2, "mgs_l1"), (2, "cgs2"),
-                                        (3, "pipeline2"), (8, "one_sync_mgs")])
+                                        (3, "pipeline2"), (8, "one_sync_mgs"),
+                                        (2, "cgs1_ghysels"), (4, "cgs1_ghysels")])
 @pytest.mark.parametrize("peer", [False, True], ids=["threadcomm", "peer"])
 def test_slab_partition_reproduces_reference(P, ranks, meth, peer):
     from paper_1809_05805_b200.parallel import run_threads
-    G = np.load(os.path.join(GOLD, "laplace3d32.npz"))
+    G = np.load(os.path.join(GOLD, "laplace3d32_ghysels.npz" if meth == "cgs1_ghysels"
+                             else "laplace3d32.npz"))
     out = run_threads(ranks, _rank, (32, 32, 32), meth, 50, 50, 1e-6, peer=peer)
     c0 = out[0][1]
     for r in range(1, ranks):   # replicated small state: identical on every rank
@@ -53,7 +55,8 @@ def test_slab_partition_reproduces_reference(P, ranks, meth, peer):
         assert out[r][3] == out[0][3]
     cr = G[meth + "__curve"]
     assert len(c0) == len(cr)
-    assert np.max(np.abs(c0 - cr) / cr) <= 1e-10
+    # Ghysels' Pythagorean residual loses digits as the radicand shrinks: 1e-7
+    assert np.max(np.abs(c0 - cr) / cr) <= (1e-7 if meth == "cgs1_ghysels" else 1e-10)
     assert out[0][2] == str(G[meth + "__outcome"])
     assert out[0][5] == list(G[meth + "__cycle_starts"])
     assert [e[1] for e in out[0][3]] == list(G[meth + "__ev_kind"])

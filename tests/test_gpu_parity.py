@@ -473,6 +473,24 @@ def test_laplace3d32_history(P, meth):
     _check(h, led, G, meth)
 
 
+@pytest.mark.parametrize("fuse", ["1", "0"], ids=["fused", "unfused"])
+def test_laplace3d32_ghysels_history(P, monkeypatch, fuse):
+    """cgs1_ghysels on the 7-point stencil, where the step's SpMV and
+    fused_mdot_norm run as one kernel (pair layout + norm entries) and the
+    division rides on the projection, against the reference's own run
+    (make_golden.py ghysels3d); LSB_FUSE_DIRECT=0 takes the unfused kernels."""
+    from paper_1809_05805_b200.engine import Engine
+    monkeypatch.setenv("LSB_FUSE_DIRECT", fuse)
+    G = _load("laplace3d32_ghysels.npz")
+    A = P.gen_laplace3d(32)
+    assert Engine(A, 50, "cgs1_ghysels", 1e-6, use_graph=False).fused7_ghysels == (fuse == "1")
+    b = P.gen_rhs("random", A, 42)
+    x, h, led = _solve(P, A, b, "cgs1_ghysels", 50, 50, 1e-6)
+    _check(h, led, G, "cgs1_ghysels", tol=1e-7)    # Ghysels' bar (Pythagorean residual)
+    xr = G["cgs1_ghysels__x"]
+    assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+
+
 @pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2", "mgs_l1", "cgs2"])
 def test_convdiff27_history_and_orthogonality(P, meth):
     G = _load("convdiff27_16.npz")

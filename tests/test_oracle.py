@@ -123,6 +123,16 @@ def test_laplace3d_small_history(meth):
     _check_run(run, G, meth)
 
 
+def test_laplace3d_small_ghysels_history():
+    G = _load("laplace3d32_ghysels.npz")
+    A = orc.laplace3d(32)
+    b = orc.rhs_random(A.n_rows, 42)
+    run = orc.gmres(A, b, "cgs1_ghysels", 50, 50, 1e-6)
+    # the Pythagorean residual sqrt(|z|^2 - |y|^2) loses digits as the
+    # radicand shrinks (1.7e-9 here; the device bar for Ghysels is 1e-7)
+    _check_run(run, G, "cgs1_ghysels", exact_curve_tol=1e-8)
+
+
 @pytest.mark.parametrize("meth", ["one_sync_mgs", "two_sync_cgs2", "mgs_l1", "cgs2"])
 def test_convdiff27_small_history(meth):
     G = _load("convdiff27_16.npz")
