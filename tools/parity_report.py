@@ -79,6 +79,11 @@ def main():
     for meth in ("one_sync_mgs", "two_sync_cgs2", "mgs_l1", "cgs2", "pipeline2"):
         h, led, dt = run(A, b, meth, 50, 50, 1e-6)
         rows.append(row("3D 7-pt 32^3 GMRES(50)", meth, G, h, led, None, dt))
+    G = np.load(os.path.join(GOLD, "laplace3d32_ghysels.npz"))
+    for tag, env in ((" SpMV+norm fused", {}), (" unfused", {"LSB_FUSE_DIRECT": "0"})):
+        h, led, dt = run(A, b, "cgs1_ghysels", 50, 50, 1e-6, env)
+        rows.append(row("3D 7-pt 32^3 GMRES(50) (bar 1e-7)" + tag, "cgs1_ghysels", G, h, led,
+                        None, dt))
     G = np.load(os.path.join(GOLD, "laplace3d64.npz"))
     A = P.gen_laplace3d(64)
     b = P.gen_rhs("random", A, 42)
