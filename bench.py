@@ -452,7 +452,11 @@ def _bench_core(args, comm, world, rank, local, comm_kind=None):
     # e2e through the public API with host buffers: solve() on one GPU,
     # solve_distributed() per rank (each rank uploads its b rows, downloads x)
     cfg = P.GmresConfig(restart_m=M, max_restarts=1, rel_tol=1e-14, method="one_sync_mgs")
-    b_host = np.ascontiguousarray(b_local)
+    # the step's input from pinned host memory (a numpy view of a page-locked
+    # buffer, as a serving process would keep its request buffers)
+    b_pin = torch.empty(len(b_local), dtype=torch.float64).pin_memory()
+    b_host = b_pin.numpy()
+    b_host[:] = b_local
 
     def e2e_once():
         if comm is None:
@@ -481,7 +485,8 @@ def _bench_core(args, comm, world, rank, local, comm_kind=None):
                      "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                      "steps": e2e_steps,
                      "what": "solve(A, b_host) -> x_host (per rank: solve_distributed), "
-                             "GmresConfig(50, 1 cycle); bytes per rank; after 2 untimed calls "
+                             "b_host a numpy view of pinned host memory, x_host a fresh numpy "
+                             "array; GmresConfig(50, 1 cycle); bytes per rank; after 2 untimed calls "
                              "(engine build, cycle-graph capture: reused by every later call "
                              "on the same operator)"}
     if world == 1 and not args.no_cpu and rank == 0 and not args.strong:

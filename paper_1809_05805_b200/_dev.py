@@ -179,6 +179,13 @@ def h2d(a, dev):
     n = a.size
     src = torch.from_numpy(a)
     out = torch.empty(n, dtype=F64, device=dev)
+    if src.is_pinned():
+        # the caller's array already sits in page-locked memory (e.g. a
+        # numpy view of a pinned torch tensor): one DMA, no staging memcpy.
+        # Stream-ordered before every kernel that reads it; the solve
+        # synchronises before returning, so `a` is free again by then.
+        out.copy_(src, non_blocking=True)
+        return out
     bufs = _staging()
     for i, lo in enumerate(range(0, n, _CHUNK)):
         hi = min(n, lo + _CHUNK)

@@ -1105,6 +1105,21 @@ def test_persistent_cycle_is_used_at_launch_bound_sizes(P):
     assert not Engine(A, 30, "two_sync_cgs2", 1e-6).persistent
 
 
+def test_pinned_host_input_takes_one_dma(P):
+    """b handed over as a numpy view of page-locked memory is copied with one
+    DMA (no staging); the solve is bitwise the pageable-input solve."""
+    A = P.gen_laplace3d(48)                      # n = 110,592 > the staging threshold
+    b = P.gen_rhs("random", A, 42)
+    pin = torch.empty(b.size, dtype=torch.float64).pin_memory()
+    bp = pin.numpy()
+    bp[:] = b
+    assert torch.from_numpy(bp).is_pinned()
+    cfg = P.GmresConfig(restart_m=30, max_restarts=3, rel_tol=1e-8)
+    x1, h1 = P.solve(A, b, config=cfg, diagnostics_every=0)
+    x2, h2 = P.solve(A, bp, config=cfg, diagnostics_every=0)
+    assert np.array_equal(x1, x2) and np.array_equal(h1.implicit_curve(), h2.implicit_curve())
+
+
 def test_repeated_solves_reuse_the_engine(P):
     """solve() on the same operator object and config reuses the engine
     (storage + captured cycle graph) when the previous history no longer
