@@ -28,6 +28,7 @@ TUNE_K3_ROWS, TUNE_K3_STAGES, TUNE_CSR_THREAD_ROW = 4, 5, 6
 TUNE_PERSIST_TRACE, TUNE_PERSIST_CTAS, TUNE_FUSED_PIPE, TUNE_CSR_DICT, TUNE_PDL = 7, 8, 9, 10, 11
 TUNE_PERSIST_TIMEOUT_S = 12
 TUNE_GRID_OCC, TUNE_GRID_TRACE, TUNE_S27_MARCH, TUNE_MGS1_GRID = 13, 14, 15, 16
+TUNE_S27_TILE_Z = 17
 
 
 class LsbUnavailable(RuntimeError):

@@ -16,6 +16,8 @@
 // with 32-bit indices: a warp stages the products of 32 consecutive rows in
 // shared memory from coalesced col/value streams, then every lane sums its
 // own row in numpy's order.
+#include <cuda.h>
+
 #include "tile.cuh"
 
 namespace lsb {
@@ -355,6 +357,267 @@ stencil27_march_kernel(const StencilK K, FastDiv fint, const double* __restrict_
   if (bad && flags) flags->nonfinite = 1;
 }
 
+// ---------------------------------------------------------------- 27-point plane tiles (TMA)
+// A CTA owns a 32 x 16 (x, y) tile of rows and marches a chunk of planes.
+// Each plane's tile plus its one-row halo (36 x 18 doubles) lands in shared
+// memory by ONE 3-D tensor copy (cp.async.bulk.tensor, OOB zero-filled --
+// absent neighbours are never read by the row plans, so the fill value does
+// not matter), issued `kT27Stages` planes ahead into a ring: the plane loads
+// never sit on a thread's critical path (the z-march kernel above stalls on
+// them: ncu long-scoreboard 4.4 of 8.6 cycles per instruction).  A thread
+// owns one row pair (ix, ix+1) of the tile and keeps the (dz, dy) lines of
+// the previous two planes in registers, so each step reads only the new
+// plane's three lines from shared memory (8 + 16 + 8 bytes per line).
+// Products, plans and summation order are box27_pair's: y is bitwise the
+// same as every other 27-point kernel.  NEG: the 20 edge/corner
+// coefficients are exactly -1.0, so their products are exact negations
+// folded into the DADDs (the same bits as __dmul_rn(-1.0, x)): 7 DMUL + 26
+// DADD per interior row instead of 27 + 26.
+constexpr int kT27X = 32, kT27Y = 16;
+constexpr int kT27Threads = (kT27X / 2) * kT27Y;                  // 256: one row pair each
+// a tensor copy's inner start must be 16-byte aligned (an odd x start traps
+// with an illegal instruction -- tools/micro/tma3d.cu), so a smem row holds
+// x0-2 .. x0+33 and a pair reads its four x values as 8 + 16 + 8 bytes
+constexpr int kT27RowD = kT27X + 4;
+constexpr int kT27PlaneB = kT27RowD * (kT27Y + 2) * 8;            // 5184 B per staged plane
+constexpr int kT27PlaneD = (kT27PlaneB + 127) / 128 * 128 / 8;    // 128-byte aligned slots
+constexpr int kT27Stages = 6;
+constexpr size_t kT27Smem = (size_t)kT27Stages * kT27PlaneD * 8 + 128 + kT27Stages * 8;
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__host__ __device__ constexpr bool box27_face_or_centre(int o) {
+  return o == 4 || o == 10 || o == 12 || o == 13 || o == 14 || o == 16 || o == 22;
+}
+
+// The rows of the 27-point box with at least one neighbour missing, as row
+// pairs (ix even): the two x-edge pairs of every line, the y-edge lines'
+// x-interior pairs, and the x/y-interior pairs of a z-edge plane (one with
+// no neighbour plane below / above, i.e. no ghost plane there).  A
+// grid-stride loop of the calling CTAs, row-pair kernel style (global
+// loads, box27_pair): ~3% of the rows at 256^3.
+__device__ __forceinline__ void stencil27_boundary_rows(const StencilK& K, const double* __restrict__ x,
+                                                     const double* __restrict__ b,
+                                                     double* __restrict__ y, lsb_flags* flags,
+                                                     unsigned cta, unsigned ctas) {
+  const int64_t nx = K.nx, plane = (int64_t)K.nx * K.ny;
+  const uint32_t nxi = (uint32_t)(K.nx / 2 - 2);               // x-interior pairs per line
+  const uint32_t nX = 2u * (uint32_t)K.ny * (uint32_t)K.nz;
+  const uint32_t nyl = K.ny >= 2 ? 2u : 1u;                     // y-edge lines per plane
+  const uint32_t nY = nyl * (uint32_t)K.nz * nxi;
+  const int zb0 = K.zlo == 0 ? 0 : -1;                          // z-edge planes (-1: none)
+  const int zb1 = (K.zhi == K.nz - 1 && K.nz - 1 != zb0) ? K.nz - 1 : -1;
+  const uint32_t nzp = (zb0 >= 0) + (zb1 >= 0);
+  const uint32_t lyi = K.ny >= 2 ? (uint32_t)(K.ny - 2) : 0u;   // y-interior lines
+  const uint32_t nZ = nzp * lyi * nxi;
+  auto cf = [&](int o) { return K.val[o]; };
+  bool bad = false;
+  for (uint32_t i = cta * blockDim.x + threadIdx.x; i < nX + nY + nZ; i += ctas * blockDim.x) {
+    int ix, iy, iz;
+    if (i < nX) {
+      const uint32_t line = i >> 1;
+      ix = (i & 1) ? K.nx - 2 : 0;
+      iz = (int)(line / (uint32_t)K.ny);
+      iy = (int)(line - (uint32_t)iz * K.ny);
+    } else if (i < nX + nY) {
+      const uint32_t e = i - nX, q = e / nxi;
+      ix = 2 + 2 * (int)(e - q * nxi);
+      iz = (int)(q / nyl);
+      iy = (q - (uint32_t)iz * nyl) ? K.ny - 1 : 0;
+    } else {
+      const uint32_t e = i - nX - nY, q = e / nxi;
+      ix = 2 + 2 * (int)(e - q * nxi);
+      const uint32_t pz = q / lyi;
+      iy = 1 + (int)(q - pz * lyi);
+      iz = (pz == 0 && zb0 >= 0) ? zb0 : zb1;
+    }
+    const int64_t r = (int64_t)iz * plane + (int64_t)iy * nx + ix;
+    const int sy = (iy >= 1) | ((iy + 1 < K.ny) << 1);
+    const int sz = (iz - 1 >= K.zlo) | ((iz + 1 <= K.zhi) << 1);
+    const bool xm = ix >= 1, xp = ix + 2 < K.nx;
+    double v[9][4];
+    load27_pair(x, r, nx, plane, sy, sz, xm, xp, v);
+    double y0, y1;
+    box27_pair(v, sy, sz, xm, xp, cf, y0, y1);
+    if (!isfinite(y0) || !isfinite(y1)) bad = true;
+    double2 out;
+    if (b) {
+      const double2 bb = __ldg(reinterpret_cast<const double2*>(b + r));
+      out = make_double2(__dsub_rn(bb.x, y0), __dsub_rn(bb.y, y1));
+    } else {
+      out = make_double2(y0, y1);
+    }
+    *reinterpret_cast<double2*>(y + r) = out;
+  }
+  if (bad && flags) flags->nonfinite = 1;
+}
+
+template <bool NEG>
+__global__ void __launch_bounds__(kT27Threads, 2)
+stencil27_tile_kernel(const __grid_constant__ CUtensorMap tm, const StencilK K,
+                      const double* __restrict__ x, const double* __restrict__ b,
+                      double* __restrict__ y, lsb_flags* flags, int it, int zc, int tiles_x) {
+  if (gated_off(flags, it)) return;
+  if (blockIdx.y == 0) {                 // the boundary rows (first, so they are not a tail)
+    stencil27_boundary_rows(K, x, b, y, flags, blockIdx.x, gridDim.x);
+    return;
+  }
+  // all shared memory dynamic, the plane slots 128-byte aligned by hand (the
+  // tensor copy's destination alignment); offsetting the shared array itself
+  // (not a cast integer) keeps the reads LDS rather than generic loads
+  extern __shared__ __align__(128) double t27_raw[];
+  double* const t27_smem = t27_raw + ((128u - (smem_u32(t27_raw) & 127u)) & 127u) / 8u;
+  uint64_t* const full = reinterpret_cast<uint64_t*>(t27_smem + kT27Stages * kT27PlaneD);
+  const int tx = (int)blockIdx.x % tiles_x, ty = (int)blockIdx.x / tiles_x;
+  const int z0 = ((int)blockIdx.y - 1) * zc, z1 = min(K.nz, z0 + zc);
+  const int x0 = tx * kT27X, y0 = ty * kT27Y;
+  const int lx = 2 * ((int)threadIdx.x & 15), ly = (int)threadIdx.x >> 4;
+  const int ix = x0 + lx, iy = y0 + ly;
+  const int nload = z1 - z0 + 2;                           // planes z0-1 .. z1
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < kT27Stages; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int k) {                                 // load k = plane z0-1+k
+    uint64_t* bar = &full[k % kT27Stages];
+    mbar_arrive_tx(bar, (unsigned)kT27PlaneB);
+    tma_load_3d(t27_smem + (k % kT27Stages) * kT27PlaneD, &tm, x0 - 2, y0 - 1,
+                z0 - 1 + k - K.zlo, bar);
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kT27Stages && k < nload; ++k) issue(k);
+  auto read = [&](double (&d)[3][4], int k) {
+    mbar_wait(&full[k % kT27Stages], (unsigned)(k / kT27Stages) & 1u);
+    const double* row = t27_smem + (k % kT27Stages) * kT27PlaneD + ly * kT27RowD + lx + 1;
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const double2 c = *reinterpret_cast<const double2*>(row + l * kT27RowD + 1);
+      d[l][0] = row[l * kT27RowD];
+      d[l][1] = c.x; d[l][2] = c.y;
+      d[l][3] = row[l * kT27RowD + 3];
+    }
+  };
+  // the slot of load t is free once every thread has read load t+2 and
+  // finished step t (the generic path reads nothing from shared memory)
+  auto release = [&](int t) {
+    __syncthreads();
+    if (threadIdx.x == 0 && t + kT27Stages < nload) issue(t + kT27Stages);
+  };
+  const int64_t nx = K.nx, plane = (int64_t)K.nx * K.ny;
+  bool bad = false;
+  auto emit = [&](int iz, double y0v, double y1v) {
+    if (!isfinite(y0v) || !isfinite(y1v)) bad = true;
+    const int64_t r = (int64_t)iz * plane + (int64_t)iy * nx + ix;
+    double2 out;
+    if (b) {
+      const double2 bb = __ldg(reinterpret_cast<const double2*>(b + r));
+      out = make_double2(__dsub_rn(bb.x, y0v), __dsub_rn(bb.y, y1v));
+    } else {
+      out = make_double2(y0v, y1v);
+    }
+    *reinterpret_cast<double2*>(y + r) = out;
+  };
+  auto mul = [&](int o, double v) {
+    if (NEG && !box27_face_or_centre(o)) return -v;
+    return __dmul_rn(K.val[o], v);
+  };
+  // interior rows only (all 26 neighbours present: the fixed interior plan,
+  // plane buffers rotated by a 3-way unrolled loop -- no register moves);
+  // the boundary rows are the blockIdx.y == 0 CTAs' work
+  const bool xy_int = ix >= 1 && ix + 2 < K.nx && iy >= 1 && iy + 1 < K.ny;
+  double A[3][4], B[3][4], Q[3][4];
+  auto step = [&](const double (&m)[3][4], const double (&c)[3][4], double (&p)[3][4], int t) {
+    read(p, t + 2);
+    const int iz = z0 + t;
+    if (xy_int && iz - 1 >= K.zlo && iz + 1 <= K.zhi) {
+      constexpr Box27Plan P = box27_plan(3, 3, 3);
+      double q0[27], q1[27];
+#pragma unroll
+      for (int j = 0; j < 27; ++j) {
+        const int o = P.idx[j], l = o / 3, k = o % 3;
+        const double v0 = l < 3 ? m[l][k] : (l < 6 ? c[l - 3][k] : p[l - 6][k]);
+        const double v1 = l < 3 ? m[l][k + 1] : (l < 6 ? c[l - 3][k + 1] : p[l - 6][k + 1]);
+        q0[j] = mul(o, v0);
+        q1[j] = mul(o, v1);
+      }
+      emit(iz, np_row_sum_fixed<27>(q0), np_row_sum_fixed<27>(q1));
+    }
+    release(t);
+  };
+  read(A, 0);
+  read(B, 1);
+  const int nt = z1 - z0;
+  for (int t = 0; t < nt; t += 3) {
+    step(A, B, Q, t);
+    if (t + 1 >= nt) break;
+    step(B, Q, A, t + 1);
+    if (t + 2 >= nt) break;
+    step(Q, A, B, t + 2);
+  }
+  if (bad && flags) flags->nonfinite = 1;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the
+// library links no libcuda).
+typedef CUresult (*t27_encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static t27_encode_fn t27_encoder() {
+  static t27_encode_fn f = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return (t27_encode_fn) nullptr;
+    return reinterpret_cast<t27_encode_fn>(p);
+  }();
+  return f;
+}
+
+// Launch the tile kernel; returns false (nothing launched) when the tensor
+// map cannot be encoded, so the caller falls back to the z-march.
+static bool launch_stencil27_tile(const StencilK& K, const double* x, const double* b, double* y,
+                                  lsb_flags* flags, int it, cudaStream_t st) {
+  t27_encode_fn enc = t27_encoder();
+  if (!enc) return false;
+  const int64_t plane = (int64_t)K.nx * K.ny;
+  const int nplanes = K.zhi - K.zlo + 1;
+  CUtensorMap tm;
+  const cuuint64_t dims[3] = {(cuuint64_t)K.nx, (cuuint64_t)K.ny, (cuuint64_t)nplanes};
+  const cuuint64_t strides[2] = {(cuuint64_t)K.nx * 8, (cuuint64_t)plane * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)kT27RowD, (cuuint32_t)(kT27Y + 2), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(x + (int64_t)K.zlo * plane), dims,
+          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  bool neg = true;
+  for (int o = 0; o < 27; ++o)
+    if (!box27_face_or_centre(o) && K.val[o] != -1.0) neg = false;
+  const int tiles_x = (K.nx + kT27X - 1) / kT27X, tiles_y = (K.ny + kT27Y - 1) / kT27Y;
+  int zc = tuning(LSB_TUNE_S27_TILE_Z);
+  if (zc <= 0) zc = 32;
+  const int nch = (K.nz + zc - 1) / zc;
+  const dim3 grid((unsigned)(tiles_x * tiles_y), (unsigned)nch + 1);   // y = 0: boundary rows
+  if (neg)
+    stencil27_tile_kernel<true><<<grid, kT27Threads, kT27Smem, st>>>(tm, K, x, b, y, flags, it,
+                                                                      zc, tiles_x);
+  else
+    stencil27_tile_kernel<false><<<grid, kT27Threads, kT27Smem, st>>>(tm, K, x, b, y, flags, it,
+                                                                       zc, tiles_x);
+  return true;
+}
+
 static bool canonical27(const lsb_stencil* S) {
   if (S->noff != 27) return false;
   for (int o = 0; o < 27; ++o)
@@ -484,7 +747,10 @@ int launch_stencil(const lsb_stencil* S, const double* x, const double* b, doubl
     if (gp > (int64_t)sm_count() * occ27p) gp = (int64_t)sm_count() * occ27p;
     if (gp < 1) gp = 1;
     const FastDiv fint = FastDiv::make(S->nx >= 6 ? (uint32_t)(S->nx / 2 - 2) : 1u);
-    if (S->nz >= 2 * kS27MarchZ && tuning(LSB_TUNE_S27_MARCH) != 2) {
+    const int mode = tuning(LSB_TUNE_S27_MARCH);
+    if (mode == 0 && launch_stencil27_tile(K, x, b, y, flags, it, st))
+      return check_launch("stencil27_tile");
+    if (S->nz >= 2 * kS27MarchZ && mode != 2) {
       static const int occm = [] {
         int o = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, stencil27_march_kernel, kS27Threads, 0);

@@ -1236,32 +1236,47 @@ def test_grid_cycle_breakdown_and_jacobi(P, monkeypatch):
     assert np.max(np.abs(c1 - c0) / np.maximum(c0, 1e-300)) <= 1e-8
 
 
+@pytest.mark.parametrize("dims", [(12, 10, 70), (66, 17, 97), (64, 48, 40)])
+@pytest.mark.parametrize("coef", ["convdiff", "random"])
 @pytest.mark.parametrize("halo", [(1, 0), (0, 1), (1, 1)])
-def test_spmv27_march_on_slabs_bitwise(P, halo):
-    """The z-marching 27-point kernel on a z-slab with ghost planes (the
-    first chunk reads the lower ghost plane, the last the upper one):
-    bitwise the row-pair kernel's y (LSB_TUNE_S27_MARCH = 2)."""
+def test_spmv27_kernels_on_slabs_bitwise(P, halo, coef, dims):
+    """The TMA plane-tile 27-point kernel (default; its boundary-row CTAs and
+    the -1.0-coefficient negation path), the z-march and its generic variant
+    on z-slabs with ghost planes, ragged tiles (nx, ny not multiples of the
+    32 x 16 tile, nz not a multiple of the plane chunk) and residual form
+    b - A x: bitwise the row-pair kernel's y (LSB_TUNE_S27_MARCH = 2)."""
     from paper_1809_05805_b200 import _abi
-    from paper_1809_05805_b200.operators import StencilOperator, convdiff27
-    nx, ny, nz = 12, 10, 70
-    S = convdiff27(0, dims=(nx, ny, nz))
+    from paper_1809_05805_b200.operators import StencilMatrix, StencilOperator, convdiff27
+    nx, ny, nz = dims
+    rng = np.random.default_rng(5)
+    if coef == "convdiff":
+        S = convdiff27(0, dims=dims)
+    else:
+        S = StencilMatrix(dims, [((o % 3 - 1, (o // 3) % 3 - 1, o // 9 - 1),
+                                  float(rng.standard_normal())) for o in range(27)], "r27")
     z0 = 8 if halo[0] else 0
-    nzl = 40 if halo[1] else nz - z0
+    nzl = (nz - 8 - z0) if halo[1] else nz - z0
     op = StencilOperator(S, z0=z0, nz_local=nzl)
     plane = nx * ny
     n = plane * nzl
-    rng = np.random.default_rng(5)
     xpad = torch.as_tensor(rng.standard_normal(n + 2 * plane + 2)).cuda()
     xs = xpad[plane:plane + n]           # ghost planes either side
-    outs = []
+    bb = torch.as_tensor(rng.standard_normal(n)).cuda()
     lib = _abi.load()
-    for knob in (0, 2):
-        lib.lsb_set_tuning(_abi.TUNE_S27_MARCH, knob)
-        y = torch.empty(n, dtype=torch.float64, device="cuda")
-        op.apply(xs, y)
-        outs.append(_np(y))
-    lib.lsb_set_tuning(_abi.TUNE_S27_MARCH, 0)
-    assert np.array_equal(outs[0], outs[1])
+    try:
+        for b in (None, bb):
+            outs = []
+            for knob, zc in ((2, 0), (0, 0), (0, 7), (4, 0), (3, 0)):
+                lib.lsb_set_tuning(_abi.TUNE_S27_MARCH, knob)
+                lib.lsb_set_tuning(_abi.TUNE_S27_TILE_Z, zc)
+                y = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+                op.apply(xs, y, b=b)
+                outs.append(_np(y))
+            for o in outs[1:]:
+                assert np.array_equal(o, outs[0])
+    finally:
+        lib.lsb_set_tuning(_abi.TUNE_S27_MARCH, 0)
+        lib.lsb_set_tuning(_abi.TUNE_S27_TILE_Z, 0)
 
 
 @pytest.mark.parametrize("persist", ["1", "0"])
