@@ -373,7 +373,7 @@ stencil27_march_kernel(const StencilK K, FastDiv fint, const double* __restrict_
 // coefficients are exactly -1.0, so their products are exact negations
 // folded into the DADDs (the same bits as __dmul_rn(-1.0, x)): 7 DMUL + 26
 // DADD per interior row instead of 27 + 26.
-constexpr int kT27X = 32, kT27Y = 16;
+constexpr int kT27X = 32, kT27Y = 8;
 constexpr int kT27Threads = (kT27X / 2) * kT27Y;                  // 256: one row pair each
 // a tensor copy's inner start must be 16-byte aligned (an odd x start traps
 // with an illegal instruction -- tools/micro/tma3d.cu), so a smem row holds
@@ -382,7 +382,7 @@ constexpr int kT27RowD = kT27X + 4;
 constexpr int kT27PlaneB = kT27RowD * (kT27Y + 2) * 8;            // 5184 B per staged plane
 constexpr int kT27PlaneD = (kT27PlaneB + 127) / 128 * 128 / 8;    // 128-byte aligned slots
 constexpr int kT27Stages = 6;
-constexpr size_t kT27Smem = (size_t)kT27Stages * kT27PlaneD * 8 + 128 + kT27Stages * 8;
+constexpr size_t kT27Smem = (size_t)kT27Stages * kT27PlaneD * 8 + 128 + 2 * kT27Stages * 8;
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1,
                                             int c2, uint64_t* bar) {
@@ -460,7 +460,7 @@ __device__ __forceinline__ void stencil27_boundary_rows(const StencilK& K, const
 }
 
 template <bool NEG>
-__global__ void __launch_bounds__(kT27Threads, 2)
+__global__ void __launch_bounds__(kT27Threads, 4)
 stencil27_tile_kernel(const __grid_constant__ CUtensorMap tm, const StencilK K,
                       const double* __restrict__ x, const double* __restrict__ b,
                       double* __restrict__ y, lsb_flags* flags, int it, int zc, int tiles_x) {
@@ -475,6 +475,7 @@ stencil27_tile_kernel(const __grid_constant__ CUtensorMap tm, const StencilK K,
   extern __shared__ __align__(128) double t27_raw[];
   double* const t27_smem = t27_raw + ((128u - (smem_u32(t27_raw) & 127u)) & 127u) / 8u;
   uint64_t* const full = reinterpret_cast<uint64_t*>(t27_smem + kT27Stages * kT27PlaneD);
+  uint64_t* const empty = full + kT27Stages;   // slot read by all 8 warps
   const int tx = (int)blockIdx.x % tiles_x, ty = (int)blockIdx.x / tiles_x;
   const int z0 = ((int)blockIdx.y - 1) * zc, z1 = min(K.nz, z0 + zc);
   const int x0 = tx * kT27X, y0 = ty * kT27Y;
@@ -483,7 +484,10 @@ stencil27_tile_kernel(const __grid_constant__ CUtensorMap tm, const StencilK K,
   const int nload = z1 - z0 + 2;                           // planes z0-1 .. z1
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int s = 0; s < kT27Stages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < kT27Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kT27Threads / 32);
+    }
     mbar_fence_init();
   }
   __syncthreads();
@@ -505,17 +509,28 @@ stencil27_tile_kernel(const __grid_constant__ CUtensorMap tm, const StencilK K,
       d[l][1] = c.x; d[l][2] = c.y;
       d[l][3] = row[l * kT27RowD + 3];
     }
+    // a slot is read exactly once (the z-window then lives in registers):
+    // each warp releases it right away (arrive = release semantics)
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[k % kT27Stages]);
   };
-  // the slot of load t is free once every thread has read load t+2 and
-  // finished step t (the generic path reads nothing from shared memory)
-  auto release = [&](int t) {
-    __syncthreads();
-    if (threadIdx.x == 0 && t + kT27Stages < nload) issue(t + kT27Stages);
+  // no CTA barrier per plane: thread 0 refills the slot of load t-1 (read by
+  // every warp at its step t-3) with load t-1+S before reading its own plane
+  auto refill = [&](int t) {
+    const int j = t - 1;
+    if (threadIdx.x == 0 && j >= 0 && j + kT27Stages < nload) {
+      mbar_wait(&empty[j % kT27Stages], (unsigned)(j / kT27Stages) & 1u);
+      issue(j + kT27Stages);
+    }
   };
   const int64_t nx = K.nx, plane = (int64_t)K.nx * K.ny;
   bool bad = false;
   auto emit = [&](int iz, double y0v, double y1v) {
-    if (!isfinite(y0v) || !isfinite(y1v)) bad = true;
+    // non-finite test on the exponent bits (integer pipe; a DSETP would
+    // take FP64 issue slots from the row sums)
+    const unsigned e0 = (unsigned)__double2hiint(y0v) & 0x7ff00000u;
+    const unsigned e1 = (unsigned)__double2hiint(y1v) & 0x7ff00000u;
+    if ((e0 == 0x7ff00000u) | (e1 == 0x7ff00000u)) bad = true;
     const int64_t r = (int64_t)iz * plane + (int64_t)iy * nx + ix;
     double2 out;
     if (b) {
@@ -536,6 +551,7 @@ stencil27_tile_kernel(const __grid_constant__ CUtensorMap tm, const StencilK K,
   const bool xy_int = ix >= 1 && ix + 2 < K.nx && iy >= 1 && iy + 1 < K.ny;
   double A[3][4], B[3][4], Q[3][4];
   auto step = [&](const double (&m)[3][4], const double (&c)[3][4], double (&p)[3][4], int t) {
+    refill(t);
     read(p, t + 2);
     const int iz = z0 + t;
     if (xy_int && iz - 1 >= K.zlo && iz + 1 <= K.zhi) {
@@ -551,7 +567,6 @@ stencil27_tile_kernel(const __grid_constant__ CUtensorMap tm, const StencilK K,
       }
       emit(iz, np_row_sum_fixed<27>(q0), np_row_sum_fixed<27>(q1));
     }
-    release(t);
   };
   read(A, 0);
   read(B, 1);
