@@ -373,6 +373,9 @@ stencil27_march_kernel(const StencilK K, FastDiv fint, const double* __restrict_
 // coefficients are exactly -1.0, so their products are exact negations
 // folded into the DADDs (the same bits as __dmul_rn(-1.0, x)): 7 DMUL + 26
 // DADD per interior row instead of 27 + 26.
+#ifndef LSB_T27_STAGES
+#define LSB_T27_STAGES 6
+#endif
 constexpr int kT27X = 32, kT27Y = 8;
 constexpr int kT27Threads = (kT27X / 2) * kT27Y;                  // 256: one row pair each
 // a tensor copy's inner start must be 16-byte aligned (an odd x start traps
@@ -381,7 +384,7 @@ constexpr int kT27Threads = (kT27X / 2) * kT27Y;                  // 256: one ro
 constexpr int kT27RowD = kT27X + 4;
 constexpr int kT27PlaneB = kT27RowD * (kT27Y + 2) * 8;            // 5184 B per staged plane
 constexpr int kT27PlaneD = (kT27PlaneB + 127) / 128 * 128 / 8;    // 128-byte aligned slots
-constexpr int kT27Stages = 6;
+constexpr int kT27Stages = LSB_T27_STAGES;
 constexpr size_t kT27Smem = (size_t)kT27Stages * kT27PlaneD * 8 + 128 + 2 * kT27Stages * 8;
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1,
