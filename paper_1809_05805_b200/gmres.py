@@ -261,6 +261,41 @@ def clear_engine_cache():
     _ENGINE_CACHE.clear()
 
 
+class _BasisSnapshot:
+    """Device copy of what a history's lazy ``basis`` / ``hessenberg`` read
+    from its engine (the basis columns and R), so the engine can be reused
+    by the next solve while that history is still alive (a solve loop
+    `x, h = solve(...)` keeps the previous h until the call returns).  Same
+    interface as Engine.basis / Engine.hessenberg."""
+
+    def __init__(self, eng, ncols):
+        c = max(0, min(ncols, eng.Vstore.shape[0]))
+        self.n = eng.n
+        self.V = eng.Vstore[:c, eng.off:eng.off + eng.n].clone()
+        self.R = eng.R.clone()
+
+    def hessenberg(self, k):
+        R = self.R.cpu().numpy()
+        H = np.zeros((k + 1, k))
+        for j in range(k):
+            H[: j + 2, j] = R[: j + 2, j + 1]
+        return H
+
+    def basis(self, k, ncols):
+        B = np.zeros((self.n, k + 1))
+        c = min(ncols, k + 1, self.V.shape[0])
+        if c > 0:
+            B[:, :c] = self.V[:c].t().cpu().numpy()
+        return B
+
+
+# a live history's basis up to this size is copied on the device (a few
+# microseconds) so the cached engine is reused; above it a new engine is
+# built instead (its allocation and graph capture are then noise next to
+# the solve itself, and a second basis copy would double the footprint)
+_SNAPSHOT_MAX_BYTES = 1 << 28
+
+
 def _cached_engine(key, A):
     ent = _ENGINE_CACHE.get(key)
     if ent is None:
@@ -270,7 +305,12 @@ def _cached_engine(key, A):
         return None
     h = h_ref() if h_ref is not None else None
     if h is not None and h._stash is not None and h._basis is None:
-        return None
+        src, k, ncols = h._stash
+        if src is not eng:
+            return eng
+        if (min(ncols, k + 1) * eng.n + eng.R.numel()) * 8 > _SNAPSHOT_MAX_BYTES:
+            return None
+        h._stash = (_BasisSnapshot(eng, min(ncols, k + 1)), k, ncols)
     return eng
 
 

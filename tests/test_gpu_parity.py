@@ -1122,9 +1122,11 @@ def test_pinned_host_input_takes_one_dma(P):
 
 def test_repeated_solves_reuse_the_engine(P):
     """solve() on the same operator object and config reuses the engine
-    (storage + captured cycle graph) when the previous history no longer
-    holds it; histories are bitwise those of a fresh engine, and a history
-    still holding its lazy basis is never overwritten."""
+    (storage + captured cycle graph); histories are bitwise those of a fresh
+    engine, and a history still holding its lazy basis is never overwritten:
+    its basis and R are first copied on the device (_BasisSnapshot), so a
+    solve loop `x, h = solve(...)` -- which keeps the previous h alive
+    during the next call -- reuses the engine too."""
     from paper_1809_05805_b200 import gmres as gm
     gm.clear_engine_cache()
     A = P.gen_laplace2d(48)
@@ -1132,17 +1134,23 @@ def test_repeated_solves_reuse_the_engine(P):
     b2 = orc.rhs_random(A.n_rows, 7)
     cfg = P.GmresConfig(restart_m=20, max_restarts=50, rel_tol=1e-8, method="two_sync_cgs2")
     x1, h1 = P.solve(A, b1, config=cfg, diagnostics_every=0)
-    x2, h2 = P.solve(A, b2, config=cfg, diagnostics_every=0)    # h1 alive and unread: no reuse
-    assert h1._stash[0] is not h2._stash[0]
-    basis1 = h1.basis
-    h1.release()
-    h2.release()
-    x3, h3 = P.solve(A, b1, config=cfg, diagnostics_every=0)    # reuses
+    eng = h1._stash[0]
+    x2, h2 = P.solve(A, b2, config=cfg, diagnostics_every=0)    # h1 alive and unread: snapshot
+    assert h2._stash[0] is eng and isinstance(h1._stash[0], gm._BasisSnapshot)
+    basis1, hess1 = h1.basis, h1.hessenberg
+    x3, h3 = P.solve(A, b1, config=cfg, diagnostics_every=0)    # reuses again
     key_eng = next(iter(gm._ENGINE_CACHE.values()))[0]
-    assert h3._stash[0] is key_eng
+    assert h3._stash[0] is key_eng is eng
     assert np.array_equal(h3.implicit_curve(), h1.implicit_curve())
     assert h3.cycle_starts == h1.cycle_starts and np.array_equal(x3, x1)
     assert basis1 is not None and np.array_equal(h3.basis, basis1)
+    assert np.array_equal(h3.hessenberg, hess1)
+    # a fresh engine agrees bitwise
+    gm.clear_engine_cache()
+    x4, h4 = P.solve(A, b2, config=cfg, diagnostics_every=0)
+    assert h4._stash[0] is not eng
+    assert np.array_equal(x4, x2) and np.array_equal(h4.implicit_curve(), h2.implicit_curve())
+    assert np.array_equal(h4.basis, h2.basis)
     gm.clear_engine_cache()
 
 
