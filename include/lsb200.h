@@ -167,8 +167,9 @@ typedef struct lsb_arnoldi {
 #define LSB_TUNE_PERSIST_TIMEOUT_S 12  /* persistent cycle: a cluster handoff waits at most this many seconds (0: 30, < 0: unbounded), then marks the mapped report -1.0 and aborts */
 #define LSB_TUNE_GRID_OCC 13       /* grid cycle CTAs per SM (0: 1) */
 #define LSB_TUNE_GRID_TRACE 14     /* 1: lsb_cycle_grid accumulates per-phase ns (lsb_grid_trace) */
-#define LSB_TUNE_S27_MARCH 15      /* 27-point stencil: 0 auto (TMA plane-tile kernel), 2 row-pair kernel,
-                                     3 z-marching without its interior fast path, 4 z-marching (nz >= 32) */
+#define LSB_TUNE_S27_MARCH 15      /* 27-point stencil: 0 auto (TMA plane-tile kernel from 2^21 rows, else
+                                     row pairs), 2 row-pair kernel, 3 z-marching without its interior fast
+                                     path, 4 z-marching (nz >= 32), 5 plane-tile kernel at any size */
 #define LSB_TUNE_MGS1_GRID 16     /* lsb_mgs1_passes: 0 cooperative single launch when it fits, 2 per-pass launches */
 #define LSB_TUNE_S27_TILE_Z 17    /* 27-point plane-tile kernel: planes per CTA (0: 32) */
 #define LSB_TUNE_COUNT 18

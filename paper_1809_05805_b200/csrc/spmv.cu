@@ -18,6 +18,8 @@
 // own row in numpy's order.
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "tile.cuh"
 
 namespace lsb {
@@ -466,10 +468,11 @@ template <bool NEG>
 __global__ void __launch_bounds__(kT27Threads, 4)
 stencil27_tile_kernel(const __grid_constant__ CUtensorMap tm, const StencilK K,
                       const double* __restrict__ x, const double* __restrict__ b,
-                      double* __restrict__ y, lsb_flags* flags, int it, int zc, int tiles_x) {
+                      double* __restrict__ y, lsb_flags* flags, int it, int zc, int tiles_x,
+                      int nbnd) {
   if (gated_off(flags, it)) return;
   if (blockIdx.y == 0) {                 // the boundary rows (first, so they are not a tail)
-    stencil27_boundary_rows(K, x, b, y, flags, blockIdx.x, gridDim.x);
+    if ((int)blockIdx.x < nbnd) stencil27_boundary_rows(K, x, b, y, flags, blockIdx.x, nbnd);
     return;
   }
   // all shared memory dynamic, the plane slots 128-byte aligned by hand (the
@@ -623,16 +626,37 @@ static bool launch_stencil27_tile(const StencilK& K, const double* x, const doub
   for (int o = 0; o < 27; ++o)
     if (!box27_face_or_centre(o) && K.val[o] != -1.0) neg = false;
   const int tiles_x = (K.nx + kT27X - 1) / kT27X, tiles_y = (K.ny + kT27Y - 1) / kT27Y;
+  // plane chunk: the longest of 64/32/16 planes that still fills one wave
+  // of tile CTAs (4 per SM; at 256^3: 64 planes 0.0745 ms, 32 0.0757, 16 0.0784)
+  const int64_t txy = (int64_t)tiles_x * tiles_y, slots = 4LL * sm_count();
   int zc = tuning(LSB_TUNE_S27_TILE_Z);
-  if (zc <= 0) zc = 32;
+  if (zc <= 0) {
+    zc = 16;
+    for (int c : {64, 32})
+      if (txy * ((K.nz + c - 1) / c) >= slots) { zc = c; break; }
+  }
   const int nch = (K.nz + zc - 1) / zc;
-  const dim3 grid((unsigned)(tiles_x * tiles_y), (unsigned)nch + 1);   // y = 0: boundary rows
+  // boundary-row CTAs (grid row 0, dispatched first): as few as keep them
+  // off the critical path -- each holds a tile slot for the whole run, so
+  // 256 of them at 256^3 cost 5% (0.0784 vs 0.0743 ms with 64); their
+  // latency-bound gathers get ~32 row pairs per thread at 256^3, scaled
+  // with n (the tile phase's length), at least 4
+  const int64_t nxi = K.nx / 2 - 2, lyi = K.ny >= 2 ? K.ny - 2 : 0;
+  const int zb0 = K.zlo == 0 ? 0 : -1;
+  const int nzp = (zb0 >= 0) + ((K.zhi == K.nz - 1 && K.nz - 1 != zb0) ? 1 : 0);
+  const int64_t nbp = 2LL * K.ny * K.nz + (K.ny >= 2 ? 2 : 1) * (int64_t)K.nz * nxi +
+                      (int64_t)nzp * lyi * nxi;
+  const int64_t n = (int64_t)K.nx * K.ny * K.nz;
+  const int64_t ipt = std::max<int64_t>(4, (32 * n) >> 24);
+  const int64_t nb = std::min<int64_t>(txy, std::max<int64_t>(1, (nbp + kT27Threads * ipt - 1) /
+                                                                     (kT27Threads * ipt)));
+  const dim3 grid((unsigned)txy, (unsigned)nch + 1);   // y = 0: boundary rows
   if (neg)
     stencil27_tile_kernel<true><<<grid, kT27Threads, kT27Smem, st>>>(tm, K, x, b, y, flags, it,
-                                                                      zc, tiles_x);
+                                                                      zc, tiles_x, (int)nb);
   else
     stencil27_tile_kernel<false><<<grid, kT27Threads, kT27Smem, st>>>(tm, K, x, b, y, flags, it,
-                                                                       zc, tiles_x);
+                                                                       zc, tiles_x, (int)nb);
   return true;
 }
 
@@ -765,10 +789,15 @@ int launch_stencil(const lsb_stencil* S, const double* x, const double* b, doubl
     if (gp > (int64_t)sm_count() * occ27p) gp = (int64_t)sm_count() * occ27p;
     if (gp < 1) gp = 1;
     const FastDiv fint = FastDiv::make(S->nx >= 6 ? (uint32_t)(S->nx / 2 - 2) : 1u);
+    // auto: the TMA plane-tile kernel from 2^21 rows (128^3: 0.018 vs 0.023
+    // ms for the row pairs), the row-pair kernel below (64^3: 0.0093 vs
+    // 0.0133 tile, 0.0230 z-march); knob 4 forces the z-march, 2 row pairs
     const int mode = tuning(LSB_TUNE_S27_MARCH);
-    if (mode == 0 && launch_stencil27_tile(K, x, b, y, flags, it, st))
+    if (mode == 0 && n64 >= (1LL << 21) && launch_stencil27_tile(K, x, b, y, flags, it, st))
       return check_launch("stencil27_tile");
-    if (S->nz >= 2 * kS27MarchZ && mode != 2) {
+    if (mode == 5 && launch_stencil27_tile(K, x, b, y, flags, it, st))
+      return check_launch("stencil27_tile");
+    if (S->nz >= 2 * kS27MarchZ && (mode == 3 || mode == 4)) {
       static const int occm = [] {
         int o = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, stencil27_march_kernel, kS27Threads, 0);

@@ -1248,7 +1248,8 @@ def test_grid_cycle_breakdown_and_jacobi(P, monkeypatch):
 @pytest.mark.parametrize("coef", ["convdiff", "random"])
 @pytest.mark.parametrize("halo", [(1, 0), (0, 1), (1, 1)])
 def test_spmv27_kernels_on_slabs_bitwise(P, halo, coef, dims):
-    """The TMA plane-tile 27-point kernel (default; its boundary-row CTAs and
+    """The TMA plane-tile 27-point kernel (default from 2^21 rows, forced here
+    with LSB_TUNE_S27_MARCH = 5; its boundary-row CTAs and
     the -1.0-coefficient negation path), the z-march and its generic variant
     on z-slabs with ghost planes, ragged tiles (nx, ny not multiples of the
     32 x 16 tile, nz not a multiple of the plane chunk) and residual form
@@ -1274,7 +1275,7 @@ def test_spmv27_kernels_on_slabs_bitwise(P, halo, coef, dims):
     try:
         for b in (None, bb):
             outs = []
-            for knob, zc in ((2, 0), (0, 0), (0, 7), (4, 0), (3, 0)):
+            for knob, zc in ((2, 0), (5, 0), (5, 7), (0, 0), (4, 0), (3, 0)):
                 lib.lsb_set_tuning(_abi.TUNE_S27_MARCH, knob)
                 lib.lsb_set_tuning(_abi.TUNE_S27_TILE_Z, zc)
                 y = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
