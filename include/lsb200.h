@@ -197,6 +197,12 @@ int lsb_spmv_csr(const lsb_csr* A, const double* x, const double* b, double* y,
  * reduceat summation order).  Replaces the same kernels.py:256-272 call. */
 int lsb_spmv_csr_dict(const lsb_csr_dict* A, const double* x, const double* b, double* y,
                       lsb_flags* flags, int32_t it, void* stream);
+/* Matrix-free constant-coefficient stencil (the CSR a StencilMatrix stands
+ * for, kernels.py:256-272; bitwise lsb_spmv_csr on it).  x points at local
+ * plane 0; with halo_lo / halo_hi the ghost planes x - nx*ny and
+ * x + nz*nx*ny must be readable.  The 27-point box from 2^21 rows runs as
+ * TMA plane tiles (cp.async.bulk.tensor via cuTensorMapEncodeTiled from the
+ * driver entry point; LSB_TUNE_S27_MARCH picks the other kernels). */
 int lsb_spmv_stencil(const lsb_stencil* S, const double* x, const double* b, double* y,
                      lsb_flags* flags, int32_t it, void* stream);
 
