@@ -464,7 +464,7 @@ __device__ __forceinline__ void stencil27_boundary_rows(const StencilK& K, const
   if (bad && flags) flags->nonfinite = 1;
 }
 
-template <bool NEG>
+template <bool NEG, bool HASB>
 __global__ void __launch_bounds__(kT27Threads, 4)
 stencil27_tile_kernel(const __grid_constant__ CUtensorMap tm, const StencilK K,
                       const double* __restrict__ x, const double* __restrict__ b,
@@ -531,21 +531,24 @@ stencil27_tile_kernel(const __grid_constant__ CUtensorMap tm, const StencilK K,
   };
   const int64_t nx = K.nx, plane = (int64_t)K.nx * K.ny;
   bool bad = false;
+  unsigned emax = 0;
+  double* const yrow = y + (int64_t)iy * nx + ix;
+  const double* const brow = HASB ? b + (int64_t)iy * nx + ix : nullptr;
   auto emit = [&](int iz, double y0v, double y1v) {
     // non-finite test on the exponent bits (integer pipe; a DSETP would
-    // take FP64 issue slots from the row sums)
-    const unsigned e0 = (unsigned)__double2hiint(y0v) & 0x7ff00000u;
-    const unsigned e1 = (unsigned)__double2hiint(y1v) & 0x7ff00000u;
-    if ((e0 == 0x7ff00000u) | (e1 == 0x7ff00000u)) bad = true;
-    const int64_t r = (int64_t)iz * plane + (int64_t)iy * nx + ix;
+    // take FP64 issue slots from the row sums): the largest exponent field
+    // seen, compared once at the end (all ones = Inf/NaN)
+    emax = max(emax, max((unsigned)__double2hiint(y0v) & 0x7ff00000u,
+                         (unsigned)__double2hiint(y1v) & 0x7ff00000u));
+    const int64_t r = (int64_t)iz * plane;
     double2 out;
-    if (b) {
-      const double2 bb = __ldg(reinterpret_cast<const double2*>(b + r));
+    if (HASB) {      // residual form b - A x: a compile-time branch
+      const double2 bb = __ldg(reinterpret_cast<const double2*>(brow + r));
       out = make_double2(__dsub_rn(bb.x, y0v), __dsub_rn(bb.y, y1v));
     } else {
       out = make_double2(y0v, y1v);
     }
-    *reinterpret_cast<double2*>(y + r) = out;
+    *reinterpret_cast<double2*>(yrow + r) = out;
   };
   auto mul = [&](int o, double v) {
     if (NEG && !box27_face_or_centre(o)) return -v;
@@ -584,7 +587,7 @@ stencil27_tile_kernel(const __grid_constant__ CUtensorMap tm, const StencilK K,
     if (t + 2 >= nt) break;
     step(Q, A, B, t + 2);
   }
-  if (bad && flags) flags->nonfinite = 1;
+  if ((bad || emax == 0x7ff00000u) && flags) flags->nonfinite = 1;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (the
@@ -651,12 +654,13 @@ static bool launch_stencil27_tile(const StencilK& K, const double* x, const doub
   const int64_t nb = std::min<int64_t>(txy, std::max<int64_t>(1, (nbp + kT27Threads * ipt - 1) /
                                                                      (kT27Threads * ipt)));
   const dim3 grid((unsigned)txy, (unsigned)nch + 1);   // y = 0: boundary rows
+  auto go = [&](auto kern) {
+    kern<<<grid, kT27Threads, kT27Smem, st>>>(tm, K, x, b, y, flags, it, zc, tiles_x, (int)nb);
+  };
   if (neg)
-    stencil27_tile_kernel<true><<<grid, kT27Threads, kT27Smem, st>>>(tm, K, x, b, y, flags, it,
-                                                                      zc, tiles_x, (int)nb);
+    b ? go(stencil27_tile_kernel<true, true>) : go(stencil27_tile_kernel<true, false>);
   else
-    stencil27_tile_kernel<false><<<grid, kT27Threads, kT27Smem, st>>>(tm, K, x, b, y, flags, it,
-                                                                       zc, tiles_x, (int)nb);
+    b ? go(stencil27_tile_kernel<false, true>) : go(stencil27_tile_kernel<false, false>);
   return true;
 }
 

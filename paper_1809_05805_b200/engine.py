@@ -21,6 +21,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
+import threading
 
 import numpy as np
 import torch
@@ -72,6 +73,14 @@ def _timing_event():
 
 
 _REPORT = {}
+
+# capture_begin registers the graph with the device's default RNG generator,
+# whose graph-safe state tensors are created lazily; ranks emulated as
+# threads that begin their captures at the same moment raced on that
+# creation ("Expected a proper Tensor but got None", seen once in ~20 runs
+# of the threaded row-block tests).  The registration is serialised; the
+# captures themselves still run concurrently (thread-local capture mode).
+_CAPTURE_BEGIN_LOCK = threading.Lock()
 
 
 def _report_buffers(m):
@@ -668,7 +677,8 @@ class Engine:
                         # instantiation may wait for the device, which must
                         # not hold a kernel spinning on a rank still capturing
                         self.comm.barrier()
-                        self.graph.capture_begin(capture_error_mode="thread_local")
+                        with _CAPTURE_BEGIN_LOCK:
+                            self.graph.capture_begin(capture_error_mode="thread_local")
                         try:
                             self.enqueue_cycle()
                         finally:

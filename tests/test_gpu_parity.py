@@ -1288,6 +1288,39 @@ def test_spmv27_kernels_on_slabs_bitwise(P, halo, coef, dims):
         lib.lsb_set_tuning(_abi.TUNE_S27_TILE_Z, 0)
 
 
+@pytest.mark.parametrize("knob", [5, 2, 4])
+@pytest.mark.parametrize("where", ["interior", "x_edge", "z_edge"])
+@pytest.mark.parametrize("bad", [float("inf"), float("nan")])
+def test_spmv27_nonfinite_flag(P, knob, where, bad):
+    """A NaN/Inf in x reaches y and sets flags.nonfinite (kernels.py:271) in
+    every 27-point kernel: the plane-tile kernel's interior rows (deferred
+    exponent test) and its boundary-row CTAs, the z-march, the row pairs;
+    a finite x leaves the flag clear."""
+    from paper_1809_05805_b200 import _abi
+    from paper_1809_05805_b200.operators import StencilOperator, convdiff27
+    dims = (66, 20, 40)
+    op = StencilOperator(convdiff27(0, dims=dims))
+    n = dims[0] * dims[1] * dims[2]
+    lib = _abi.load()
+    try:
+        lib.lsb_set_tuning(_abi.TUNE_S27_MARCH, knob)
+        for poison in (False, True):
+            x = torch.ones(n, dtype=torch.float64, device="cuda")
+            if poison:
+                ix, iy, iz = {"interior": (31, 9, 17), "x_edge": (0, 9, 17),
+                              "z_edge": (31, 9, 0)}[where]
+                x[(iz * dims[1] + iy) * dims[0] + ix] = bad
+            flags = torch.tensor([_abi.NO_STOP, 0, -1, 0, 0, 0, 0, 0], dtype=torch.int32,
+                                 device="cuda")
+            y = torch.empty(n, dtype=torch.float64, device="cuda")
+            op.apply(x, y, flags=flags)
+            torch.cuda.synchronize()
+            assert int(flags[4]) == int(poison), (poison, where)
+            assert bool(torch.isfinite(y).all()) == (not poison)
+    finally:
+        lib.lsb_set_tuning(_abi.TUNE_S27_MARCH, 0)
+
+
 @pytest.mark.parametrize("persist", ["1", "0"])
 def test_zero_restarts_stalls_like_reference(P, monkeypatch, persist):
     """GmresConfig(max_restarts=0) is legal in the reference (gmres.py:87-103):
